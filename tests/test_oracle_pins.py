@@ -1,0 +1,369 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix
+(never against the oracle itself, never against the CUDA path).
+
+Each test names the passage or fact it pins; see DESIGN.md §Oracle pins."""
+import math
+import statistics
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import oracle as O
+import qmc_workloads as W
+from conftest import load_golden
+
+SMALL_PRIMES = [p for p in range(3, 102) if all(p % d for d in range(2, int(p ** 0.5) + 1))]
+
+
+# ---------------------------------------------------------------- worked example
+def test_worked_example_tables():
+    g = load_golden("worked_example_n7.json")
+    N = g["N"]
+    beta = O.primitive_root(N)
+    assert beta == g["beta"]
+    assert (beta * g["beta_inv"]) % N == 1
+    P = O.power_table(N, beta)
+    L = O.log_table(N, P)
+    c = O.column_exponents(g["g"], L)
+    assert list(c) == g["c"]
+
+
+def test_worked_example_points_and_factorisation():
+    g = load_golden("worked_example_n7.json")
+    N, z, beta, c = g["N"], g["g"], g["beta"], g["c"]
+    conv = O.lattice_index_matrix(N, z, np.arange(N))
+    assert conv.tolist() == g["conventional_numerators"]
+    reord = [O.reordered_lattice_point(N, beta, c, n).tolist() for n in range(N)]
+    assert reord == g["reordered_numerators"]
+    # Z (phi = identity, numerators over 7) and P as printed; Y' = Z P (Eq. ZPa)
+    zeta = O.power_table(N, beta).astype(float)              # z_k = {β^k/N}·N
+    Z = O.circulant_Z(zeta)
+    assert Z.astype(int).tolist() == g["Z_numerators"]
+    Psel = O.selection_P(c, N - 1)
+    assert Psel.astype(int).tolist() == g["P"]
+    assert (Z @ Psel).astype(int).tolist() == g["reordered_numerators"][1:]
+
+
+def test_worked_example_product_identity_phi():
+    """X = Y·a with the paper's printed conventional points, a = (7,7,7)."""
+    g = load_golden("worked_example_n7.json")
+    N = g["N"]
+    tab = O.phi_table(O.PHI_IDENTITY, N)
+    idx = O.lattice_index_matrix(N, g["g"], np.arange(N))
+    a = np.array([[7.0], [7.0], [7.0]])
+    X = O.oracle_X_rows(tab, idx, a)[:, 0]
+    printed = np.array(g["conventional_numerators"]).sum(axis=1)   # 7·(n_j/7)
+    np.testing.assert_allclose(X, printed, rtol=0, atol=1e-13)
+    assert np.round(X).astype(int).tolist() == [0, 9, 11, 6, 15, 10, 12]
+    # the same values in the paper's reordered order
+    spec = load_golden("spec_examples.json")
+    # reordered row i is conventional row n_i; since g_1 = 1 its first
+    # coordinate numerator is n_i itself
+    order = [0] + [r[0] for r in g["reordered_numerators"][1:]]
+    Xr = [X[0]] + [X[n] for n in order[1:]]
+    assert np.round(Xr).astype(int).tolist() == spec["matvec_reordered_a777"]
+    a1 = np.array([[1.0], [0.0], [0.0]])
+    X1 = O.oracle_X_rows(tab, idx, a1)[:, 0] * 7
+    assert np.round([X1[0]] + [X1[n] for n in order[1:]]).astype(int).tolist() == \
+        spec["matvec_reordered_a100_times7"]
+
+
+def test_spec_number_theory_examples():
+    spec = load_golden("spec_examples.json")
+    for b, e, n, want in spec["pow_mod"]:
+        P = O.power_table(n, b % n) if O.is_prime(n) else None
+        assert pow(b, e, n) == want
+        if P is not None and e < n - 1:
+            assert P[e] == want                            # repeated multiplication
+    for n, want in spec["primitive_root"]:
+        assert O.primitive_root(n) == want
+    for a, n, want in spec["mod_inverse"]:
+        assert (a * want) % n == 1
+    # scatter: c = (1,6,2), a -> (a1, a3, 0, 0, 0, a2)
+    c = spec["scatter_c"]
+    a = np.array([1.5, -2.0, 3.25])
+    sc = O.selection_P(c, 6) @ a
+    np.testing.assert_array_equal(sc, [1.5, 3.25, 0, 0, 0, -2.0])
+    # circulant first column
+    Z = O.circulant_Z(O.power_table(7, 3).astype(float))
+    assert Z[:, 0].astype(int).tolist() == spec["Z_first_column_times7"]
+
+
+# ---------------------------------------------------------------- number theory
+def _order(b, N):
+    k, v = 1, b % N
+    while v != 1:
+        v = (v * b) % N
+        k += 1
+    return k
+
+
+@pytest.mark.parametrize("N", SMALL_PRIMES)
+def test_primitive_root_brute_force(N):
+    beta = O.primitive_root(N)
+    assert _order(beta, N) == N - 1
+    assert all(_order(b, N) < N - 1 for b in range(2, beta))   # smallest (R1)
+    P = O.power_table(N, beta)
+    assert sorted(P.tolist()) == list(range(1, N))        # {β^k} = Z_N^*
+    L = O.log_table(N, P)
+    for r in range(1, N):                                  # brute-force discrete log
+        assert pow(beta, int(L[r]), N) == r
+    binv = pow(beta, N - 2, N)
+    assert _order(binv, N) == N - 1
+
+
+def test_config_primitive_roots():
+    g = load_golden("primitive_roots.json")
+    for Ns, want in g["roots"].items():
+        N = int(Ns)
+        assert O.primitive_root(N) == want
+        qs = O.prime_factors(N - 1)
+        assert all(pow(want, (N - 1) // q, N) != 1 for q in qs)
+    assert pow(3, 128, 257) == 256 and pow(3, 32768, 65537) == 65536   # Pépin
+    assert O.prime_factors(65535) == [3, 5, 17, 257]
+    assert O.prime_factors(786432) == [2, 3] and O.prime_factors(40960) == [2, 5]
+
+
+# ---------------------------------------------------------------- circulant invariance
+@pytest.mark.parametrize("N", [5, 7, 11, 13, 31, 61, 101])
+@pytest.mark.parametrize("phi", [O.PHI_IDENTITY, O.PHI_SHIFT_HALF, O.PHI_TENT, O.PHI_INVNORM_MID])
+def test_circulant_invariance_lattice(N, phi):
+    """Rows of the conventional Y, permuted to n_i = β^{-(i)}
+    and with row 0 dropped, equal Z·P (Eq. ZPa), where Z is
+    built from z_k = φ({β^k/N}).  z covers all of Z_N^* plus
+    random repeats (P may then hold several 1s per row, reading R18)."""
+    rng = np.random.default_rng(N)
+    z = np.concatenate([np.arange(1, N), rng.integers(1, N, size=7)])
+    beta = O.primitive_root(N)
+    tab = O.phi_table(phi, N)
+    Y = O.point_matrix_rows(tab, O.lattice_index_matrix(N, z, np.arange(N)))
+    binv = pow(beta, N - 2, N)
+    rows = [pow(binv, i, N) for i in range(N - 1)]         # n_i = β^{-i}, paper n = i+1
+    Yp = Y[rows, :]
+    zeta = tab[O.power_table(N, beta)]
+    c = O.column_exponents(z, O.log_table(N, O.power_table(N, beta)))
+    np.testing.assert_array_equal(Yp, O.circulant_Z(zeta) @ O.selection_P(c, N - 1))
+    # y_0 = (φ(0), ..., φ(0))
+    assert np.all(Y[0] == tab[0])
+
+
+@pytest.mark.parametrize("N", SMALL_PRIMES)
+def test_columns_are_permutations(N):
+    """Each column of Y is a permutation of {φ(i/N)} (gcd(z_j, N) = 1)."""
+    rng = np.random.default_rng(1000 + N)
+    z = rng.integers(1, N, size=5)
+    idx = O.lattice_index_matrix(N, z, np.arange(N))
+    for j in range(len(z)):
+        assert sorted(idx[:, j].tolist()) == list(range(N))
+
+
+# ---------------------------------------------------------------- closed forms on X
+@pytest.mark.parametrize("N,s,t", [(257, 300, 64), (65537, 64, 8), (40961, 128, 4)])
+def test_column_sum_closed_form(N, s, t):
+    """Σ_n {n z/N} = (N-1)/2 for gcd(z,N)=1 (north star; reading R8), so with
+    φ = u - 1/2: Σ_n Y[n,j] = -1/2 and Σ_n X[n,k] = -1/2 Σ_j A[j,k]."""
+    rng = np.random.default_rng(s)
+    z = rng.integers(1, N, size=s)
+    A = rng.standard_normal((s, t))
+    tab = O.phi_table(O.PHI_SHIFT_HALF, N)
+    X = O.oracle_X_full(lambda r: O.lattice_index_matrix(N, z, r), tab, N, A)
+    colsum = np.array([math.fsum(X[:, k]) for k in range(t)])
+    want = -0.5 * A.sum(axis=0)
+    bound = 1e-15 * N * np.abs(A).sum(axis=0) * 0.5 * 8
+    assert np.all(np.abs(colsum - want) <= bound + 1e-13)
+    # identity φ: Σ_n Y[n,j] = (N-1)/2 exactly
+    tabi = O.phi_table(O.PHI_IDENTITY, N)
+    Yi = O.point_matrix_rows(tabi, O.lattice_index_matrix(N, z[:3], np.arange(N)))
+    for j in range(3):
+        assert abs(math.fsum(Yi[:, j]) - (N - 1) / 2) < 1e-9
+
+
+def test_special_cases():
+    N, s = 101, 12
+    rng = np.random.default_rng(7)
+    z = rng.integers(1, N, size=s)
+    tab = O.phi_table(O.PHI_TENT, N)
+    idx = O.lattice_index_matrix(N, z, np.arange(N))
+    Y = O.point_matrix_rows(tab, idx)
+    # A = I gives X = Y
+    np.testing.assert_array_equal(O.oracle_X_rows(tab, idx, np.eye(s)), Y)
+    # all z equal: X[n,k] = φ({n z/N}) Σ_j A[j,k]
+    A = rng.standard_normal((s, 3))
+    zz = np.full(s, 17)
+    Xz = O.oracle_X_rows(tab, O.lattice_index_matrix(N, zz, np.arange(N)), A)
+    want = tab[(np.arange(N) * 17) % N][:, None] * A.sum(axis=0)[None, :]
+    np.testing.assert_allclose(Xz, want, rtol=0, atol=1e-13)
+    # row 0: φ(0) Σ_j a_j
+    X = O.oracle_X_rows(tab, idx, A)
+    np.testing.assert_allclose(X[0], tab[0] * A.sum(axis=0), atol=1e-14)
+
+
+def test_product_within_rounding_bound_exact_rational():
+    """φ = identity, integer A: exact rational Y·A vs the fp64 oracle, within
+    the fp64 dot-product error bound s·u·Σ|y||a|."""
+    N, s, t = 61, 40, 3
+    rng = np.random.default_rng(11)
+    z = rng.integers(1, N, size=s)
+    A = rng.integers(-50, 51, size=(s, t)).astype(float)
+    tab = O.phi_table(O.PHI_IDENTITY, N)
+    idx = O.lattice_index_matrix(N, z, np.arange(N))
+    X = O.oracle_X_rows(tab, idx, A)
+    Xf = O.oracle_X_rows_fsum(tab, idx, A)
+    for n in range(N):
+        for k in range(t):
+            exact = sum(Fraction(int((n * int(z[j])) % N), N) * int(A[j, k]) for j in range(s))
+            bound = s * 2.0 ** -53 * float(sum(abs(A[:, k]))) * 2
+            assert abs(float(exact) - X[n, k]) <= bound
+            assert abs(float(exact) - Xf[n, k]) <= 2e-14 * max(1.0, abs(float(exact)))
+
+
+# ---------------------------------------------------------------- φ = Φ^{-1}(u + 1/(2N))
+def test_invnorm_mid_round_trip_and_symmetry():
+    """Φ(φ(i/N)) = (2i+1)/(2N) with Φ(x) = erfc(-x/√2)/2 (an independent
+    routine), and the symmetry φ(i) = -φ(N-1-i)."""
+    for N in (7, 257, 65537):
+        tab = O.phi_table(O.PHI_INVNORM_MID, N)
+        ii = np.unique(np.linspace(0, N - 1, 200).astype(int))
+        for i in ii:
+            u = 0.5 * math.erfc(-tab[i] / math.sqrt(2.0))
+            assert abs(u - (2 * i + 1) / (2 * N)) <= 1e-14 * max(1.0, (2 * i + 1) / (2 * N)) + 1e-17
+        np.testing.assert_allclose(tab, -tab[::-1], rtol=0, atol=1e-12)
+    # R6: φ(0) values of configs 2 and 5
+    scipy_special = pytest.importorskip("scipy.special")
+    for N, want in ((65537, -4.324922404542677), (786433, -4.8441475519550155)):
+        v = statistics.NormalDist().inv_cdf(1.0 / (2 * N))
+        assert abs(v - want) < 1e-12
+        assert abs(v - scipy_special.ndtri(1.0 / (2 * N))) < 1e-12
+        assert O.phi_value(O.PHI_INVNORM_MID, 0, N) == v
+
+
+def test_phi_definitions():
+    """tent 1-|2x-1|, identity; shift u-1/2."""
+    N = 8
+    assert O.phi_value(O.PHI_TENT, 6, N) == 0.5           # tent(3/4) = 1/2
+    assert O.phi_value(O.PHI_TENT, 4, N) == 1.0           # tent(1/2) = 1
+    assert O.phi_value(O.PHI_TENT, 0, N) == 0.0
+    assert O.phi_value(O.PHI_SHIFT_HALF, 0, N) == -0.5
+    assert O.phi_value(O.PHI_IDENTITY, 3, N) == 3 / 8
+    assert O.phi_value(O.PHI_INVNORM_MID, 3, 7) == 0.0    # Φ^{-1}(1/2)
+
+
+# ---------------------------------------------------------------- F_2 polynomial lattice
+def _gf2_order_of_x(p, D):
+    v, k = 2, 1
+    while v != 1:
+        v <<= 1
+        if v >> D:
+            v ^= p
+        k += 1
+        if k > (1 << D):
+            return None
+    return k
+
+
+def test_gf2_smallest_primitive_brute_force():
+    g = load_golden("gf2_primitive.json")["smallest"]
+    for Ds, p in g.items():
+        D = int(Ds)
+        assert O.gf2_smallest_primitive(D) == p if D <= 8 else O.gf2_is_primitive(p, D)
+        assert _gf2_order_of_x(p, D) == (1 << D) - 1      # brute-force order of x
+        if D <= 8:   # every smaller candidate of degree D fails by brute force
+            for c in range((1 << D) | 1, p, 2):
+                assert _gf2_order_of_x(c, D) != (1 << D) - 1
+    assert O.gf2_smallest_primitive(16) == 65581
+
+
+@pytest.mark.parametrize("D", [2, 3, 4, 5, 6, 7, 8])
+def test_gf2_vd_index_is_polynomial_quotient(D):
+    """v_D(r/p)·2^D is the quotient of r(x)·x^D by p(x) (long division, an
+    independent algorithm from the digit recurrence), and is a bijection."""
+    p = O.gf2_smallest_primitive(D)
+    got = [O.gf2_vd_index(r, p, D) for r in range(1 << D)]
+    for r in range(1 << D):
+        q, _ = O.gf2_divmod(r << D, p)
+        assert got[r] == q
+    assert sorted(got) == list(range(1 << D))
+
+
+def test_gf2_index_matrix_vectorised_matches_scalar():
+    for D in (3, 5, 8):
+        p = O.gf2_smallest_primitive(D)
+        rng = np.random.default_rng(D)
+        q = rng.integers(1, 1 << D, size=9)
+        rows = np.arange(1 << D)
+        M = O.polylattice_index_matrix(D, p, q, rows)
+        for n in rows:
+            for j, qj in enumerate(q):
+                assert M[n, j] == O.gf2_vd_index(O.gf2_mulmod(int(n), int(qj), p), p, D)
+        for j in range(len(q)):                          # column = permutation
+            assert sorted(M[:, j].tolist()) == list(range(1 << D))
+    # D = 16 (config 4): permutation property on 3 columns
+    D, p = 16, 65581
+    M = O.polylattice_index_matrix(D, p, [1, 12345, 65535], np.arange(1 << D))
+    for j in range(3):
+        assert np.array_equal(np.sort(M[:, j]), np.arange(1 << D))
+
+
+@pytest.mark.parametrize("D", [2, 3, 4, 5, 6])
+def test_circulant_invariance_poly_all_primitive(D):
+    """Remark PAPER.md:456-459: the same factorisation holds for polynomial
+    lattices over F_2 with x as generator; exhaustive over every primitive p of
+    degree D and every nonzero q (reading R9)."""
+    m = (1 << D) - 1
+    prims = [p for p in range((1 << D) | 1, 1 << (D + 1), 2) if _gf2_order_of_x(p, D) == m]
+    assert prims
+    for p in prims:
+        q = np.arange(1, m + 1)
+        tab = O.phi_table(O.PHI_SHIFT_HALF, 1 << D)
+        Y = O.point_matrix_rows(tab, O.polylattice_index_matrix(D, p, q, np.arange(1 << D)))
+        P = O.gf2_power_table(p, D)
+        assert sorted(P.tolist()) == list(range(1, m + 1))
+        L = O.gf2_log_table(D, P)
+        # n_i = x^{-i}
+        rows = [int(P[(-i) % m]) for i in range(m)]
+        zeta = np.array([tab[O.gf2_vd_index(int(P[k]), p, D)] for k in range(m)])
+        c = L[q] + 1
+        np.testing.assert_array_equal(Y[rows, :], O.circulant_Z(zeta) @ O.selection_P(c, m))
+
+
+def test_lattice_and_poly_index_maps_agree_small():
+    """Both maps k -> β^k mod N and k -> x^k mod p are bijections onto the
+    nonzero residues whose inverse is the brute-force discrete log (R9)."""
+    for N in SMALL_PRIMES[:12]:
+        beta = O.primitive_root(N)
+        P = O.power_table(N, beta)
+        L = O.log_table(N, P)
+        for k in range(N - 1):
+            assert L[pow(beta, k, N)] == k
+    for D in range(2, 9):
+        p = O.gf2_smallest_primitive(D)
+        P = O.gf2_power_table(p, D)
+        L = O.gf2_log_table(D, P)
+        v = 1
+        for k in range((1 << D) - 1):
+            assert L[v] == k
+            v = O.gf2_mulmod(v, 2, p)
+
+
+# ---------------------------------------------------------------- inputs module
+def test_ar1_cholesky_closed_form_matches_lapack():
+    A = W.ar1_upper_cholesky(256, 102.4)
+    i = np.arange(256)
+    Sigma = np.exp(-np.abs(i[:, None] - i[None, :]) / 102.4)
+    np.testing.assert_allclose(A.T @ A, Sigma, atol=1e-13)
+    np.testing.assert_allclose(A, np.linalg.cholesky(Sigma).T, atol=1e-12)
+
+
+def test_config3_means_closed_form():
+    """mean_n(1 + X[n,k]) = 1 + S_φ/N·colsum_k = 1 - colsum_k/(2N) for φ = u-1/2
+    (reading R8), on two full columns of config 3."""
+    N, s = 40961, 4096
+    rng = np.random.default_rng(3)
+    z = rng.integers(1, N, size=s)
+    A = W.kl_sine_matrix(s, 65536, 2.0, 1.0, cols=[0, 40000])
+    tab = O.phi_table(O.PHI_SHIFT_HALF, N)
+    X = O.oracle_X_full(lambda r: O.lattice_index_matrix(N, z, r), tab, N, A, block=2048)
+    means = O.column_means(X, O.F_AFFINE, 1.0)
+    want = 1.0 - A.sum(axis=0) / (2 * N)
+    np.testing.assert_allclose(means, want, rtol=0, atol=1e-13)
