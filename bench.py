@@ -1,0 +1,405 @@
+#!/usr/bin/env python
+"""Benchmark of the fast QMC matrix product X = Y·A on B200 (one process per
+GPU; torchrun for N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+
+A step is one pass of the whole hot path over the configured workload
+(BASELINE.json configs[C-1], default C = 2, the config the metric is quoted
+on): qmc_mean (or qmc_matmul) over this rank's contiguous column slab, X
+written to HBM, plus the collective and finalize for the fused QMC mean.
+Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "fast Y·A output entries/s (fp64) and % HBM roofline at 1/2/4/8 B200"
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
+FP64_FMA_PER_CLK_PER_SM = 64   # B200: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz = 37.2 TFLOP/s
+N_SM = 148
+F_NAMES = {None: "none", 0: "identity_mean", 1: "affine_mean", 2: "exp_mean", 3: "rowmean_relu"}
+PHI_NAMES = {0: "identity", 1: "u-1/2", 2: "tent", 3: "invnorm(u+1/(2N))"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return dict(PEAKS_FALLBACK, source="fallback (B200_PROFILING.md)")
+
+
+# ----------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- CPU oracle (baseline)
+def cpu_oracle_rate(w, seconds: float, rows_per_block: int = 2048, seed: int = 0):
+    """Entries/s of the oracle (Y by φ-table gather + NumPy GEMM) on the
+    host, over row blocks for about `seconds`; the φ table build is excluded
+    (PAPER.md:800-801)."""
+    import numpy as np
+    import oracle as O
+    tab = O.phi_table(w.phi, w.N)
+    if w.family == "poly":
+        idx_fn = lambda r: O.polylattice_index_matrix(w.D, w.p, w.z, r)  # noqa: E731
+    else:
+        idx_fn = lambda r: O.lattice_index_matrix(w.N, w.z, r)  # noqa: E731
+    rng = np.random.default_rng(seed)
+    done, t0 = 0, time.perf_counter()
+    while True:
+        r0 = int(rng.integers(0, max(1, w.N - rows_per_block)))
+        rows = np.arange(r0, min(w.N, r0 + rows_per_block))
+        O.oracle_X_rows(tab, idx_fn(rows), w.A)
+        done += len(rows)
+        el = time.perf_counter() - t0
+        if el >= seconds or done >= w.N:
+            break
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        threads = os.cpu_count()
+    return done * w.t / el, done, el, threads
+
+
+def reference_arm(args, rank, world):
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0)."""
+    import numpy as np  # noqa: F401
+    import qmc_workloads as W
+    if rank != 0:
+        return
+    w = W.config(args.config)
+    rows = 1024
+    # warmup + timed steps, each a bounded sample of `rows` rows × all t columns
+    for _ in range(args.warmup):
+        cpu_oracle_rate(w, 0.0, rows_per_block=rows, seed=1)
+    t0 = time.perf_counter()
+    done = 0
+    for k in range(args.steps):
+        _, d, _, threads = cpu_oracle_rate(w, 0.0, rows_per_block=rows, seed=100 + k)
+        done += d
+    el = time.perf_counter() - t0
+    value = done * w.t / el
+    sample = f"{rows} random contiguous rows x all {w.t} columns per step (of N={w.N})"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": w.name, "N": w.N, "s": w.s, "t": w.t},
+        "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------- our arm
+def ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1501_06286_b200 as q
+    import qmc_workloads as W
+    from paper_1501_06286_b200 import _abi as abi
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    w = W.config(args.config)
+    G = world
+    if w.t % G:
+        raise SystemExit(f"t={w.t} not divisible by {G}")
+    tl = w.t // G
+    c0, c1 = rank * tl, (rank + 1) * tl
+    plan = q.Plan.from_workload(w, device=dev)
+    A_host = np.ascontiguousarray(w.A[:, c0:c1].T)          # (tl, s) row-major = A slab col-major
+    A = torch.from_numpy(A_host).to(dev).t()
+    X = q.colmajor_empty(w.N, tl, dev)
+    f, fp = w.f, w.f_param
+    N = w.N
+    if f == W.F_ROWMEAN_RELU:
+        out = torch.empty(N, dtype=torch.float64, device=dev)
+        res = torch.empty(1, dtype=torch.float64, device=dev)
+    elif f is not None:
+        out = torch.empty(tl, dtype=torch.float64, device=dev)
+        res = torch.empty(w.t, dtype=torch.float64, device=dev)
+    plan.call_workspace(tl, -1 if f is None else f)
+
+    def step():
+        if f is None:
+            plan.matmul(A, X)
+            return None
+        plan.mean(A, f, fp, X=X, out=out)
+        if f == W.F_ROWMEAN_RELU:
+            if G > 1:
+                dist.all_reduce(out)
+            plan.finalize(f, out, w.t, out=res)
+        else:
+            if G > 1:
+                dist.all_gather_into_tensor(res, out)     # zero-padded allreduce == allgather (R11)
+            else:
+                res.copy_(out)
+        return res
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    time.sleep(0.3)
+    abi.qmc_profile_read()
+    abi.qmc_profile_enable(True)
+    l0 = abi.qmc_launch_count()
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    for k in range(args.steps):
+        flush.zero_()                     # L2 flush between timed steps (untimed)
+        evs[k][0].record(stream)
+        step()
+        evs[k][1].record(stream)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    launches = abi.qmc_launch_count() - l0
+    abi.qmc_profile_enable(False)
+    prof = abi.qmc_profile_read()
+    clocks = sampler.stop()
+    ms_local = sum(a.elapsed_time(b) for a, b in evs)
+    t_ms = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if G > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms_total = float(t_ms.item())
+    ms_step = ms_total / args.steps
+    entries = N * w.t
+    value = entries * args.steps / (ms_total / 1e3)
+
+    # ---- roofline of the dominant kernel (per-class CUDA events, this rank)
+    peaks = load_peaks()
+    info = plan.info
+    L, L1, L2 = info["L"], info["L1"], info["L2"]
+    npairs = (tl + 1) // 2
+    kernels = {}
+    tot_prof = sum(v[1] for v in prof.values()) or 1.0
+    for name, (n, ms) in prof.items():
+        if n:
+            kernels[name] = {"launches": n, "ms_total": ms, "share": ms / tot_prof}
+    dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
+    dn, dms = kernels[dom]["launches"], kernels[dom]["ms_total"]
+    fp64_peak = N_SM * FP64_FMA_PER_CLK_PER_SM * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    if dom == "k_rows":
+        flops = args.steps * npairs * L1 * 2 * 5.0 * L2 * math.log2(L2)
+        achieved = flops / (dms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None, "kernel": dom,
+                "work": "algorithmic fp64 flops = 2 FFTs x 5 L2 log2 L2 per row-CTA",
+                "peak_source": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md)"}
+    elif dom == "k_cols":
+        flops = args.steps * npairs * L2 * 5.0 * L1 * math.log2(max(L1, 2))
+        achieved = flops / (dms / 1e3) / 1e12
+        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp64_peak, "traffic": None, "kernel": dom}
+    else:  # HBM-bound classes: algorithmic bytes
+        if dom == "k_gather":
+            nbytes = args.steps * (8.0 * N * tl + 4.0 * N * dn / args.steps)
+        elif dom == "k_pack":
+            nbytes = args.steps * 8.0 * w.s * tl
+        else:
+            nbytes = args.steps * 8.0 * tl
+        achieved = nbytes / (dms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom}
+    roof["launches"] = dn
+    roof["avg_launch_ms"] = dms / dn
+    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(traffic_file):
+        with open(traffic_file) as fh:
+            tf = json.load(fh).get(f"c{args.config}", {})
+        if dom in tf:
+            roof["traffic"] = tf[dom]
+    # whole-step HBM roofline (north star): compulsory bytes = read A + write X
+    step_bytes = 8.0 * (N + w.s) * w.t
+    hbm_ach = step_bytes / (ms_step / 1e3) / 1e9
+    hbm = {"bytes_per_step": step_bytes, "achieved_GBps": hbm_ach, "peak_GBps": peaks["hbm_gbs"],
+           "frac": hbm_ach / peaks["hbm_gbs"], "frac_vs_8TBps_nominal": hbm_ach / 8000.0,
+           "peak_source": peaks["source"]}
+
+    # ---- e2e: host buffers in, result back to host, through the C ABI
+    e2e = None
+    if G == 1:
+        A_pin = torch.from_numpy(A_host).pin_memory()
+        A_dev2 = torch.empty_like(A_pin, device=dev)
+        f_e2e = f if f is not None else W.F_IDENTITY
+        n_res = 1 if f_e2e == W.F_ROWMEAN_RELU else tl
+        out_pin = torch.empty(n_res, dtype=torch.float64).pin_memory()
+        out_dev = torch.empty(max(N, tl), dtype=torch.float64, device=dev)
+        ws = plan.call_workspace(tl, f_e2e)
+        st = stream.cuda_stream
+        def e2e_step():
+            abi.qmc_mean_host(plan.handle, A_pin, w.s, tl, f_e2e, fp, out_pin, A_dev2, X, N,
+                              out_dev, ws, ws.numel(), st)
+        for _ in range(max(1, args.warmup)):
+            e2e_step()
+        ee = []
+        for k in range(args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            e2e_step()
+            b.record(stream)
+            torch.cuda.synchronize()
+            ee.append(a.elapsed_time(b))
+        e_ms = sum(ee)
+        e2e = {"value": entries * args.steps / (e_ms / 1e3), "unit": "entries/s",
+               "h2d_bytes_per_step": int(A_pin.numel() * 8), "d2h_bytes_per_step": int(n_res * 8),
+               "ms_per_step": e_ms / args.steps, "api": "qmc_mean_host (C ABI, pinned host A)"}
+    else:
+        A_pin = torch.from_numpy(A_host).pin_memory()
+        A_dev2 = torch.empty_like(A_pin, device=dev)
+        ee = []
+        for k in range(args.warmup + args.steps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            A_dev2.copy_(A_pin, non_blocking=True)
+            r = step()
+            host = r.cpu() if r is not None else X[0, :1].cpu()
+            b.record(stream)
+            torch.cuda.synchronize()
+            if k >= args.warmup:
+                ee.append(a.elapsed_time(b))
+        t_e = torch.tensor([sum(ee)], dtype=torch.float64, device=dev)
+        dist.all_reduce(t_e, op=dist.ReduceOp.MAX)
+        e_ms = float(t_e.item())
+        e2e = {"value": entries * args.steps / (e_ms / 1e3), "unit": "entries/s",
+               "h2d_bytes_per_step": int(A_pin.numel() * 8),
+               "d2h_bytes_per_step": int(host.numel() * 8), "ms_per_step": e_ms / args.steps,
+               "api": "Plan.mean + torch.distributed (pinned host A slab per rank)"}
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        rate, rows, el, threads = cpu_oracle_rate(w, args.cpu_seconds)
+        cpu = {"value": rate, "unit": "entries/s", "cores": threads, "kind": "oracle",
+               "sample": f"{rows} of {w.N} rows x all {w.t} columns in {el:.1f} s "
+                         f"(phi-table gather + NumPy/OpenBLAS GEMM, host has {os.cpu_count()} cpus)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": w.name, "family": w.family, "N": N, "s": w.s, "t": w.t,
+                       "phi": PHI_NAMES[w.phi], "f": F_NAMES[w.f], "L": L, "L1": L1, "L2": L2,
+                       "batch_pairs": info["batch_pairs"], "parallelism": f"columns/{G}",
+                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
+            "roofline": roof, "hbm_roofline_step": hbm, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(launches), "clocks": clocks, "kernels": kernels,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    ours(args, rank, world, local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,178 @@
+/*
+ * qmc.h — C ABI of the B200-native fast QMC matrix product
+ *         X = Y·A  (Dick, Kuo, Le Gia, Schwab, "Fast QMC matrix-vector
+ *         multiplication", arXiv 1501.06286; text in PAPER.md).
+ *
+ * What is computed (§1): for QMC points y_0..y_{N-1}
+ * (rows of Y, N×s) and a dense fp64 matrix A (s×t), the product
+ *     X = Y·A,   X[n,k] = Σ_j Y[n,j]·A[j,k],
+ * with Y[n,j] = φ(x_{n,j}) the same univariate φ on every coordinate
+ * (PAPER.md:288-302), where x_n is either
+ *   - the rank-1 lattice point ({n z_1/N}, …, {n z_s/N}), N prime
+ *     (PAPER.md:243-253), or
+ *   - the polynomial-lattice point over F_2 with modulus p(x) primitive of
+ *     degree D, N = 2^D: x_{n,j} = v_D(n(x) q_j(x) mod p(x) / p(x))
+ *     (reading R3).
+ * Rows are returned in the CONVENTIONAL order n = 0..N-1 (reading R4).
+ *
+ * How (§2.1): with β a primitive element (the smallest,
+ * reading R1) and z_j = β^{c_j-1}, rows 1..N-1 in the reordered order
+ * factor as Y' = Z·P (Eq. ZPa), Z circulant of length
+ * m = N-1 (m = 2^D-1 for F_2).  Per column a of A the library scatter-adds
+ * a into m bins (a' = P a), computes Z a' by FFT
+ * (PAPER.md:358-362), fuses the un-permutation to conventional order and
+ * the row-0 term y_0·a = φ(0) Σ_j a_j, and optionally
+ * a downstream f and its QMC mean (1/N) Σ_n f(b_n) (PAPER.md:60-62,
+ * 154-157).  Every step runs in this library's CUDA kernels (sm_100a).
+ *
+ * Conventions for every entry point
+ *   - Return value: QMC_OK (0) or a negative QMC_E* code; qmc_strerror()
+ *     names it.  No exception crosses the ABI.  Invalid arguments are
+ *     detected on the host before anything is launched.
+ *   - Asynchrony: compute calls enqueue work on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream) and return; device
+ *     faults surface at the caller's next synchronisation.  qmc_plan_create*
+ *     and qmc_plan_tables synchronise `stream` before returning.
+ *   - Memory: "device" pointers are CUDA device memory on the current
+ *     device, owned by the caller; the library never allocates device
+ *     memory.  The plan handle is a small host object owned by the caller
+ *     (free with qmc_plan_destroy); it references plan_ws, which must
+ *     outlive it.  A plan is immutable after creation; concurrent calls on
+ *     one plan are safe if each uses its own call workspace.
+ *   - Layouts: A is column-major s×t with leading dimension lda >= s
+ *     (column k at A + k*lda); X is column-major N×t with ldx >= N.  A
+ *     column shard is a pointer offset.
+ */
+#ifndef QMC_H
+#define QMC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct qmc_plan* qmc_plan_t;
+
+/* point-set family */
+enum { QMC_FAMILY_LATTICE = 0, QMC_FAMILY_POLY = 1 };
+
+/* φ: the univariate transform applied to every coordinate.
+ * IDENTITY φ(u)=u; SHIFT_HALF φ(u)=u-1/2; TENT φ(u)=1-|2u-1|;
+ * INVNORM_MID φ(u)=Φ^{-1}(u + 1/(2N)) — the paper's Φ^{-1} with the equal
+ * shift Δ=1/(2N) it allows, finite at u=0 (reading R6).
+ * Plain Φ^{-1} is not offered: Φ^{-1}(0) = -inf at row 0. */
+enum { QMC_PHI_IDENTITY = 0, QMC_PHI_SHIFT_HALF = 1, QMC_PHI_TENT = 2, QMC_PHI_INVNORM_MID = 3 };
+
+/* fused downstream functional for qmc_mean (PAPER.md:60-62 eq_qmc) */
+enum {
+  QMC_F_IDENTITY = 0,      /* out[k] = (1/N) Σ_n X[n,k]                       */
+  QMC_F_AFFINE = 1,        /* out[k] = (1/N) Σ_n (c + X[n,k]); X receives c+X  */
+  QMC_F_EXP = 2,           /* out[k] = (1/N) Σ_n exp(X[n,k]); X receives X     */
+  QMC_F_ROWMEAN_RELU = 3   /* out[n] = Σ_k X[n,k] over the local columns (N
+                              partial row sums); qmc_mean_finalize then gives
+                              Q = (1/N) Σ_n max(0, r_n / t_total) (reading R10) */
+};
+
+/* status codes */
+enum {
+  QMC_OK = 0,
+  QMC_EINVAL_N = -1,      /* N not prime / out of range / unsupported length  */
+  QMC_EINVAL_Z = -2,      /* z_j not in [1, N-1] (q_j not in [1, 2^D-1])      */
+  QMC_EINVAL_POLY = -3,   /* p not of degree D, or not primitive              */
+  QMC_EINVAL_DIM = -4,    /* s < 1, t < 0, lda < s, ldx < N                   */
+  QMC_EINVAL_PHI = -5,    /* unknown φ                                        */
+  QMC_ENULL = -6,         /* required pointer is NULL                         */
+  QMC_ECUDA = -7,         /* CUDA launch / runtime error                      */
+  QMC_EWORKSPACE = -8,    /* workspace too small or misaligned (256 B)        */
+  QMC_EINVAL_F = -9       /* unknown f                                        */
+};
+
+/* Bytes of device memory the plan needs (plan_ws).  family/N_or_D/s as in
+ * qmc_plan_create / qmc_plan_create_poly.  Validates N (or D) and s. */
+int qmc_plan_workspace_size(int family, int64_t N_or_D, int64_t s, size_t* plan_bytes);
+
+/* Bytes of device scratch one qmc_matmul / qmc_mean call on t columns
+ * needs (call_ws).  Independent of A and X. */
+int qmc_call_workspace_size(qmc_plan_t plan, int64_t t, int f, size_t* call_bytes);
+
+/* Rank-1 lattice plan.  N prime, 3 <= N < 2^31;
+ * z_host: s host int64 values, each in [1, N-1] (repeats allowed,
+ * reading R18).  Builds on the device, in plan_ws (256-B aligned, at least
+ * qmc_plan_workspace_size bytes): β (smallest primitive root, R1), the power
+ * table P[k] = β^k mod N, the log table L (L[P[k]] = k, L[0] = -1), e_j =
+ * c_j - 1 = L[z_j], the circulant base ζ_k = φ(P[k]/N)
+ * and the spectrum of Z.  Synchronises `stream`.  On error *out is NULL. */
+int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
+                    void* plan_ws, size_t plan_ws_bytes, void* stream);
+
+/* Polynomial lattice over F_2 (PAPER.md:456-459 Remark; reading R2/R3):
+ * p has bit D set, 2 <= D <= 24, and must be primitive (checked on the
+ * device: x has order 2^D-1); q_host: s values in [1, 2^D-1] (integer
+ * encoding, bit i = coefficient of x^i).  N = 2^D points, m = 2^D-1. */
+int qmc_plan_create_poly(qmc_plan_t* out, int D, uint64_t p, int64_t s, const int64_t* q_host,
+                         int phi, void* plan_ws, size_t plan_ws_bytes, void* stream);
+
+/* X = Y·A (device pointers).  t >= 0 columns; t = 0 is a no-op. */
+int qmc_matmul(qmc_plan_t plan, const double* A, int64_t lda, int64_t t, double* X, int64_t ldx,
+               void* call_ws, size_t call_ws_bytes, void* stream);
+
+/* X = Y·A fused with f and the QMC mean.  out (device): t doubles for
+ * IDENTITY/AFFINE/EXP (complete means of the local columns), N doubles for
+ * ROWMEAN_RELU (partial row sums over the local columns).  X_or_null: if not
+ * NULL, X (or c + X for AFFINE) is written as in qmc_matmul. */
+int qmc_mean(qmc_plan_t plan, const double* A, int64_t lda, int64_t t, int f, double f_param,
+             double* out, double* X_or_null, int64_t ldx, void* call_ws, size_t call_ws_bytes,
+             void* stream);
+
+/* After the (optional, caller-side) allreduce of qmc_mean's out over column
+ * shards.  ROWMEAN_RELU: out[0] = (1/N) Σ_n max(0, reduced[n]/t_total), a
+ * fixed-order device reduction.  Other f: copies the t_total means
+ * (reduced → out, may alias).  Device pointers. */
+int qmc_mean_finalize(qmc_plan_t plan, int f, const double* reduced, int64_t t_total, double* out,
+                      void* stream);
+
+/* End-to-end entry with HOST buffers: copies A_host (pinned or pageable,
+ * column-major s×t, lda) into A_dev (device, s*t doubles, ld = s), runs
+ * qmc_mean (+ finalize), and copies the result to out_host (1 double for
+ * ROWMEAN_RELU, else t doubles); X_dev (device, ldx) receives X.  out_dev
+ * (device) must hold max(N, t) doubles.  Synchronises `stream`. */
+int qmc_mean_host(qmc_plan_t plan, const double* A_host, int64_t lda, int64_t t, int f,
+                  double f_param, double* out_host, double* A_dev, double* X_dev, int64_t ldx,
+                  double* out_dev, void* call_ws, size_t call_ws_bytes, void* stream);
+
+/* Plan facts: info[0..11] = family, N, m, s, phi, generator (β or the
+ * encoding of x = 2), L (FFT length; L = m or padded L >= 2m-1), L1, L2,
+ * pairs per batch, D, p.  Host pointer, >= 12 int64. */
+int qmc_plan_info(qmc_plan_t plan, int64_t* info);
+
+/* D2H copies of the plan tables for bit-exact tests (host buffers; any may
+ * be NULL): gen[1]; P[m] (β^k mod N or x^k mod p); L[N] (L[0] = -1);
+ * e[s] (e_j = c_j - 1); zeta[m] (ζ_k).  Synchronises the plan's stream. */
+int qmc_plan_tables(qmc_plan_t plan, int64_t* gen, int32_t* P, int32_t* L, int32_t* e,
+                    double* zeta);
+
+/* Kernels this library has launched since it was loaded (all entry points). */
+int64_t qmc_launch_count(void);
+
+/* Per-kernel-class timing for roofline reporting.  qmc_profile_enable(1)
+ * makes every later hot-path call record CUDA events on its stream around
+ * each launch class (k_pack, k_rows, k_cols, k_gather, k_colmean_reduce,
+ * k_finalize — qmc_profile_class_name(i) for i = 0..5).  qmc_profile_read
+ * waits for those events and returns, per class i < n, the number of
+ * timed launches (one "launch" of k_rows = the launch for one batch) and
+ * their summed device time in ms (host arrays of n entries); it then clears
+ * the record.  Not thread-safe; for benchmarking only. */
+int qmc_profile_enable(int on);
+int qmc_profile_read(int64_t* launches, double* ms, int n);
+const char* qmc_profile_class_name(int i);
+
+void qmc_plan_destroy(qmc_plan_t plan);
+const char* qmc_strerror(int code);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QMC_H */

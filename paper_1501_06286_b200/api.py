@@ -1,0 +1,121 @@
+"""Python face of libqmc: a `Plan` that owns its device workspaces (torch
+tensors — PyTorch supplies device memory and streams only) and forwards to
+the C ABI.  Argument marshalling only; every step of X = Y·A runs in the
+library's CUDA kernels.
+
+Layouts: A is (s, t) column-major (``A.stride(0) == 1``), X is (N, t)
+column-major, both fp64 CUDA tensors.  ``colmajor`` / ``to_device_colmajor``
+build such tensors.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _abi as abi
+
+
+def colmajor_empty(rows: int, cols: int, device, dtype=torch.float64) -> torch.Tensor:
+    return torch.empty((cols, rows), dtype=dtype, device=device).t()
+
+
+def to_device_colmajor(A: np.ndarray, device) -> torch.Tensor:
+    """Host (s, t) array -> device (s, t) column-major fp64 tensor (same bits)."""
+    At = np.ascontiguousarray(np.asarray(A, dtype=np.float64).T)
+    return torch.from_numpy(At).to(device).t()
+
+
+def _ld(x: torch.Tensor, rows: int) -> int:
+    if x.dtype != torch.float64:
+        raise TypeError("fp64 tensors required")
+    if x.dim() != 2 or x.shape[0] != rows:
+        raise ValueError(f"expected ({rows}, t), got {tuple(x.shape)}")
+    if x.shape[1] > 1 and x.stride(0) != 1:
+        raise ValueError("column-major (stride(0) == 1) tensor required")
+    return max(x.stride(1), rows) if x.shape[1] > 1 else rows
+
+
+def _stream(device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+class Plan:
+    """Fast QMC point-matrix operator Y (N × s) for one device."""
+
+    def __init__(self, family: int, N_or_D: int, z, phi: int, p: int = 0, device=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("libqmc needs a CUDA device (no CPU fallback)")
+        self.device = torch.device(device if device is not None else "cuda")
+        z = np.asarray(z, dtype=np.int64)
+        self.s = int(len(z))
+        nbytes = abi.qmc_plan_workspace_size(family, N_or_D, self.s)
+        self.plan_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            st = _stream(self.device)
+            if family == abi.QMC_FAMILY_LATTICE:
+                self.handle = abi.qmc_plan_create(N_or_D, self.s, z, phi, self.plan_ws, nbytes, st)
+            else:
+                self.handle = abi.qmc_plan_create_poly(N_or_D, p, self.s, z, phi, self.plan_ws, nbytes, st)
+        self.info = abi.qmc_plan_info(self.handle)
+        self.N, self.m, self.phi = self.info["N"], self.info["m"], phi
+        self._ws = None
+
+    @classmethod
+    def lattice(cls, N: int, z, phi: int, device=None) -> "Plan":
+        return cls(abi.QMC_FAMILY_LATTICE, N, z, phi, device=device)
+
+    @classmethod
+    def poly(cls, D: int, p: int, q, phi: int, device=None) -> "Plan":
+        return cls(abi.QMC_FAMILY_POLY, D, q, phi, p=p, device=device)
+
+    @classmethod
+    def from_workload(cls, w, device=None) -> "Plan":
+        if w.family == "poly":
+            return cls.poly(w.D, w.p, w.z, w.phi, device)
+        return cls.lattice(w.N, w.z, w.phi, device)
+
+    def call_workspace(self, t: int, f: int = abi.QMC_F_NONE) -> torch.Tensor:
+        nbytes = abi.qmc_call_workspace_size(self.handle, t, f)
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    def matmul(self, A: torch.Tensor, X: torch.Tensor | None = None) -> torch.Tensor:
+        lda = _ld(A, self.s)
+        t = A.shape[1]
+        if X is None:
+            X = colmajor_empty(self.N, t, self.device)
+        ldx = _ld(X, self.N)
+        ws = self.call_workspace(t)
+        abi.qmc_matmul(self.handle, A, lda, t, X, ldx, ws, ws.numel(), _stream(self.device))
+        return X
+
+    def mean(self, A: torch.Tensor, f: int, f_param: float = 0.0, X: torch.Tensor | None = None,
+             out: torch.Tensor | None = None) -> torch.Tensor:
+        lda = _ld(A, self.s)
+        t = A.shape[1]
+        n_out = self.N if f == abi.QMC_F_ROWMEAN_RELU else t
+        if out is None:
+            out = torch.empty(max(n_out, 1), dtype=torch.float64, device=self.device)
+        ldx = _ld(X, self.N) if X is not None else self.N
+        ws = self.call_workspace(t, f)
+        abi.qmc_mean(self.handle, A, lda, t, f, f_param, out, X, ldx, ws, ws.numel(),
+                     _stream(self.device))
+        return out
+
+    def finalize(self, f: int, reduced: torch.Tensor, t_total: int,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+        if out is None:
+            out = torch.empty(1 if f == abi.QMC_F_ROWMEAN_RELU else t_total, dtype=torch.float64,
+                              device=self.device)
+        abi.qmc_mean_finalize(self.handle, f, reduced, t_total, out, _stream(self.device))
+        return out
+
+    def tables(self):
+        return abi.qmc_plan_tables(self.handle, self.m, self.N, self.s)
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None:
+            abi.qmc_plan_destroy(h)
+            self.handle = None

@@ -1,0 +1,632 @@
+// plan.cu — plan construction of libqmc: host validation and the integer /
+// spectral plan kernels (sm_100a).
+//
+//   a0  validate N prime (or p of degree D), factor m            host
+//   a0  β = smallest primitive root (R1)      k_find_generator
+//       or check x generates F_2[x]/p (p primitive, R2)          k_check_poly
+//   a1  P[k] = β^k mod N  /  x^k mod p      k_pow_table
+//   a2  L[P[k]] = k, L[0] = -1      k_log_table
+//   a3  e_j = L[z_j] = c_j - 1; buckets by e_j mod L2           k_colmap, k_buckets
+//       R[n] = (m - L[n]) mod m  (conventional row n is reordered row R[n])
+//   a4  ζ_k = φ(u(P[k])); W = DFT_L(K)/L     k_zeta, k_spectrum_rows
+//
+// The plan is excluded from the paper's timings and from
+// bench.py's timed region.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <vector>
+
+#include "fft.cuh"
+#include "qmc_internal.cuh"
+
+namespace qmc {
+
+std::atomic<int64_t> g_launches{0};
+
+// ------------------------------------------------------------------ profiling
+namespace {
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev[KC_COUNT];
+  cudaEvent_t open[KC_COUNT] = {};
+  cudaEvent_t get() {
+    if (!pool.empty()) {
+      cudaEvent_t e = pool.back();
+      pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+Prof g_prof;
+}  // namespace
+
+void prof_begin(int kc, cudaStream_t st) {
+  if (!g_prof.on) return;
+  cudaEvent_t e = g_prof.get();
+  cudaEventRecord(e, st);
+  g_prof.open[kc] = e;
+}
+
+void prof_end(int kc, cudaStream_t st) {
+  if (!g_prof.on || !g_prof.open[kc]) return;
+  cudaEvent_t e = g_prof.get();
+  cudaEventRecord(e, st);
+  g_prof.ev[kc].push_back({g_prof.open[kc], e});
+  g_prof.open[kc] = nullptr;
+}
+
+// ------------------------------------------------------------------ host
+static bool host_is_prime(int64_t n) {
+  if (n < 2) return false;
+  if (n % 2 == 0) return n == 2;
+  for (int64_t d = 3; d * d <= n; d += 2)
+    if (n % d == 0) return false;
+  return true;
+}
+
+static std::vector<int64_t> host_prime_factors(int64_t m) {
+  std::vector<int64_t> q;
+  for (int64_t d = 2; d * d <= m; ++d)
+    if (m % d == 0) {
+      q.push_back(d);
+      while (m % d == 0) m /= d;
+    }
+  if (m > 1) q.push_back(m);
+  return q;
+}
+
+static bool smooth235(int64_t x) {
+  for (int q : {2, 3, 5})
+    while (x % q == 0) x /= q;
+  return x == 1;
+}
+
+bool choose_split(int64_t m, int64_t s, Split* out) {
+  const int64_t cap = s > 4096 ? 8192 : 4096;
+  auto try_len = [&](int64_t len) -> bool {
+    int64_t l2 = 1;
+    while (len % (l2 * 2) == 0 && l2 * 2 <= cap) l2 *= 2;
+    if (l2 < 16) return false;
+    int64_t l1 = len / l2;
+    if (l1 > 1024 || !smooth235(l1)) return false;
+    out->L = len;
+    out->L1 = l1;
+    out->L2 = l2;
+    return true;
+  };
+  if (m >= 64 && try_len(m)) {
+    out->padded = false;
+    return true;
+  }
+  for (int64_t len = 2 * m - 1; len <= (int64_t(1) << 26); ++len)
+    if (smooth235(len) && try_len(len)) {
+      out->padded = true;
+      return true;
+    }
+  return false;
+}
+
+PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
+  PlanLayout l;
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  l.off_scal = take(16 * 8);
+  l.off_P = take(size_t(m) * 4);
+  l.off_L = take(size_t(N) * 4);
+  l.off_R = take(size_t(N) * 4);
+  l.off_e = take(size_t(s) * 4);
+  l.off_bstart = take(size_t(sp.L2 + 1) * 4);
+  l.off_bidx = take(size_t(s) * 4);
+  l.off_be1 = take(size_t(s) * 4);
+  l.off_zeta = take(size_t(m) * 8);
+  l.off_W = take(size_t(sp.L) * 16);
+  l.off_tw1 = take(size_t(sp.L1) * 16);
+  l.off_tw2 = take(size_t(sp.L2) * 16);
+  l.off_twL = take(size_t(sp.L2) * 16);
+  l.off_radix1 = take(24 * 4);
+  l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
+  l.total = o;
+  return l;
+}
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint64_t mulmod(uint64_t a, uint64_t b, uint64_t n) { return (a * b) % n; }
+
+__device__ uint64_t powmod(uint64_t b, uint64_t e, uint64_t n) {
+  uint64_t r = 1 % n;
+  b %= n;
+  while (e) {
+    if (e & 1) r = mulmod(r, b, n);
+    b = mulmod(b, b, n);
+    e >>= 1;
+  }
+  return r;
+}
+
+// a·b mod p in F_2[x], deg a, deg b < D (Horner, keeps the partial < 2^D)
+__device__ __forceinline__ uint64_t gf2_mulmod(uint64_t a, uint64_t b, uint64_t p, int D) {
+  uint64_t r = 0;
+  for (int i = D - 1; i >= 0; --i) {
+    r <<= 1;
+    if ((r >> D) & 1) r ^= p;
+    if ((b >> i) & 1) r ^= a;
+  }
+  return r;
+}
+
+__device__ uint64_t gf2_powmod(uint64_t b, uint64_t e, uint64_t p, int D) {
+  uint64_t r = 1;
+  while (e) {
+    if (e & 1) r = gf2_mulmod(r, b, p, D);
+    b = gf2_mulmod(b, b, p, D);
+    e >>= 1;
+  }
+  return r;
+}
+
+// 2^D · v_D(r/p): digits of r(x)/p(x) by long division (reading R3)
+__device__ __forceinline__ int64_t gf2_vd_index(uint64_t r, uint64_t p, int D) {
+  uint64_t idx = 0;
+  for (int i = 0; i < D; ++i) {
+    uint64_t t = (r >> (D - 1)) & 1;
+    r = (r << 1) ^ (t ? p : 0);
+    idx = (idx << 1) | t;
+  }
+  return int64_t(idx);
+}
+
+// φ(i/N) (INVNORM_MID per reading R6)
+__device__ __forceinline__ double phi_eval(int phi, int64_t i, int64_t N) {
+  const double u = double(i) / double(N);
+  switch (phi) {
+    case QMC_PHI_IDENTITY: return u;
+    case QMC_PHI_SHIFT_HALF: return u - 0.5;
+    case QMC_PHI_TENT: return 1.0 - fabs(2.0 * u - 1.0);
+    default: return normcdfinv(double(2 * i + 1) / double(2 * N));
+  }
+}
+
+// ------------------------------------------------------------------ plan kernels
+__global__ void k_find_generator(int64_t N, int64_t base, const int64_t* __restrict__ qf, int nq,
+                                 unsigned long long* best) {
+  const int64_t beta = base + blockIdx.x * blockDim.x + threadIdx.x;
+  if (beta >= N) return;
+  const uint64_t m = uint64_t(N - 1);
+  for (int i = 0; i < nq; ++i)
+    if (powmod(uint64_t(beta), m / uint64_t(qf[i]), uint64_t(N)) == 1) return;
+  atomicMin(best, (unsigned long long)beta);
+}
+
+// flags bit0: x^m != 1; bit1: some x^{m/q} == 1  (p primitive iff flags == 0)
+__global__ void k_check_poly(uint64_t p, int D, const int64_t* __restrict__ qf, int nq,
+                             unsigned long long* flags) {
+  const int i = threadIdx.x;
+  const uint64_t m = (uint64_t(1) << D) - 1;
+  if (i == 0) {
+    if (gf2_powmod(2, m, p, D) != 1) atomicOr(flags, 1ull);
+  } else if (i <= nq) {
+    if (gf2_powmod(2, m / uint64_t(qf[i - 1]), p, D) == 1) atomicOr(flags, 2ull);
+  }
+}
+
+__global__ void k_pow_table(int family, int64_t N, uint64_t p, int D, int64_t gen, int64_t m,
+                            int32_t* __restrict__ P) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= m) return;
+  P[k] = family == QMC_FAMILY_LATTICE ? int32_t(powmod(uint64_t(gen), uint64_t(k), uint64_t(N)))
+                                      : int32_t(gf2_powmod(2, uint64_t(k), p, D));
+}
+
+__global__ void k_fill_i32(int32_t* __restrict__ a, int64_t n, int32_t v) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) a[i] = v;
+}
+
+__global__ void k_log_scatter(const int32_t* __restrict__ P, int64_t m, int32_t* __restrict__ L) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k < m) L[P[k]] = int32_t(k);
+}
+
+__global__ void k_colmap(const int64_t* __restrict__ z, int64_t s, const int32_t* __restrict__ L,
+                         int32_t* __restrict__ e) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < s) e[j] = L[z[j]];
+}
+
+// Stable counting sort of j by e2 = e_j mod L2 (one CTA; plan time only).
+__global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ bstart,
+                          int32_t* __restrict__ bidx, int32_t* __restrict__ be1) {
+  extern __shared__ int32_t cursor[];
+  for (int i = threadIdx.x; i <= L2; i += blockDim.x) bstart[i] = 0;
+  __syncthreads();
+  for (int64_t j = threadIdx.x; j < s; j += blockDim.x) atomicAdd(&bstart[(e[j] & (L2 - 1)) + 1], 1);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int i = 1; i <= L2; ++i) bstart[i] += bstart[i - 1];
+    for (int i = 0; i < L2; ++i) cursor[i] = bstart[i];
+    for (int64_t j = 0; j < s; ++j) {
+      const int ej = e[j];
+      const int pos = cursor[ej & (L2 - 1)]++;
+      bidx[pos] = int32_t(j);
+      be1[pos] = ej / L2;
+    }
+  }
+}
+
+__global__ void k_rtable(const int32_t* __restrict__ L, int64_t N, int64_t m, int32_t* __restrict__ R) {
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  R[n] = n == 0 ? -1 : int32_t((m - L[n]) % m);
+}
+
+__global__ void k_zeta(int family, int phi, int64_t N, uint64_t p, int D, int64_t m,
+                       const int32_t* __restrict__ P, double* __restrict__ zeta, double* __restrict__ scal) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k == 0) scal[0] = phi_eval(phi, 0, N);
+  if (k >= m) return;
+  const int64_t r = P[k];
+  const int64_t idx = family == QMC_FAMILY_LATTICE ? r : gf2_vd_index(uint64_t(r), p, D);
+  zeta[k] = phi_eval(phi, idx, N);
+}
+
+// tw[k] = ω_n^k = exp(-2πi k/n), k < count
+__global__ void k_twiddles(double2* __restrict__ tw, int64_t n, int64_t count) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= count) return;
+  double sv, cv;
+  sincospi(2.0 * double(k) / double(n), &sv, &cv);
+  tw[k] = make_double2(cv, -sv);
+}
+
+// W[f1*L2 + f2] = DFT_L(K)[f1 + L1·f2] / L with the correlation kernel
+// K[d] = ζ[(-d) mod m] for d < m, K[L-d'] = ζ[d'] for 0 < d' < m (padded),
+// 0 otherwise.  Four-step: T[f1,e2] = Σ_{e1} K[L2 e1 + e2] ω_L^{(L2 e1+e2) f1}
+// evaluated directly, then the length-L2 row FFT over e2.
+template <int L2>
+__global__ void __launch_bounds__(RowThreads<L2>::value)
+    k_spectrum_rows(const double* __restrict__ zeta, int64_t m, int64_t L, int L1,
+                    const double2* __restrict__ tw1, const double2* __restrict__ twL,
+                    const double2* __restrict__ tw2, double2* __restrict__ W) {
+  extern __shared__ double2 S[];
+  constexpr int NT = RowThreads<L2>::value;
+  const int f1 = blockIdx.x;
+  for (int e2 = threadIdx.x; e2 < L2; e2 += NT) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int e1 = 0; e1 < L1; ++e1) {
+      const int64_t d = int64_t(L2) * e1 + e2;
+      double kv = 0.0;
+      if (d < m) kv = zeta[(m - d) % m];
+      else if (d > L - m) kv = zeta[L - d];
+      if (kv != 0.0) {
+        const int64_t x = (d * f1) % L;
+        const double2 w = cmul(tw1[x / L2], twL[x % L2]);
+        acc.x = fma(kv, w.x, acc.x);
+        acc.y = fma(kv, w.y, acc.y);
+      }
+    }
+    S[swz(e2)] = acc;
+  }
+  __syncthreads();
+  row_fft<L2, -1>(S, tw2);
+  const double inv = 1.0 / double(L);
+  for (int f2 = threadIdx.x; f2 < L2; f2 += NT) {
+    const double2 v = S[swz(f2)];
+    W[int64_t(f1) * L2 + f2] = make_double2(v.x * inv, v.y * inv);
+  }
+}
+
+template <int L2>
+static int launch_spectrum(const qmc_plan* pl) {
+  const size_t smem = size_t(L2) * sizeof(double2);
+  cudaFuncSetAttribute(k_spectrum_rows<L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+  k_spectrum_rows<L2><<<unsigned(pl->sp.L1), RowThreads<L2>::value, smem, pl->stream>>>(
+      pl->d_zeta, pl->m, pl->sp.L, int(pl->sp.L1), pl->d_tw1, pl->d_twL, pl->d_tw2, pl->d_W);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
+static int spectrum_dispatch(const qmc_plan* pl) {
+  switch (pl->sp.L2) {
+    case 16: return launch_spectrum<16>(pl);
+    case 32: return launch_spectrum<32>(pl);
+    case 64: return launch_spectrum<64>(pl);
+    case 128: return launch_spectrum<128>(pl);
+    case 256: return launch_spectrum<256>(pl);
+    case 512: return launch_spectrum<512>(pl);
+    case 1024: return launch_spectrum<1024>(pl);
+    case 2048: return launch_spectrum<2048>(pl);
+    case 4096: return launch_spectrum<4096>(pl);
+    case 8192: return launch_spectrum<8192>(pl);
+  }
+  return QMC_EINVAL_N;
+}
+
+static unsigned blocks(int64_t n, int b) { return unsigned((n + b - 1) / b); }
+
+// ------------------------------------------------------------------ create
+static int validate_family(int family, int64_t N_or_D, int64_t s, int64_t* N, int64_t* m) {
+  if (s < 1 || s > (int64_t(1) << 30)) return QMC_EINVAL_DIM;
+  if (family == QMC_FAMILY_LATTICE) {
+    if (N_or_D < 3 || N_or_D >= (int64_t(1) << 31) || !host_is_prime(N_or_D)) return QMC_EINVAL_N;
+    *N = N_or_D;
+    *m = N_or_D - 1;
+  } else if (family == QMC_FAMILY_POLY) {
+    if (N_or_D < 2 || N_or_D > 24) return QMC_EINVAL_POLY;
+    *N = int64_t(1) << N_or_D;
+    *m = *N - 1;
+  } else {
+    return QMC_EINVAL_N;
+  }
+  return QMC_OK;
+}
+
+static int pick_radices(int64_t L1, int* r, int* n) {
+  int k = 0;
+  int64_t x = L1;
+  while (x % 8 == 0) { r[k++] = 8; x /= 8; }
+  while (x % 4 == 0) { r[k++] = 4; x /= 4; }
+  while (x % 2 == 0) { r[k++] = 2; x /= 2; }
+  while (x % 5 == 0) { r[k++] = 5; x /= 5; }
+  while (x % 3 == 0) { r[k++] = 3; x /= 3; }
+  *n = k;
+  return x == 1 ? QMC_OK : QMC_EINVAL_N;
+}
+
+static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p, int64_t s,
+                         const int64_t* z_host, int phi, void* plan_ws, size_t plan_ws_bytes,
+                         void* stream) {
+  if (!out) return QMC_ENULL;
+  *out = nullptr;
+  if (!z_host || !plan_ws) return QMC_ENULL;
+  if (phi < QMC_PHI_IDENTITY || phi > QMC_PHI_INVNORM_MID) return QMC_EINVAL_PHI;
+  int64_t N, m;
+  int rc = validate_family(family, N_or_D, s, &N, &m);
+  if (rc) return rc;
+  if (family == QMC_FAMILY_POLY) {
+    const int D = int(N_or_D);
+    if ((p >> D) != 1 || !(p & 1)) return QMC_EINVAL_POLY;
+  }
+  for (int64_t j = 0; j < s; ++j)
+    if (z_host[j] < 1 || z_host[j] > m) return QMC_EINVAL_Z;
+  Split sp;
+  if (!choose_split(m, s, &sp)) return QMC_EINVAL_N;
+  const PlanLayout lay = plan_layout(N, m, s, sp);
+  if (plan_ws_bytes < lay.total || (uintptr_t(plan_ws) % kAlign)) return QMC_EWORKSPACE;
+
+  qmc_plan* pl = new (std::nothrow) qmc_plan();
+  if (!pl) return QMC_ECUDA;
+  pl->family = family;
+  pl->phi = phi;
+  pl->N = N;
+  pl->m = m;
+  pl->s = s;
+  pl->D = family == QMC_FAMILY_POLY ? int(N_or_D) : 0;
+  pl->p = p;
+  pl->sp = sp;
+  pl->stream = (cudaStream_t)stream;
+  pl->ws = (char*)plan_ws;
+  pl->ws_bytes = plan_ws_bytes;
+  pl->batch_pairs = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(40) << 20) / (sp.L * 16)));
+  int cb = 32;
+  while (cb > 1 && (int64_t(cb) * sp.L1 > 2048 || cb > sp.L2)) cb >>= 1;
+  pl->col_cb = cb;
+  rc = pick_radices(sp.L1, pl->rad1, &pl->nrad1);
+  if (rc) { delete pl; return rc; }
+  char* b = pl->ws;
+  pl->d_scal = (double*)(b + lay.off_scal);
+  pl->d_P = (int32_t*)(b + lay.off_P);
+  pl->d_L = (int32_t*)(b + lay.off_L);
+  pl->d_R = (int32_t*)(b + lay.off_R);
+  pl->d_e = (int32_t*)(b + lay.off_e);
+  pl->d_bstart = (int32_t*)(b + lay.off_bstart);
+  pl->d_bidx = (int32_t*)(b + lay.off_bidx);
+  pl->d_be1 = (int32_t*)(b + lay.off_be1);
+  pl->d_zeta = (double*)(b + lay.off_zeta);
+  pl->d_W = (double2*)(b + lay.off_W);
+  pl->d_tw1 = (double2*)(b + lay.off_tw1);
+  pl->d_tw2 = (double2*)(b + lay.off_tw2);
+  pl->d_twL = (double2*)(b + lay.off_twL);
+  pl->d_rad1 = (int32_t*)(b + lay.off_radix1);
+  cudaStream_t st = pl->stream;
+
+  auto fail = [&](int code) {
+    delete pl;
+    return code;
+  };
+
+  // plan-time scratch inside plan_ws: z, the prime factors of m, one flag
+  std::vector<int64_t> qf = host_prime_factors(m);
+  int64_t* d_z = (int64_t*)(b + lay.off_tmp);
+  int64_t* d_qf = d_z + s;
+  unsigned long long* d_flag = (unsigned long long*)(d_qf + 64);
+  auto cleanup = [&]() { cudaStreamSynchronize(st); };
+#define QMC_PLAN_CHECK(expr)              \
+  do {                                    \
+    int _rc = (expr);                     \
+    if (_rc) {                            \
+      cleanup();                          \
+      return fail(_rc);                   \
+    }                                     \
+  } while (0)
+#define QMC_PLAN_LAUNCHED() QMC_PLAN_CHECK(cudaPeekAtLastError() == cudaSuccess ? (g_launches++, 0) : (cudaGetLastError(), QMC_ECUDA))
+
+  QMC_PLAN_CHECK(cudaMemcpyAsync(d_z, z_host, sizeof(int64_t) * s, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
+  if (!qf.empty())
+    QMC_PLAN_CHECK(cudaMemcpyAsync(d_qf, qf.data(), sizeof(int64_t) * qf.size(), cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
+  QMC_PLAN_CHECK(cudaMemcpyAsync(pl->d_rad1, pl->rad1, sizeof(int32_t) * 24, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
+
+  // a0: generator
+  if (family == QMC_FAMILY_LATTICE) {
+    unsigned long long best = ~0ull;
+    for (int64_t base = 2; base < N && best == ~0ull; base += 4096) {
+      unsigned long long init = ~0ull;
+      QMC_PLAN_CHECK(cudaMemcpyAsync(d_flag, &init, 8, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
+      k_find_generator<<<16, 256, 0, st>>>(N, base, d_qf, int(qf.size()), d_flag);
+      QMC_PLAN_LAUNCHED();
+      QMC_PLAN_CHECK(cudaMemcpyAsync(&best, d_flag, 8, cudaMemcpyDeviceToHost, st) ? QMC_ECUDA : 0);
+      QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
+    }
+    if (best == ~0ull) { cleanup(); return fail(QMC_EINVAL_N); }
+    pl->gen = int64_t(best);
+  } else {
+    unsigned long long flags = 0;
+    QMC_PLAN_CHECK(cudaMemcpyAsync(d_flag, &flags, 8, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
+    k_check_poly<<<1, 64, 0, st>>>(p, pl->D, d_qf, int(qf.size()), d_flag);
+    QMC_PLAN_LAUNCHED();
+    QMC_PLAN_CHECK(cudaMemcpyAsync(&flags, d_flag, 8, cudaMemcpyDeviceToHost, st) ? QMC_ECUDA : 0);
+    QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
+    if (flags) { cleanup(); return fail(QMC_EINVAL_POLY); }
+    pl->gen = 2;  // the polynomial x
+  }
+
+  // a1..a3
+  k_pow_table<<<blocks(m, 256), 256, 0, st>>>(family, N, p, pl->D, pl->gen, m, pl->d_P);
+  QMC_PLAN_LAUNCHED();
+  k_fill_i32<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, -1);
+  QMC_PLAN_LAUNCHED();
+  k_log_scatter<<<blocks(m, 256), 256, 0, st>>>(pl->d_P, m, pl->d_L);
+  QMC_PLAN_LAUNCHED();
+  k_colmap<<<blocks(s, 256), 256, 0, st>>>(d_z, s, pl->d_L, pl->d_e);
+  QMC_PLAN_LAUNCHED();
+  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bidx, pl->d_be1);
+  QMC_PLAN_LAUNCHED();
+  k_rtable<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, m, pl->d_R);
+  QMC_PLAN_LAUNCHED();
+  // a4
+  k_zeta<<<blocks(m, 256), 256, 0, st>>>(family, phi, N, p, pl->D, m, pl->d_P, pl->d_zeta, pl->d_scal);
+  QMC_PLAN_LAUNCHED();
+  k_twiddles<<<blocks(sp.L1, 256), 256, 0, st>>>(pl->d_tw1, sp.L1, sp.L1);
+  QMC_PLAN_LAUNCHED();
+  k_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tw2, sp.L2, sp.L2);
+  QMC_PLAN_LAUNCHED();
+  k_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_twL, sp.L, sp.L2);
+  QMC_PLAN_LAUNCHED();
+  QMC_PLAN_CHECK(spectrum_dispatch(pl));
+  QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
+#undef QMC_PLAN_CHECK
+#undef QMC_PLAN_LAUNCHED
+  *out = pl;
+  return QMC_OK;
+}
+
+}  // namespace qmc
+
+using namespace qmc;
+
+extern "C" {
+
+int qmc_plan_workspace_size(int family, int64_t N_or_D, int64_t s, size_t* plan_bytes) {
+  if (!plan_bytes) return QMC_ENULL;
+  int64_t N, m;
+  int rc = validate_family(family, N_or_D, s, &N, &m);
+  if (rc) return rc;
+  Split sp;
+  if (!choose_split(m, s, &sp)) return QMC_EINVAL_N;
+  *plan_bytes = plan_layout(N, m, s, sp).total;
+  return QMC_OK;
+}
+
+int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
+                    void* plan_ws, size_t plan_ws_bytes, void* stream) {
+  return create_common(out, QMC_FAMILY_LATTICE, N, 0, s, z_host, phi, plan_ws, plan_ws_bytes, stream);
+}
+
+int qmc_plan_create_poly(qmc_plan_t* out, int D, uint64_t p, int64_t s, const int64_t* q_host,
+                         int phi, void* plan_ws, size_t plan_ws_bytes, void* stream) {
+  return create_common(out, QMC_FAMILY_POLY, D, p, s, q_host, phi, plan_ws, plan_ws_bytes, stream);
+}
+
+int qmc_plan_info(qmc_plan_t pl, int64_t* info) {
+  if (!pl || !info) return QMC_ENULL;
+  info[0] = pl->family;
+  info[1] = pl->N;
+  info[2] = pl->m;
+  info[3] = pl->s;
+  info[4] = pl->phi;
+  info[5] = pl->gen;
+  info[6] = pl->sp.L;
+  info[7] = pl->sp.L1;
+  info[8] = pl->sp.L2;
+  info[9] = pl->batch_pairs;
+  info[10] = pl->D;
+  info[11] = int64_t(pl->p);
+  return QMC_OK;
+}
+
+int qmc_plan_tables(qmc_plan_t pl, int64_t* gen, int32_t* P, int32_t* L, int32_t* e, double* zeta) {
+  if (!pl) return QMC_ENULL;
+  if (cudaStreamSynchronize(pl->stream) != cudaSuccess) return QMC_ECUDA;
+  if (gen) *gen = pl->gen;
+  if (P && cudaMemcpy(P, pl->d_P, 4 * pl->m, cudaMemcpyDeviceToHost) != cudaSuccess) return QMC_ECUDA;
+  if (L && cudaMemcpy(L, pl->d_L, 4 * pl->N, cudaMemcpyDeviceToHost) != cudaSuccess) return QMC_ECUDA;
+  if (e && cudaMemcpy(e, pl->d_e, 4 * pl->s, cudaMemcpyDeviceToHost) != cudaSuccess) return QMC_ECUDA;
+  if (zeta && cudaMemcpy(zeta, pl->d_zeta, 8 * pl->m, cudaMemcpyDeviceToHost) != cudaSuccess) return QMC_ECUDA;
+  return QMC_OK;
+}
+
+int64_t qmc_launch_count(void) { return g_launches.load(); }
+
+int qmc_profile_enable(int on) {
+  g_prof.on = on != 0;
+  return QMC_OK;
+}
+
+int qmc_profile_read(int64_t* launches, double* ms, int n) {
+  if (!launches || !ms) return QMC_ENULL;
+  for (int k = 0; k < KC_COUNT; ++k) {
+    double tot = 0.0;
+    for (auto& pr : g_prof.ev[k]) {
+      if (cudaEventSynchronize(pr.second) != cudaSuccess) return QMC_ECUDA;
+      float x = 0.f;
+      cudaEventElapsedTime(&x, pr.first, pr.second);
+      tot += x;
+      g_prof.pool.push_back(pr.first);
+      g_prof.pool.push_back(pr.second);
+    }
+    if (k < n) {
+      launches[k] = int64_t(g_prof.ev[k].size());
+      ms[k] = tot;
+    }
+    g_prof.ev[k].clear();
+  }
+  return QMC_OK;
+}
+
+const char* qmc_profile_class_name(int k) {
+  static const char* names[KC_COUNT] = {"k_pack", "k_rows", "k_cols", "k_gather", "k_colmean_reduce",
+                                        "k_finalize"};
+  return (k >= 0 && k < KC_COUNT) ? names[k] : "";
+}
+
+void qmc_plan_destroy(qmc_plan_t pl) { delete pl; }
+
+const char* qmc_strerror(int code) {
+  switch (code) {
+    case QMC_OK: return "ok";
+    case QMC_EINVAL_N: return "N not prime, out of range, or circulant length unsupported";
+    case QMC_EINVAL_Z: return "generating vector entry outside [1, m]";
+    case QMC_EINVAL_POLY: return "modulus not of degree D or not primitive over F_2";
+    case QMC_EINVAL_DIM: return "invalid dimension (s < 1, t < 0, lda < s, ldx < N)";
+    case QMC_EINVAL_PHI: return "unknown phi";
+    case QMC_ENULL: return "required pointer is NULL";
+    case QMC_ECUDA: return "CUDA error";
+    case QMC_EWORKSPACE: return "workspace too small or not 256-byte aligned";
+    case QMC_EINVAL_F: return "unknown f";
+  }
+  return "unknown status";
+}
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// qmc_internal.cuh — plan object and shared helpers of libqmc (not part of
+// the ABI).  See include/qmc.h for the contract and DESIGN.md for the data
+// layout in HBM.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/qmc.h"
+
+namespace qmc {
+
+constexpr size_t kAlign = 256;
+
+inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+// number of kernels launched by the library (qmc_launch_count)
+extern std::atomic<int64_t> g_launches;
+
+// Optional per-kernel-class CUDA-event timing (qmc_profile_*): events are
+// recorded on the launching stream around every hot-path launch.
+enum KernelClass { KC_PACK = 0, KC_ROWS, KC_COLS, KC_GATHER, KC_REDUCE, KC_FINALIZE, KC_COUNT };
+void prof_begin(int kc, cudaStream_t st);
+void prof_end(int kc, cudaStream_t st);
+
+inline int cuda_status() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? QMC_OK : QMC_ECUDA;
+}
+
+#define QMC_LAUNCHED()                                    \
+  do {                                                    \
+    ::qmc::g_launches.fetch_add(1, std::memory_order_relaxed); \
+    if (cudaPeekAtLastError() != cudaSuccess) {           \
+      cudaGetLastError();                                 \
+      return QMC_ECUDA;                                   \
+    }                                                     \
+  } while (0)
+
+// FFT length selection (host): L = L1·L2, L2 a power of two in [16, 8192]
+// (row FFT, shared memory), L1 ∈ {1} ∪ 2^a 3^b 5^c ≤ 1024 (column FFT).
+// L = m when m splits that way, otherwise the smallest such L ≥ 2m-1
+// (zero-padded cyclic correlation; exact).
+struct Split {
+  int64_t L, L1, L2;
+  bool padded;
+};
+bool choose_split(int64_t m, int64_t s, Split* out);
+
+// Plan-workspace carve-up (device pointers), identical for the size query
+// and the create call.
+struct PlanLayout {
+  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bidx, off_be1, off_zeta, off_W,
+      off_tw1, off_tw2, off_twL, off_radix1, off_tmp, total;
+};
+PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
+
+}  // namespace qmc
+
+struct qmc_plan {
+  int family;
+  int phi;
+  int64_t N, m, s;
+  int D;
+  uint64_t p;
+  int64_t gen;
+  qmc::Split sp;
+  int64_t batch_pairs;  // column pairs per batch (scratch sized to stay in L2)
+  int col_cb;           // column-FFT block width (K2)
+  int nrad1;            // radices of L1
+  int rad1[24];
+  cudaStream_t stream;
+  // device pointers into plan_ws
+  char* ws;
+  size_t ws_bytes;
+  double* d_scal;    // [0] = φ(0), [1] = generator (as double), [2] = status flags
+  int32_t* d_P;      // [m]
+  int32_t* d_L;      // [N]
+  int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1
+  int32_t* d_e;      // [s]
+  int32_t* d_bstart; // [L2+1]
+  int32_t* d_bidx;   // [s]   j in bucket order (e2 = e_j mod L2, then j)
+  int32_t* d_be1;    // [s]   e_j / L2 in bucket order
+  double* d_zeta;    // [m]
+  double2* d_W;      // [L]   W[f1*L2 + f2] = DFT_L(K)[f1 + L1 f2] / L
+  double2* d_tw1;    // [L1]  ω_{L1}^k
+  double2* d_tw2;    // [L2]  ω_{L2}^k
+  double2* d_twL;    // [L2]  ω_L^k, k < L2
+  int32_t* d_rad1;   // [24]
+};

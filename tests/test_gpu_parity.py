@@ -1,0 +1,267 @@
+"""Parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (north_star, reading R16): per column k,
+    max_n |X_gpu[n,k] - X_oracle[n,k]| <= 1e-11 · ||A[:,k]||_1 · max|φ|;
+plan tables (generator, P, L, e) bit-exact.  Inputs are the seeded
+workloads of qmc_workloads; expected values come only from oracle/.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import qmc_workloads as W
+from _ref import X_full, X_rows, col_tolerance, index_fn, phi_tab, sample_rows
+
+pytestmark = pytest.mark.gpu
+
+PHIS = [W.PHI_IDENTITY, W.PHI_SHIFT_HALF, W.PHI_TENT, W.PHI_INVNORM_MID]
+
+
+@pytest.fixture(scope="module")
+def qmc():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need CUDA"
+    import paper_1501_06286_b200 as q
+    return q
+
+
+def dev_X(q, w, t=None):
+    import torch
+    plan = q.Plan.from_workload(w)
+    A = q.to_device_colmajor(w.A if t is None else w.A[:, :t], "cuda")
+    X = plan.matmul(A)
+    torch.cuda.synchronize()
+    return plan, X.cpu().numpy()
+
+
+def check_X(w, Xg, Xo, rows=None, cols=None):
+    tol = col_tolerance(w, cols=cols)
+    Xg_s = Xg if rows is None else Xg[rows]
+    if cols is not None:
+        Xg_s = Xg_s[:, cols]
+    err = np.abs(Xg_s - Xo).max(axis=0)
+    assert np.all(np.isfinite(Xg_s))
+    bad = np.nonzero(err > tol)[0]
+    assert bad.size == 0, f"columns {bad[:5]} err {err[bad[:5]]} tol {tol[bad[:5]]}"
+    return float((err / tol).max())
+
+
+# ------------------------------------------------------------------ plan tables
+def _oracle_tables(w):
+    if w.family == "poly":
+        P = O.gf2_power_table(w.p, w.D)
+        L = O.gf2_log_table(w.D, P)
+        gen = 2
+    else:
+        gen = O.primitive_root(w.N)
+        P = O.power_table(w.N, gen)
+        L = O.log_table(w.N, P)
+    e = O.column_exponents(w.z, L) - 1
+    return gen, P, L, e
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_plan_tables_bit_exact(qmc, c):
+    w = W.config(c, t_override=2)
+    plan = qmc.Plan.from_workload(w)
+    gen, P, L, e, zeta = plan.tables()
+    og, oP, oL, oe = _oracle_tables(w)
+    assert gen == og
+    np.testing.assert_array_equal(P, oP)
+    np.testing.assert_array_equal(L, oL)
+    np.testing.assert_array_equal(e, oe)
+    tab = phi_tab(w)
+    idx = oP if w.family == "lattice" else np.array([O.gf2_vd_index(int(r), w.p, w.D) for r in oP])
+    np.testing.assert_allclose(zeta, tab[idx], rtol=1e-14, atol=1e-15)
+
+
+def test_worked_example_gpu(qmc):
+    """N=7, g=(1,5,3), φ = identity, a = (7,7,7) -> (0,9,11,6,15,10,12)."""
+    import torch
+    plan = qmc.Plan.lattice(7, [1, 5, 3], W.PHI_IDENTITY)
+    gen, P, L, e, _ = plan.tables()
+    assert gen == 3 and list(e + 1) == [1, 6, 2]
+    A = qmc.to_device_colmajor(np.array([[7.0, 1.0], [7.0, 0.0], [7.0, 0.0]]), "cuda")
+    X = plan.matmul(A).cpu().numpy()
+    np.testing.assert_allclose(X[:, 0], [0, 9, 11, 6, 15, 10, 12], atol=1e-13)
+    np.testing.assert_allclose(X[:, 1] * 7, [0, 1, 2, 3, 4, 5, 6], atol=1e-13)
+    torch.cuda.synchronize()
+
+
+# ------------------------------------------------------------------ small cases, full X
+SMALL = [(7, 3, 2), (11, 20, 5), (13, 4, 1), (31, 100, 7), (61, 17, 8), (101, 300, 9), (257, 300, 64),
+         (1021, 50, 6), (4001, 400, 10), (16001, 200, 4)]
+
+
+@pytest.mark.parametrize("N,s,t", SMALL)
+@pytest.mark.parametrize("phi", PHIS)
+def test_small_lattice_full(qmc, N, s, t, phi):
+    w = W.custom_lattice(N, s, t, phi, seed=N * 10 + phi)
+    plan, Xg = dev_X(qmc, w)
+    check_X(w, Xg, X_full(w))
+
+
+@pytest.mark.parametrize("D", [2, 3, 4, 5, 6, 7, 8, 10, 12])
+@pytest.mark.parametrize("phi", [W.PHI_SHIFT_HALF, W.PHI_INVNORM_MID])
+def test_small_poly_full(qmc, D, phi):
+    p = O.gf2_smallest_primitive(D)
+    w = W.custom_poly(D, p, s=3 * D + 5, t=5, phi=phi, seed=D)
+    plan, Xg = dev_X(qmc, w)
+    check_X(w, Xg, X_full(w))
+
+
+def test_config1_full(qmc):
+    w = W.config(1)
+    plan, Xg = dev_X(qmc, w)
+    assert plan.info["L"] == 256 and plan.info["L1"] == 1
+    ratio = check_X(w, Xg, X_full(w))
+    assert ratio < 1e-2
+
+
+# ------------------------------------------------------------------ edge cases
+def test_edge_cases(qmc):
+    import torch
+    q = qmc
+    # s = 1, t = 1 (odd, single column), all z equal, repeated z (s > m)
+    for (N, z) in [(13, [5]), (13, [4] * 9), (11, list(range(1, 11)) * 3)]:
+        w = W.custom_lattice(N, len(z), 1, W.PHI_TENT, seed=3)
+        w.z = np.array(z, dtype=np.int64)
+        plan, Xg = dev_X(q, w)
+        check_X(w, Xg, X_full(w))
+    # t = 0 is a no-op
+    plan = q.Plan.lattice(13, [1, 2], W.PHI_SHIFT_HALF)
+    A0 = torch.empty((0, 2), dtype=torch.float64, device="cuda").t()
+    X0 = plan.matmul(A0)
+    assert X0.shape == (13, 0)
+    # lda > s and ldx > N: padding rows of X untouched
+    w = W.custom_lattice(101, 30, 6, W.PHI_SHIFT_HALF, seed=9)
+    plan = q.Plan.from_workload(w)
+    Abig = torch.zeros((6, 40), dtype=torch.float64, device="cuda")
+    Abig[:, :30] = torch.from_numpy(np.ascontiguousarray(w.A.T)).cuda()
+    A = Abig.t()[:30]                       # (30, 6), lda = 40
+    Xbig = torch.full((6, 128), 7.5, dtype=torch.float64, device="cuda")
+    X = Xbig.t()[:101]                      # (101, 6), ldx = 128
+    plan.matmul(A, X)
+    Xh = Xbig.cpu().numpy()
+    assert np.all(Xh[:, 101:] == 7.5)
+    check_X(w, Xh[:, :101].T, X_full(w))
+
+
+def test_invalid_arguments(qmc):
+    from paper_1501_06286_b200 import _abi as abi
+    with pytest.raises(abi.QMCError) as e:
+        qmc.Plan.lattice(15, [1, 2], W.PHI_IDENTITY)
+    assert e.value.code == -1
+    for z in ([0, 1], [1, 13]):
+        with pytest.raises(abi.QMCError) as e:
+            qmc.Plan.lattice(13, z, W.PHI_IDENTITY)
+        assert e.value.code == -2
+    with pytest.raises(abi.QMCError) as e:
+        qmc.Plan.lattice(13, [1], 7)
+    assert e.value.code == -5
+    with pytest.raises(abi.QMCError) as e:     # x^4+x^2+1 = (x^2+x+1)^2 not primitive
+        qmc.Plan.poly(4, 0b10101, [1, 2], W.PHI_IDENTITY)
+    assert e.value.code == -3
+
+
+def test_deterministic_and_shard_invariant(qmc):
+    """Two runs are bitwise identical; computing columns [0,t) in two slabs
+    with an even boundary gives bitwise the same X (columns are packed in
+    pairs (2i, 2i+1), so an even split keeps every pair)."""
+    import torch
+    w = W.config(2, t_override=64)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X1 = plan.matmul(A).clone()
+    X2 = plan.matmul(A).clone()
+    assert torch.equal(X1, X2)
+    Xs = qmc.colmajor_empty(plan.N, 64, "cuda")
+    plan.matmul(A[:, :24], Xs[:, :24])
+    plan.matmul(A[:, 24:], Xs[:, 24:])
+    assert torch.equal(X1, Xs)
+
+
+# ------------------------------------------------------------------ the five configs
+def test_config2_full_and_rowmean_relu(qmc):
+    """Config 2 at full size in bench.py's launch configuration (qmc_mean,
+    f = ROWMEAN_RELU, X written): full X and the scalar Q (reading R10)."""
+    import torch
+    w = W.config(2)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    rs = plan.mean(A, W.F_ROWMEAN_RELU, 0.0, X=X)
+    Q = plan.finalize(W.F_ROWMEAN_RELU, rs, w.t)
+    Xg = X.cpu().numpy()
+    Xo = X_full(w, block=8192)
+    check_X(w, Xg, Xo)
+    Qo = O.rowmean_relu(Xo)
+    # |ΔQ| <= (1/t) Σ_k tol_k + 1e-14·Q  (reading R16)
+    tolQ = col_tolerance(w).sum() / w.t + 1e-14 * abs(Qo)
+    assert abs(float(Q.item()) - Qo) <= tolQ
+    rs_o = O.row_sums(Xo)
+    np.testing.assert_allclose(rs.cpu().numpy(), rs_o, rtol=0, atol=col_tolerance(w).sum())
+    torch.cuda.synchronize()
+
+
+def test_config3_sampled(qmc):
+    """Config 3 full size (qmc_mean, f = AFFINE c=1, X receives 1+X): 260 sampled rows
+    × all 65536 columns, two full columns and their means (closed form R8 too)."""
+    import torch
+    w = W.config(3)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    means = plan.mean(A, W.F_AFFINE, 1.0, X=X)
+    rows = sample_rows(w.N, 256, seed=3)
+    idx = torch.from_numpy(rows).cuda()
+    Xs = X.index_select(0, idx).cpu().numpy()
+    Xo = 1.0 + X_rows(w, rows)
+    check_X(w, Xs, Xo)
+    cols = [0, 1, 33333, w.t - 1]
+    Xc = X[:, cols].cpu().numpy()
+    Xoc = 1.0 + X_full(w, cols=cols, block=2048)
+    check_X(w, Xc, Xoc, cols=cols)
+    m_g = means.cpu().numpy()
+    m_o = O.column_means(Xoc, O.F_IDENTITY)
+    np.testing.assert_allclose(m_g[cols], m_o, rtol=0, atol=1e-13)
+    closed = 1.0 - w.A.sum(axis=0) / (2 * w.N)
+    np.testing.assert_allclose(m_g, closed, rtol=0, atol=1e-12)
+
+
+def test_config4_sampled(qmc):
+    """Config 4 (F_2 polynomial lattice, zero-padded 2^17 correlation)."""
+    import torch
+    w = W.config(4)
+    plan = qmc.Plan.from_workload(w)
+    assert plan.info["L"] == 131072
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = plan.matmul(A)
+    rows = sample_rows(w.N, 512, seed=4)
+    Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    check_X(w, Xs, X_rows(w, rows))
+    cols = [0, 1, 1000, 1999]
+    check_X(w, X[:, cols].cpu().numpy(), X_full(w, cols=cols), cols=cols)
+
+
+def test_config5_sampled(qmc):
+    """Config 5 full size (qmc_mean, f = EXP, X written): sampled rows × all
+    columns and one full column pair with its mean of exp(X)."""
+    import torch
+    w = W.config(5)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    means = plan.mean(A, W.F_EXP, 0.0, X=X)
+    rows = sample_rows(w.N, 256, seed=5)
+    Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    check_X(w, Xs, X_rows(w, rows))
+    cols = [0, 8191]
+    Xc = X[:, cols].cpu().numpy()
+    Xoc = X_full(w, cols=cols, block=8192)
+    check_X(w, Xc, Xoc, cols=cols)
+    m_o = O.column_means(Xoc, O.F_EXP)
+    m_g = means.cpu().numpy()[cols]
+    # Δ mean(exp X) <= tol · max exp(X) + 1e-14 · mean  (reading R16)
+    tol = col_tolerance(w, cols=cols) * np.exp(Xoc).max(axis=0) + 1e-14 * np.abs(m_o)
+    assert np.all(np.abs(m_g - m_o) <= tol)
