@@ -34,11 +34,10 @@ def dev_X(q, w, t=None):
     return plan, X.cpu().numpy()
 
 
-def check_X(w, Xg, Xo, rows=None, cols=None):
+def check_X(w, Xg_s, Xo, cols=None):
+    """Xg_s, Xo: the same rows and columns (cols names them for the tolerance)."""
     tol = col_tolerance(w, cols=cols)
-    Xg_s = Xg if rows is None else Xg[rows]
-    if cols is not None:
-        Xg_s = Xg_s[:, cols]
+    assert Xg_s.shape == Xo.shape
     err = np.abs(Xg_s - Xo).max(axis=0)
     assert np.all(np.isfinite(Xg_s))
     bad = np.nonzero(err > tol)[0]
