@@ -15,6 +15,10 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#ifndef QMC_TW_RECUR
+#define QMC_TW_RECUR 1
+#endif
+
 namespace qmc {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -34,6 +38,33 @@ __device__ __forceinline__ double2 rot(double2 a) {
 template <int DIR>
 __device__ __forceinline__ double2 twid(double2 w) {  // forward table → direction
   return DIR < 0 ? w : make_double2(w.x, -w.y);
+}
+// 32-byte read-only load of two adjacent complex values (LDG.E.256 on
+// sm_100a); p must be 32-byte aligned.
+__device__ __forceinline__ void ldg2_256(const double2* p, double2& a, double2& b) {
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+      : "l"(p));
+}
+// streaming (evict-first) variants for data read or written exactly once
+__device__ __forceinline__ void ldcs2_256(const double2* p, double2& a, double2& b) {
+  asm("ld.global.cs.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(a.x), "=d"(a.y), "=d"(b.x), "=d"(b.y)
+      : "l"(p));
+}
+__device__ __forceinline__ double2 ldcs(const double2* p) {
+  double2 r;
+  asm("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void stcs(double* p, double v) { asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory"); }
+// Read-only 16-byte load kept in program order (volatile): stops the compiler
+// from hoisting every stage's twiddles to the kernel start, which costs more
+// registers than the latency it hides.
+__device__ __forceinline__ double2 ldg_ordered(const double2* p) {
+  double2 r;
+  asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
+  return r;
 }
 
 // ----------------------------------------------------------------- DFT_R
@@ -112,6 +143,49 @@ template <int DIR> struct Dft<5, DIR> {
     v[2] = cadd(a2, b2);
     v[3] = csub(a2, b2);
   }
+};
+
+// DFT16 = 4 x 4 with internal twiddles ω16^{n2·k1} (constants)
+template <int DIR>
+__device__ __forceinline__ double2 cmul_k(double2 a, double c, double s) {  // a · (c + DIR·i·s)
+  return make_double2(fma(a.x, c, -DIR * a.y * s), fma(a.y, c, DIR * a.x * s));
+}
+
+template <int DIR> struct Dft<16, DIR> {
+  static __device__ __forceinline__ void run(double2* v) {
+    const double c1 = 0.92387953251128675612818318939679;  // cos(π/8)
+    const double s1 = 0.38268343236508977172845998403040;  // sin(π/8)
+    const double h = 0.70710678118654752440084436210485;
+    double2 y[4][4];
+#pragma unroll
+    for (int n2 = 0; n2 < 4; ++n2) {
+      double2 a[4] = {v[n2], v[4 + n2], v[8 + n2], v[12 + n2]};
+      Dft<4, DIR>::run(a);
+#pragma unroll
+      for (int k1 = 0; k1 < 4; ++k1) y[n2][k1] = a[k1];
+    }
+    // y[n2][k1] *= ω16^{n2 k1}, ω16^q = (cos(qπ/8), DIR·sin(qπ/8))
+    y[1][1] = cmul_k<DIR>(y[1][1], c1, s1);
+    y[1][2] = cmul_k<DIR>(y[1][2], h, h);
+    y[1][3] = cmul_k<DIR>(y[1][3], s1, c1);
+    y[2][1] = cmul_k<DIR>(y[2][1], h, h);
+    y[2][2] = rot<DIR>(y[2][2]);
+    y[2][3] = cmul_k<DIR>(y[2][3], -h, h);
+    y[3][1] = cmul_k<DIR>(y[3][1], s1, c1);
+    y[3][2] = cmul_k<DIR>(y[3][2], -h, h);
+    y[3][3] = cmul_k<DIR>(y[3][3], -c1, -s1);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) {
+      double2 b[4] = {y[0][k1], y[1][k1], y[2][k1], y[3][k1]};
+      Dft<4, DIR>::run(b);
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = b[k2];
+    }
+  }
+};
+
+template <int DIR> struct Dft<1, DIR> {
+  static __device__ __forceinline__ void run(double2*) {}
 };
 
 template <int DIR>
@@ -205,6 +279,184 @@ __device__ __forceinline__ void row_fft_rec(double2* S, const double2* __restric
 template <int N, int DIR>
 __device__ __forceinline__ void row_fft(double2* S, const double2* __restrict__ tw) {
   row_fft_rec<N, RowThreads<N>::value, DIR, 1, 0>(S, tw, threadIdx.x);
+}
+
+}  // namespace qmc
+
+
+namespace qmc {
+
+// ----------------------------------------------------------------- register row FFT
+// Length-N FFT with E points per thread (E = 8 or 16, NT = N/E threads):
+// thread `tid` holds element tid + NT·q in v[q] before and after the
+// transform (natural order, strided).  Stages are radix E (plus one smaller
+// radix stage when N is not a power of E); between stages the row is
+// exchanged through shared memory S (padding of one slot per E elements),
+// two barriers per exchange.  A forward transform, a pointwise product and
+// an inverse transform therefore never round-trip through shared memory
+// between them.
+
+// %tid.x read through volatile asm: addresses derived from it cannot be
+// hoisted above the point of use, so each stage holds only its own
+// shared-memory / twiddle addresses live (instead of all stages' at once).
+__device__ __forceinline__ int tid_fresh() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
+template <int E> struct Lg;
+template <> struct Lg<8> { static constexpr int v = 3; };
+template <> struct Lg<16> { static constexpr int v = 4; };
+
+// padded shared-memory index: all 8-thread phases of the stage loads and
+// stores hit distinct bank groups; every address of a stage is a per-thread
+// base plus a compile-time offset
+template <int E>
+__device__ __forceinline__ int padE(int i) { return i + (i >> Lg<E>::v); }
+template <int N, int E> struct PadE { static constexpr int size = N + N / E; };
+__device__ __forceinline__ int swz16(int i) { return padE<16>(i); }
+template <int N> struct Pad16 { static constexpr int size = PadE<N, 16>::size; };
+
+// radix plan: log_E(N) radix-E stages, then the remainder
+template <int N, int E> struct RPlan {
+  static constexpr int count = (N >= E) ? 1 + RPlan<(N >= E ? N / E : 1), E>::count : (N > 1 ? 1 : 0);
+  static __host__ __device__ constexpr int get(int i) {
+    return i == 0 ? (N >= E ? E : N) : RPlan<(N >= E ? N / E : 1), E>::get(i - 1);
+  }
+};
+template <int E> struct RPlan<1, E> {
+  static constexpr int count = 0;
+  static __host__ __device__ constexpr int get(int) { return 1; }
+};
+
+// One radix-R stage on registers.  twS = this stage's twiddle table,
+// stage-major: twS[(r-1)·NS + k] = ω_{NS·R}^{k·r} (forward sign), so the
+// loads of consecutive threads (consecutive k) are contiguous.
+template <int R, int N, int E, int NS, int DIR>
+__device__ __forceinline__ void reg_stage(double2 (&v)[E], const double2* __restrict__ twS, int tid) {
+  constexpr int NT = N / E, BPT = E / R;
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    double2 u[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) u[r] = v[b + r * BPT];
+    if (NS > 1) {
+      const double2* twk = twS + (tid_fresh() + b * NT) % NS;
+#if QMC_TW_RECUR
+      // one load; w^r by a product tree of depth <= 4 (w^r = w^{r/2} w^{r-r/2})
+      double2 pw[R];
+      pw[1] = twid<DIR>(ldg_ordered(twk));
+#pragma unroll
+      for (int r = 2; r < R; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
+#pragma unroll
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], pw[r]);
+#else
+#pragma unroll
+      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twid<DIR>(ldg_ordered(twk + (r - 1) * NS)));
+#endif
+    }
+    Dft<R, DIR>::run(u);
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b + r * BPT] = u[r];
+  }
+}
+
+// After reg_stage<R,N,E,NS>: v[b + r·BPT] holds output index base_b + r·NS.
+template <int R, int N, int E, int NS>
+__device__ __forceinline__ void store_stage(const double2 (&v)[E], double2* S) {
+  constexpr int NT = N / E, BPT = E / R;
+  const int tid = tid_fresh();
+#pragma unroll
+  for (int b = 0; b < BPT; ++b) {
+    const int j = tid + b * NT;
+    const int base = (j / NS) * NS * R + (j % NS);
+#pragma unroll
+    for (int r = 0; r < R; ++r) S[padE<E>(base + r * NS)] = v[b + r * BPT];
+  }
+}
+
+template <int N, int E>
+__device__ __forceinline__ void load_strided(double2 (&v)[E], const double2* S) {
+  constexpr int NT = N / E;
+  const int tid = tid_fresh();
+#pragma unroll
+  for (int q = 0; q < E; ++q) v[q] = S[padE<E>(tid + q * NT)];
+}
+
+template <int N, int E>
+__device__ __forceinline__ void store_strided(const double2 (&v)[E], double2* S) {
+  constexpr int NT = N / E;
+  const int tid = tid_fresh();
+#pragma unroll
+  for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = v[q];
+}
+
+// tws: all stages' twiddle tables back to back (stage I >= 1 at offset OFF,
+// NS·(R-1) entries each; see qmc_plan.d_tws).
+template <int N, int E, int DIR, int NS, int I, int OFF>
+__device__ __forceinline__ void fftE_rec(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid) {
+  if constexpr (I < RPlan<N, E>::count) {
+    constexpr int R = RPlan<N, E>::get(I);
+    if constexpr (I > 0) {
+      constexpr int RP = RPlan<N, E>::get(I - 1);
+      __syncthreads();
+      store_stage<RP, N, E, NS / RP>(v, S);
+      __syncthreads();
+      load_strided<N, E>(v, S);
+    }
+    reg_stage<R, N, E, NS, DIR>(v, tws + OFF, tid);
+    fftE_rec<N, E, DIR, NS * R, I + 1, (I > 0 ? OFF + NS * (R - 1) : OFF)>(v, S, tws, tid);
+  }
+}
+
+template <int N, int E, int DIR>
+__device__ __forceinline__ void fftE(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid) {
+  fftE_rec<N, E, DIR, 1, 0, 0>(v, S, tws, tid);
+}
+
+// ----------------------------------------------------------------- register column DFT
+// Length-N DFT entirely in one thread's registers, N = R·M with R, M in
+// {1,2,3,4,5,8,16}: M-point DFTs over stride-R subsequences, twiddles
+// ω_N^{r·k2} from the table twN (ω_N^k, forward sign), R-point DFTs.
+// Natural order in and out.
+__host__ __device__ constexpr bool direct_radix(int n) {
+  return n == 1 || n == 2 || n == 3 || n == 4 || n == 5 || n == 8 || n == 16;
+}
+__host__ __device__ constexpr int reg_split(int n) {  // R with n = R·M, both direct; 0 if none
+  for (int r = 2; r <= 16; ++r)
+    if (n % r == 0 && direct_radix(r) && direct_radix(n / r)) return r;
+  return direct_radix(n) ? 1 : 0;
+}
+
+template <int N, int DIR>
+__device__ __forceinline__ void reg_dft(double2* v, const double2* __restrict__ twN) {
+  if constexpr (direct_radix(N)) {
+    Dft<N, DIR>::run(v);
+  } else {
+    constexpr int R = reg_split(N), M = N / R;
+    static_assert(R > 1, "unsupported register DFT length");
+    double2 y[N];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double2 sv[M];
+#pragma unroll
+      for (int m = 0; m < M; ++m) sv[m] = v[m * R + r];
+      Dft<M, DIR>::run(sv);
+#pragma unroll
+      for (int k2 = 0; k2 < M; ++k2)
+        y[r * M + k2] = (r * k2 == 0) ? sv[k2] : cmul(sv[k2], twid<DIR>(__ldg(&twN[r * k2])));
+    }
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) {
+      double2 sv[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) sv[r] = y[r * M + k2];
+      Dft<R, DIR>::run(sv);
+#pragma unroll
+      for (int k1 = 0; k1 < R; ++k1) v[k2 + M * k1] = sv[k1];
+    }
+  }
 }
 
 }  // namespace qmc

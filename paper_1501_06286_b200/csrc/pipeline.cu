@@ -28,14 +28,26 @@
 
 #include "fft.cuh"
 #include "qmc_internal.cuh"
+#include "rowcfg.cuh"
 
 namespace qmc {
 
-constexpr int kPackThreads = 256;
 constexpr int kGatherThreads = 256;
-constexpr int kColMeanRows = 2048;  // rows per CTA in the column-mean epilogue
+constexpr int kColMeanRows = 1024;  // rows per CTA in the column-mean epilogue
 
 enum GatherMode { GM_X = 0, GM_ROWSUM = 1 };
+
+// cache policy of the epilogue: Y is dead after the gather and X is only
+// written, so both use evict-first (streaming) accesses unless disabled
+#ifndef QMC_NO_STREAMING
+#define QMC_LD2(p, a, b) ldcs2_256(p, a, b)
+#define QMC_LD1(p) ldcs(p)
+#define QMC_ST(p, v) stcs(p, v)
+#else
+#define QMC_LD2(p, a, b) ldg2_256(p, a, b)
+#define QMC_LD1(p) __ldg(p)
+#define QMC_ST(p, v) (*(p) = (v))
+#endif
 
 // deterministic block sum (fixed shuffle tree, then warp 0 over warps)
 template <int NT>
@@ -59,85 +71,173 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* red) {
   return v;  // valid in thread 0
 }
 
-// ---------------------------------------------------------------- K0
-__global__ void __launch_bounds__(kPackThreads)
-    k_pack(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0, int64_t s,
-           const int32_t* __restrict__ bidx, double2* __restrict__ Ab, double* __restrict__ colsum) {
-  __shared__ double2 red[kPackThreads / 32];
-  const int64_t p = blockIdx.x;
+// ---------------------------------------------------------------- K1
+// One CTA per (row f1, pair p): L2/16 threads, 16 points per thread.
+//   T[f1,e2] = Σ_{j in bucket(e2)} a_j ω_L^{e_j f1}     (a_j = A[j,k1] + i A[j,k2])
+//   forward FFT_L2 → ·W[f1,:] → inverse FFT_L2 → U[p][f1][e2]
+// The twiddle conj(ω_L^{e2 f1}) of the second FFT dimension is applied by K2.
+// CTA f1 = 0 also writes the row-0 sums Σ_j a_j = DC term of the spectrum.
+#ifdef QMC_PHASE_TIMING
+__device__ long long g_phase[4096][8];
+#define QMC_TS(i)                                                                                      \
+  do {                                                                                               \
+    __syncthreads();                                                                                 \
+    if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 4096)                              \
+      g_phase[blockIdx.x + gridDim.x * blockIdx.y][i] = clock64();                                   \
+  } while (0)
+extern "C" int qmc_debug_phases(long long* host, int n) {
+  return cudaMemcpyFromSymbol(host, g_phase, sizeof(long long) * 8 * n) == cudaSuccess ? 0 : -7;
+}
+#else
+#define QMC_TS(i) \
+  do {            \
+  } while (0)
+#endif
+template <int L2>
+__global__ void __launch_bounds__(L2 / QMC_ROW_E, QMC_ROWS_MINB)
+    k_rows16(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
+             const int32_t* __restrict__ e, const int32_t* __restrict__ bnext, int64_t s,
+             const double2* __restrict__ twj, const double2* __restrict__ tws,
+             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum) {
+  extern __shared__ double2 smem[];
+  constexpr int E = QMC_ROW_E;
+  constexpr int NT = L2 / E;
+  double2* S = smem;
+  const int tid = threadIdx.x;
+  const int f1 = blockIdx.x;
+  const int64_t p = blockIdx.y;
   const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
   const bool has2 = k2 < t;
   const double* a1 = A + k1 * lda;
   const double* a2 = A + (has2 ? k2 : k1) * lda;
-  double2* out = Ab + p * s;
-  double2 cs = make_double2(0.0, 0.0);
-  for (int64_t i = threadIdx.x; i < s; i += kPackThreads) {
-    const int j = bidx[i];
-    out[i] = make_double2(__ldg(a1 + j), has2 ? __ldg(a2 + j) : 0.0);
-    cs.x += __ldg(a1 + i);
-    if (has2) cs.y += __ldg(a2 + i);
-  }
-  cs = block_sum2<kPackThreads>(cs, red);
-  if (threadIdx.x == 0) {
-    colsum[k1] = cs.x;
-    if (has2) colsum[k2] = cs.y;
-  }
-}
-
-// ---------------------------------------------------------------- K1
-template <int L2>
-__global__ void __launch_bounds__(RowThreads<L2>::value, 1)
-    k_rows(const double2* __restrict__ Ab, int64_t s, const int32_t* __restrict__ bstart,
-           const int32_t* __restrict__ be1, const double2* __restrict__ tw1,
-           const double2* __restrict__ twL, const double2* __restrict__ tw2,
-           const double2* __restrict__ W, double2* __restrict__ U, int64_t L, int L1) {
-  extern __shared__ double2 smem[];
-  constexpr int NT = RowThreads<L2>::value;
-  constexpr int EPT = L2 / NT;
-  double2* S = smem;
-  double2* rowtw = smem + L2;  // ω_{L1}^{e1·f1}, e1 < L1
-  const int f1 = blockIdx.x;
-  const int64_t p = blockIdx.y;
-  for (int e1 = threadIdx.x; e1 < L1; e1 += NT) rowtw[e1] = __ldg(&tw1[(e1 * f1) % L1]);
-  __syncthreads();
-  const double2* ab = Ab + p * s;
-#pragma unroll 1
-  for (int i = 0; i < EPT; ++i) {
-    const int e2 = threadIdx.x + i * NT;
-    const int b0 = __ldg(&bstart[e2]), b1 = __ldg(&bstart[e2 + 1]);
-    double2 acc = make_double2(0.0, 0.0);
-    for (int b = b0; b < b1; ++b) {
-      const double2 a = __ldg(&ab[b]);
-      const double2 w = rowtw[__ldg(&be1[b])];
-      acc = cadd(acc, cmul(a, w));
+  QMC_TS(0);
+  // scatter a' = P a fused with the first DFT dimension:
+  //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
+  // Entries in natural j order (coalesced, independent loads, issued before
+  // the shared row is cleared); the smallest j of each bucket sums the bucket
+  // along its collision chain in increasing j -> deterministic.
+  constexpr int UE = 4;
+  const double2* twr = twj + int64_t(f1) * s;
+  for (int j0 = 0; j0 < s; j0 += NT * UE) {
+    int ej[UE], nx[UE];
+    double2 a[UE], w[UE];
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      const int j = j0 + tid + u * NT;
+      nx[u] = -2;
+      if (j < s) {
+        ej[u] = __ldg(&e[j]);
+        nx[u] = __ldg(&bnext[j]);
+        a[u] = make_double2(__ldg(a1 + j), has2 ? __ldg(a2 + j) : 0.0);
+        w[u] = __ldg(&twr[j]);
+      }
     }
-    const int x = e2 * f1;  // < L, ω_L^x = ω_{L1}^{x/L2} · ω_L^{x mod L2}
-    const double2 w = cmul(__ldg(&tw1[x / L2]), __ldg(&twL[x % L2]));
-    S[swz(e2)] = cmul(acc, w);
+    if (j0 == 0) {
+#pragma unroll
+      for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = make_double2(0.0, 0.0);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < UE; ++u) {
+      if (nx[u] >= -1) {
+        double2 acc = cmul(a[u], w[u]);
+        for (int jj = nx[u]; jj >= 0;) {  // collisions (rare)
+          acc = cadd(acc, cmul(make_double2(__ldg(a1 + jj), has2 ? __ldg(a2 + jj) : 0.0), __ldg(&twr[jj])));
+          const int v = __ldg(&bnext[jj]);
+          jj = v <= -3 ? -3 - v : -1;
+        }
+        S[padE<E>(ej[u] & (L2 - 1))] = acc;
+      }
+    }
   }
   __syncthreads();
-  row_fft<L2, -1>(S, tw2);
+  QMC_TS(1);
+  double2 v[E];
+  load_strided<L2, E>(v, S);
+  fftE<L2, E, -1>(v, S, tws, tid);
+  QMC_TS(2);
+  if (f1 == 0 && tid == 0) {
+    colsum[k1] = v[0].x;
+    if (has2) colsum[k2] = v[0].y;
+  }
   const double2* Wr = W + int64_t(f1) * L2;
 #pragma unroll
-  for (int i = 0; i < EPT; ++i) {
-    const int f2 = threadIdx.x + i * NT;
-    S[swz(f2)] = cmul(S[swz(f2)], __ldg(&Wr[f2]));
-  }
-  __syncthreads();
-  row_fft<L2, +1>(S, tw2);
+  for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid + q * NT]));
+  QMC_TS(3);
+  fftE<L2, E, +1>(v, S, tws, tid);
+  QMC_TS(4);
   double2* Ur = U + p * L + int64_t(f1) * L2;
-#pragma unroll 2
-  for (int i = 0; i < EPT; ++i) {
-    const int e2 = threadIdx.x + i * NT;
-    const int x = e2 * f1;
-    const double2 w = cmul(__ldg(&tw1[x / L2]), __ldg(&twL[x % L2]));
-    Ur[e2] = cmulc(S[swz(e2)], w);
-  }
+#pragma unroll
+  for (int q = 0; q < E; ++q) Ur[tid + q * NT] = v[q];
+  QMC_TS(5);
 }
 
 // ---------------------------------------------------------------- K2
-// One inverse Stockham stage of radix R over CB interleaved columns
-// (element (i, c) at buf[i·CB + c]); ping-pong in -> out.
+// Inverse DFT of length L1 along f1 for CB adjacent columns e2 of every pair
+// of the batch, after the twiddle conj(ω_L^{e2 f1}); writes the batch
+// pair-interleaved: Y[(L2·e1 + e2)·np + p] = B'_p[L2·e1 + e2].
+// Register path (L1 = R·M, R, M direct radices): one thread per column.
+constexpr int kColCB = 4;  // columns e2 per CTA in the register path
+template <int L1>
+__global__ void __launch_bounds__(256)
+    k_cols_reg(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int np, int NPP,
+               const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Y) {
+  constexpr int CB = kColCB, SA = L1 + 2;  // SA ≡ 2 (mod 8) for even L1: phase A conflict-free
+  extern __shared__ double2 sm[];
+  double2* tcta = sm;                      // [L1][CB] ω_L^{e2·f1}
+  double2* tileA = sm + L1 * CB;           // [p·CB + c][SA]
+  double2* tileC = tileA + np * CB * SA;   // [e1·CB + c][NPP], NPP ≡ 2 (mod 8)
+  const int e2_0 = blockIdx.x * CB;
+  for (int i = threadIdx.x; i < L1 * CB; i += blockDim.x) {
+    const int f1 = i / CB, c = i % CB;
+    const int x = (e2_0 + c) * f1;
+    tcta[i] = cmul(__ldg(&tw1[x >> lg2L2]), __ldg(&twL[x & (L2 - 1)]));
+  }
+  __syncthreads();
+  const int tot = np * L1 * CB;
+  constexpr int UA = 8;  // loads in flight per thread
+  for (int i0 = 0; i0 < tot; i0 += 256 * UA) {
+    double2 u[UA];
+#pragma unroll
+    for (int k = 0; k < UA; ++k) {
+      const int idx = i0 + k * 256 + threadIdx.x;
+      if (idx < tot) {
+        const int c = idx % CB, r = idx / CB;
+        const int f1 = r % L1, p = r / L1;
+        u[k] = __ldg(&U[int64_t(p) * L + int64_t(f1) * L2 + e2_0 + c]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UA; ++k) {
+      const int idx = i0 + k * 256 + threadIdx.x;
+      if (idx < tot) {
+        const int c = idx % CB, r = idx / CB;
+        const int f1 = r % L1, p = r / L1;
+        tileA[(p * CB + c) * SA + f1] = cmulc(u[k], tcta[f1 * CB + c]);
+      }
+    }
+  }
+  __syncthreads();
+  for (int col = threadIdx.x; col < np * CB; col += blockDim.x) {
+    double2 v[L1];
+#pragma unroll
+    for (int f1 = 0; f1 < L1; ++f1) v[f1] = tileA[col * SA + f1];
+    reg_dft<L1, +1>(v, tw1);
+    const int p = col / CB, c = col % CB;
+#pragma unroll
+    for (int e1 = 0; e1 < L1; ++e1) tileC[(e1 * CB + c) * NPP + p] = v[e1];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int rc = wrp; rc < L1 * CB; rc += nw) {
+    const int e1 = rc / CB, c = rc % CB;
+    double2* Yr = Y + (int64_t(e1) * L2 + e2_0 + c) * np;
+    for (int p = lane; p < np; p += 32) Yr[p] = tileC[rc * NPP + p];
+  }
+}
+
+// Generic path (any smooth L1 <= 1024): one CTA per (CB columns, pair),
+// Stockham stages over shared memory with runtime radices.
 template <int R>
 __device__ __forceinline__ void col_stage(const double2* in, double2* out, int L1, int CB, int Ns,
                                           const double2* __restrict__ tw1) {
@@ -159,21 +259,22 @@ __device__ __forceinline__ void col_stage(const double2* in, double2* out, int L
   }
 }
 
-// In-place inverse DFT of length L1 along f1 for CB adjacent columns e2 of
-// U[p] (layout [f1][e2]); result y[e1][e2] = B'[L2·e1 + e2].
 __global__ void __launch_bounds__(256)
-    k_cols(double2* __restrict__ U, int64_t L, int L1, int L2, int CB,
-           const int32_t* __restrict__ rad, int nrad, const double2* __restrict__ tw1) {
+    k_cols_smem(const double2* __restrict__ U, int64_t L, int L1, int L2, int CB, int np,
+                const int32_t* __restrict__ rad, int nrad, const double2* __restrict__ tw1,
+                const double2* __restrict__ twL, double2* __restrict__ Y) {
   extern __shared__ double2 smem[];
   double2* in = smem;
   double2* out = smem + L1 * CB;
-  const int64_t p = blockIdx.y;
+  const int p = blockIdx.y;
   const int c0 = blockIdx.x * CB;
-  double2* Up = U + p * L + c0;
+  const double2* Up = U + int64_t(p) * L + c0;
   const int tot = L1 * CB;
   for (int q = threadIdx.x; q < tot; q += blockDim.x) {
     const int f1 = q / CB, c = q - f1 * CB;
-    in[q] = Up[int64_t(f1) * L2 + c];
+    const int x = (c0 + c) * f1;
+    const double2 w = cmul(__ldg(&tw1[x / L2]), __ldg(&twL[x % L2]));
+    in[q] = cmulc(Up[int64_t(f1) * L2 + c], w);
   }
   __syncthreads();
   int Ns = 1;
@@ -194,85 +295,158 @@ __global__ void __launch_bounds__(256)
   }
   for (int q = threadIdx.x; q < tot; q += blockDim.x) {
     const int e1 = q / CB, c = q - e1 * CB;
-    Up[int64_t(e1) * L2 + c] = in[q];
+    Y[(int64_t(e1) * L2 + c0 + c) * np + p] = in[q];
   }
 }
 
 // ---------------------------------------------------------------- K3
-// One thread per conventional row n, looping over the pairs of the batch.
+// Grid (row blocks, pair groups): thread = conventional row n, looping over
+// the pairs [g·ppg, (g+1)·ppg) of the batch; B' of all pairs of the batch at
+// reordered index R[n] is contiguous in Y.  ROWSUM mode accumulates
+// Σ_k X[n,k] into rowsum[g·N + n] (reduced over g at the end of the call).
 template <int MODE>
 __global__ void __launch_bounds__(kGatherThreads)
-    k_gather(const double2* __restrict__ U, int64_t L, int npairs, int64_t pair0, int64_t t,
+    k_gather(const double2* __restrict__ Y, int np, int ppg, int64_t pair0, int64_t t,
              const int32_t* __restrict__ R, const double* __restrict__ colsum,
              const double* __restrict__ scal, int64_t N, double* __restrict__ X, int64_t ldx,
              double* __restrict__ rowsum, int first) {
   const int64_t n = int64_t(blockIdx.x) * kGatherThreads + threadIdx.x;
   if (n >= N) return;
-  const double phi0 = __ldg(scal);
-  const int r = n > 0 ? __ldg(&R[n]) : 0;
+  const int g = blockIdx.y;
+  const int pb = g * ppg, pe = min(np, pb + ppg);
   double rs = 0.0;
-  for (int p = 0; p < npairs; ++p) {
-    const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-    const bool has2 = k2 < t;
-    double2 v;
-    if (n == 0) v = make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0);
-    else v = __ldg(&U[int64_t(p) * L + r]);
-    if (X) {
-      X[n + k1 * ldx] = v.x;
-      if (has2) X[n + k2 * ldx] = v.y;
+  if (n == 0) {
+    const double phi0 = __ldg(scal);
+    for (int p = pb; p < pe; ++p) {
+      const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+      const bool has2 = k2 < t;
+      const double2 v = make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0);
+      if (X) {
+        X[k1 * ldx] = v.x;
+        if (has2) X[k2 * ldx] = v.y;
+      }
+      rs += v.x;
+      if (has2) rs += v.y;
     }
-    if (MODE == GM_ROWSUM) {
+  } else {
+    const double2* yp = Y + int64_t(__ldg(&R[n])) * np;
+    double* Xn = X ? X + n + 2 * pair0 * ldx : nullptr;
+    int p = pb;
+    constexpr int U8 = 8;
+    const bool al32 = ((np | pb) & 1) == 0;  // yp + p 32-byte aligned
+    for (; p + U8 <= pe && 2 * (pair0 + p + U8 - 1) + 1 < t; p += U8) {
+      double2 v[U8];
+      if (al32) {
+#pragma unroll
+        for (int i = 0; i < U8; i += 2) QMC_LD2(&yp[p + i], v[i], v[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < U8; ++i) v[i] = QMC_LD1(&yp[p + i]);
+      }
+#pragma unroll
+      for (int i = 0; i < U8; ++i) {
+        if (Xn) {
+          QMC_ST(&Xn[(2 * (p + i)) * ldx], v[i].x);
+          QMC_ST(&Xn[(2 * (p + i) + 1) * ldx], v[i].y);
+        }
+        rs += v[i].x;
+        rs += v[i].y;
+      }
+    }
+    for (; p < pe; ++p) {
+      const int64_t k2 = 2 * (pair0 + p) + 1;
+      const bool has2 = k2 < t;
+      const double2 v = __ldg(&yp[p]);
+      if (Xn) {
+        Xn[(2 * p) * ldx] = v.x;
+        if (has2) Xn[(2 * p + 1) * ldx] = v.y;
+      }
       rs += v.x;
       if (has2) rs += v.y;
     }
   }
-  if (MODE == GM_ROWSUM) rowsum[n] = (first ? 0.0 : rowsum[n]) + rs;
+  if (MODE == GM_ROWSUM) {
+    double* rsg = rowsum + int64_t(g) * N;
+    rsg[n] = (first ? 0.0 : rsg[n]) + rs;
+  }
 }
 
-// Per (row block, pair): writes X (c + X for AFFINE) and Σ_rows f(X) per
-// column into partial[nb·t + k].
+__global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int64_t N, double* __restrict__ out) {
+  const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (n >= N) return;
+  double s = 0.0;
+  for (int g = 0; g < ng; ++g) s += parts[int64_t(g) * N + n];
+  out[n] = s;
+}
+
+// Grid (row blocks of kColMeanRows, pair groups): writes X (c + X for
+// AFFINE) and the per-column block sums of f(X) into partial[nb·t + k]
+// (warp shuffles, then a fixed-order sum over warps).
 template <int F>
 __global__ void __launch_bounds__(kGatherThreads)
-    k_gather_colmean(const double2* __restrict__ U, int64_t L, int64_t pair0, int64_t t,
+    k_gather_colmean(const double2* __restrict__ Y, int np, int ppg, int64_t pair0, int64_t t,
                      const int32_t* __restrict__ R, const double* __restrict__ colsum,
                      const double* __restrict__ scal, int64_t N, double fparam,
                      double* __restrict__ X, int64_t ldx, double* __restrict__ partial) {
-  __shared__ double2 red[kGatherThreads / 32];
+  extern __shared__ double2 red[];  // [kGatherThreads/32][ppg]
+  constexpr int RPT = kColMeanRows / kGatherThreads;
   const int64_t nb = blockIdx.x;
-  const int p = blockIdx.y;
-  const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-  const bool has2 = k2 < t;
+  const int g = blockIdx.y;
+  const int pb = g * ppg, pe = min(np, pb + ppg);
   const double phi0 = __ldg(scal);
-  const double2* Up = U + int64_t(p) * L;
-  double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
-  for (int i = 0; i < kColMeanRows / kGatherThreads; ++i) {
-    const int64_t n = nb * kColMeanRows + i * kGatherThreads + threadIdx.x;
-    if (n < N) {
-      double2 v;
-      if (n == 0) v = make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0);
-      else v = __ldg(&Up[__ldg(&R[n])]);
-      if (F == QMC_F_AFFINE) {
-        v.x += fparam;
-        v.y += fparam;
-      }
-      if (X) {
-        X[n + k1 * ldx] = v.x;
-        if (has2) X[n + k2 * ldx] = v.y;
-      }
-      if (F == QMC_F_EXP) {
-        acc.x += exp(v.x);
-        acc.y += exp(v.y);
-      } else {
-        acc.x += v.x;
-        acc.y += v.y;
+  int64_t rows[RPT];
+  int rr[RPT];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    rows[i] = nb * kColMeanRows + i * kGatherThreads + threadIdx.x;
+    rr[i] = (rows[i] > 0 && rows[i] < N) ? __ldg(&R[rows[i]]) : 0;
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  for (int p = pb; p < pe; ++p) {
+    const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+    const bool has2 = k2 < t;
+    double2 vv[RPT];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i)
+      vv[i] = rows[i] == 0 ? make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0)
+              : rows[i] < N ? __ldg(&Y[int64_t(rr[i]) * np + p]) : make_double2(0.0, 0.0);
+    double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const int64_t n = rows[i];
+      if (n < N) {
+        double2 v = vv[i];
+        if (F == QMC_F_AFFINE) {
+          v.x += fparam;
+          v.y += fparam;
+        }
+        if (X) {
+          X[n + k1 * ldx] = v.x;
+          if (has2) X[n + k2 * ldx] = v.y;
+        }
+        if (F == QMC_F_EXP) {
+          acc.x += exp(v.x);
+          if (has2) acc.y += exp(v.y);
+        } else {
+          acc.x += v.x;
+          if (has2) acc.y += v.y;
+        }
       }
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
+    }
+    if (l == 0) red[w * ppg + (p - pb)] = acc;
   }
-  acc = block_sum2<kGatherThreads>(acc, red);
-  if (threadIdx.x == 0) {
-    partial[nb * t + k1] = acc.x;
-    if (has2) partial[nb * t + k2] = acc.y;
+  __syncthreads();
+  for (int p = pb + threadIdx.x; p < pe; p += kGatherThreads) {
+    double2 sacc = make_double2(0.0, 0.0);
+    for (int ww = 0; ww < kGatherThreads / 32; ++ww) sacc = cadd(sacc, red[ww * ppg + (p - pb)]);
+    const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+    partial[nb * t + k1] = sacc.x;
+    if (k2 < t) partial[nb * t + k2] = sacc.y;
   }
 }
 
@@ -304,8 +478,18 @@ __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int
 
 // ---------------------------------------------------------------- host side
 struct CallLayout {
-  size_t off_Ab, off_U, off_colsum, off_partial, total;
+  size_t off_U, off_Y, off_colsum, off_partial, off_rowsum, total;
+  int ngroups, ppg;
 };
+
+// pair groups of the gather: enough rows × groups for ~2 waves of threads
+static void gather_groups(const qmc_plan* pl, int64_t pairs, int* ngroups, int* ppg) {
+  int64_t g = std::max<int64_t>(1, (int64_t(148) * 2048 * 2) / std::max<int64_t>(pl->N, 1));
+  g = std::min<int64_t>(g, pairs);
+  const int64_t per = (pairs + g - 1) / g;
+  *ppg = int(per);
+  *ngroups = int((pairs + per - 1) / per);
+}
 
 static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   CallLayout c;
@@ -316,51 +500,94 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
     o = align_up(o + b);
     return r;
   };
-  c.off_Ab = take(size_t(pairs) * pl->s * 16);
   c.off_U = take(size_t(pairs) * pl->sp.L * 16);
+  c.off_Y = take(size_t(pairs) * pl->sp.L * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int64_t nblocks = (pl->N + kColMeanRows - 1) / kColMeanRows;
   c.off_partial = take(colmean ? size_t(nblocks) * std::max<int64_t>(t, 1) * 8 : 0);
+  gather_groups(pl, pairs, &c.ngroups, &c.ppg);
+  c.off_rowsum = take(f == QMC_F_ROWMEAN_RELU ? size_t(c.ngroups) * pl->N * 8 : 0);
   c.total = o;
   return c;
 }
 
+template <typename K>
+static void set_smem_attr(K kernel) {
+  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+}
+
 template <int L2>
-static int launch_rows(const qmc_plan* pl, const double2* Ab, double2* U, int npairs, cudaStream_t st) {
-  const size_t smem = size_t(L2 + pl->sp.L1) * sizeof(double2);
-  static bool attr_done = false;  // per template instance
-  if (!attr_done) {
-    cudaFuncSetAttribute(k_rows<L2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_done = true;
-  }
+static int launch_rows(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0,
+                       double2* U, int npairs, double* colsum, cudaStream_t st) {
+  const size_t smem = size_t(PadE<L2, QMC_ROW_E>::size) * sizeof(double2);
+  set_smem_attr(k_rows16<L2>);
   dim3 grid((unsigned)pl->sp.L1, (unsigned)npairs);
-  k_rows<L2><<<grid, RowThreads<L2>::value, smem, st>>>(Ab, pl->s, pl->d_bstart, pl->d_be1, pl->d_tw1,
-                                                        pl->d_twL, pl->d_tw2, pl->d_W, U, pl->sp.L,
-                                                        int(pl->sp.L1));
+  k_rows16<L2><<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj,
+                                                   pl->d_tws, pl->d_W, U, pl->sp.L, colsum);
   QMC_LAUNCHED();
   return QMC_OK;
 }
 
-static int rows_dispatch(const qmc_plan* pl, const double2* Ab, double2* U, int npairs, cudaStream_t st) {
+static int rows_dispatch(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0, double2* U,
+                         int np, double* colsum, cudaStream_t st) {
   switch (pl->sp.L2) {
-    case 16: return launch_rows<16>(pl, Ab, U, npairs, st);
-    case 32: return launch_rows<32>(pl, Ab, U, npairs, st);
-    case 64: return launch_rows<64>(pl, Ab, U, npairs, st);
-    case 128: return launch_rows<128>(pl, Ab, U, npairs, st);
-    case 256: return launch_rows<256>(pl, Ab, U, npairs, st);
-    case 512: return launch_rows<512>(pl, Ab, U, npairs, st);
-    case 1024: return launch_rows<1024>(pl, Ab, U, npairs, st);
-    case 2048: return launch_rows<2048>(pl, Ab, U, npairs, st);
-    case 4096: return launch_rows<4096>(pl, Ab, U, npairs, st);
-    case 8192: return launch_rows<8192>(pl, Ab, U, npairs, st);
+#define QMC_ROWS_CASE(NN) \
+  case NN: return launch_rows<NN>(pl, A, lda, t, pair0, U, np, colsum, st);
+    QMC_ROWS_CASE(16) QMC_ROWS_CASE(32) QMC_ROWS_CASE(64) QMC_ROWS_CASE(128) QMC_ROWS_CASE(256)
+    QMC_ROWS_CASE(512) QMC_ROWS_CASE(1024) QMC_ROWS_CASE(2048) QMC_ROWS_CASE(4096) QMC_ROWS_CASE(8192)
+#undef QMC_ROWS_CASE
   }
   return QMC_EINVAL_N;
 }
 
+static int ilog2(int64_t x) {
+  int r = 0;
+  while ((int64_t(1) << r) < x) ++r;
+  return r;
+}
+
+size_t cols_reg_smem(int64_t L1, int64_t np) {
+  const int64_t npp = np + ((2 - np % 8) + 8) % 8;  // ≡ 2 (mod 8)
+  return size_t(L1 * kColCB + np * kColCB * (L1 + 2) + L1 * kColCB * npp) * 16;
+}
+
+template <int L1>
+static int launch_cols_reg(const qmc_plan* pl, const double2* U, double2* Y, int np, cudaStream_t st) {
+  const size_t smem = cols_reg_smem(L1, np);
+  const int npp = np + ((2 - np % 8) + 8) % 8;
+  set_smem_attr(k_cols_reg<L1>);
+  dim3 g((unsigned)(pl->sp.L2 / kColCB), 1);
+  k_cols_reg<L1><<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp, pl->d_tw1,
+                                       pl->d_twL, Y);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
+static int cols_dispatch(const qmc_plan* pl, const double2* U, double2* Y, int np, cudaStream_t st) {
+  if (pl->col_reg) {
+    switch (pl->sp.L1) {
+#define QMC_COLS_CASE(NN) \
+  case NN: return launch_cols_reg<NN>(pl, U, Y, np, st);
+      QMC_COLS_CASE(2) QMC_COLS_CASE(3) QMC_COLS_CASE(4) QMC_COLS_CASE(5) QMC_COLS_CASE(6) QMC_COLS_CASE(8)
+      QMC_COLS_CASE(9) QMC_COLS_CASE(10) QMC_COLS_CASE(12) QMC_COLS_CASE(15) QMC_COLS_CASE(16) QMC_COLS_CASE(20)
+      QMC_COLS_CASE(24) QMC_COLS_CASE(25) QMC_COLS_CASE(32)
+#undef QMC_COLS_CASE
+    }
+  }
+  const int CB = pl->col_cb_smem;
+  const size_t smem = size_t(2) * pl->sp.L1 * CB * sizeof(double2);
+  set_smem_attr(k_cols_smem);
+  dim3 g((unsigned)(pl->sp.L2 / CB), (unsigned)np);
+  k_cols_smem<<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L1), int(pl->sp.L2), CB, np, pl->d_rad1, pl->nrad1,
+                                    pl->d_tw1, pl->d_twL, Y);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
 static unsigned nblk(int64_t n, int b) { return unsigned((n + b - 1) / b); }
 
-// core: all batches; mode: -1 = X only, else f
+// all batches of column pairs; f = -1: X only
 static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int f, double fparam,
                double* out, double* X, int64_t ldx, void* call_ws, size_t call_ws_bytes, cudaStream_t st) {
   if (!pl) return QMC_ENULL;
@@ -373,64 +600,75 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   const CallLayout cl = call_layout(pl, t, f);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
-  double2* Ab = (double2*)(ws + cl.off_Ab);
   double2* U = (double2*)(ws + cl.off_U);
+  double2* Y = (double2*)(ws + cl.off_Y);
   double* colsum = (double*)(ws + cl.off_colsum);
   double* partial = (double*)(ws + cl.off_partial);
+  double* rowparts = (double*)(ws + cl.off_rowsum);
   const int64_t npairs_total = (t + 1) / 2;
   const int64_t nb3 = (pl->N + kColMeanRows - 1) / kColMeanRows;
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
-  static bool cols_attr = false;
-  if (!cols_attr) {
-    cudaFuncSetAttribute(k_cols, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cols_attr = true;
-  }
   for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs) {
     const int np = int(std::min<int64_t>(pl->batch_pairs, npairs_total - pair0));
-    prof_begin(KC_PACK, st);
-    k_pack<<<np, kPackThreads, 0, st>>>(A, lda, t, pair0, pl->s, pl->d_bidx, Ab, colsum);
-    QMC_LAUNCHED();
-    prof_end(KC_PACK, st);
     prof_begin(KC_ROWS, st);
-    int rc = rows_dispatch(pl, Ab, U, np, st);
+    int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, st);
     if (rc) return rc;
     prof_end(KC_ROWS, st);
+    const double2* Yb = U;
     if (pl->sp.L1 > 1) {
-      dim3 g((unsigned)(pl->sp.L2 / pl->col_cb), (unsigned)np);
-      const size_t smem = size_t(2) * pl->sp.L1 * pl->col_cb * sizeof(double2);
       prof_begin(KC_COLS, st);
-      k_cols<<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L1), int(pl->sp.L2), pl->col_cb, pl->d_rad1,
-                                   pl->nrad1, pl->d_tw1);
-      QMC_LAUNCHED();
+      rc = cols_dispatch(pl, U, Y, np, st);
+      if (rc) return rc;
       prof_end(KC_COLS, st);
+      Yb = Y;
+    } else if (np > 1) {
+      // L1 = 1: B' = U; interleave pairs for the gather
+      prof_begin(KC_COLS, st);
+      rc = cols_dispatch(pl, U, Y, np, st);
+      if (rc) return rc;
+      prof_end(KC_COLS, st);
+      Yb = Y;
     }
     prof_begin(KC_GATHER, st);
+    const int ppg = cl.ppg;
+    const unsigned ng = unsigned((np + ppg - 1) / ppg);
     if (colmean) {
-      dim3 g((unsigned)nb3, (unsigned)np);
+      const size_t smem = size_t(kGatherThreads / 32) * ppg * sizeof(double2);
+      dim3 g((unsigned)nb3, ng);
       switch (f) {
         case QMC_F_IDENTITY:
-          k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, 0, st>>>(U, pl->sp.L, pair0, t, pl->d_R, colsum,
-                                                                        pl->d_scal, pl->N, fparam, X, ldx, partial);
+          k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, smem, st>>>(
+              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
           break;
         case QMC_F_AFFINE:
-          k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, 0, st>>>(U, pl->sp.L, pair0, t, pl->d_R, colsum,
-                                                                      pl->d_scal, pl->N, fparam, X, ldx, partial);
+          k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, smem, st>>>(
+              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
           break;
         default:
-          k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, 0, st>>>(U, pl->sp.L, pair0, t, pl->d_R, colsum,
-                                                                   pl->d_scal, pl->N, fparam, X, ldx, partial);
+          k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, smem, st>>>(
+              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
       }
       QMC_LAUNCHED();
     } else if (f == QMC_F_ROWMEAN_RELU) {
-      k_gather<GM_ROWSUM><<<nblk(pl->N, kGatherThreads), kGatherThreads, 0, st>>>(
-          U, pl->sp.L, np, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X, ldx, out, pair0 == 0);
+      // groups absent from a short last batch keep their sums (first = 0)
+      dim3 g(nblk(pl->N, kGatherThreads), ng);
+      k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
+                                                        pl->N, X, ldx, rowparts, pair0 == 0);
       QMC_LAUNCHED();
     } else {
-      k_gather<GM_X><<<nblk(pl->N, kGatherThreads), kGatherThreads, 0, st>>>(
-          U, pl->sp.L, np, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X, ldx, nullptr, 0);
+      dim3 g(nblk(pl->N, kGatherThreads), ng);
+      k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
+                                                   ldx, nullptr, 0);
       QMC_LAUNCHED();
     }
     prof_end(KC_GATHER, st);
+  }
+  if (f == QMC_F_ROWMEAN_RELU) {
+    prof_begin(KC_REDUCE, st);
+    const int ngr = int(std::min<int64_t>(cl.ngroups, (npairs_total + cl.ppg - 1) / cl.ppg));
+    k_rowsum_reduce<<<nblk(pl->N, 256), 256, 0, st>>>(rowparts, ngr, pl->N, out);
+    QMC_LAUNCHED();
+    prof_end(KC_REDUCE, st);
   }
   if (colmean) {
     prof_begin(KC_REDUCE, st);

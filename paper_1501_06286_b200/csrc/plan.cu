@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -23,6 +24,7 @@
 
 #include "fft.cuh"
 #include "qmc_internal.cuh"
+#include "rowcfg.cuh"
 
 namespace qmc {
 
@@ -95,7 +97,7 @@ bool choose_split(int64_t m, int64_t s, Split* out) {
   auto try_len = [&](int64_t len) -> bool {
     int64_t l2 = 1;
     while (len % (l2 * 2) == 0 && l2 * 2 <= cap) l2 *= 2;
-    if (l2 < 16) return false;
+    if (l2 < 16 || (l2 < 256 && l2 != len)) return false;  // rows of >= 256, or one short row
     int64_t l1 = len / l2;
     if (l1 > 1024 || !smooth235(l1)) return false;
     out->L = len;
@@ -129,13 +131,15 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_R = take(size_t(N) * 4);
   l.off_e = take(size_t(s) * 4);
   l.off_bstart = take(size_t(sp.L2 + 1) * 4);
-  l.off_bidx = take(size_t(s) * 4);
-  l.off_be1 = take(size_t(s) * 4);
+  l.off_bent = take(size_t(s) * 16);
+  l.off_bnext = take(size_t(s) * 4);
   l.off_zeta = take(size_t(m) * 8);
   l.off_W = take(size_t(sp.L) * 16);
   l.off_tw1 = take(size_t(sp.L1) * 16);
   l.off_tw2 = take(size_t(sp.L2) * 16);
   l.off_twL = take(size_t(sp.L2) * 16);
+  l.off_tws = take(size_t(sp.L2) * 16);
+  l.off_twj = take(size_t(sp.L1) * size_t(s) * 16);
   l.off_radix1 = take(24 * 4);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
   l.total = o;
@@ -248,7 +252,7 @@ __global__ void k_colmap(const int64_t* __restrict__ z, int64_t s, const int32_t
 
 // Stable counting sort of j by e2 = e_j mod L2 (one CTA; plan time only).
 __global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ bstart,
-                          int32_t* __restrict__ bidx, int32_t* __restrict__ be1) {
+                          int4* __restrict__ bent, int32_t* __restrict__ bnext) {
   extern __shared__ int32_t cursor[];
   for (int i = threadIdx.x; i <= L2; i += blockDim.x) bstart[i] = 0;
   __syncthreads();
@@ -260,9 +264,19 @@ __global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int3
     for (int64_t j = 0; j < s; ++j) {
       const int ej = e[j];
       const int pos = cursor[ej & (L2 - 1)]++;
-      bidx[pos] = int32_t(j);
-      be1[pos] = ej / L2;
+      const int e2 = ej & (L2 - 1);
+      bent[pos] = make_int4(int(j), ej, e2, pos == bstart[e2] ? bstart[e2 + 1] : -1);
     }
+    // collision chains in increasing j (entries of a bucket are in j order)
+    for (int i = 0; i < L2; ++i)
+      for (int pos = bstart[i]; pos < bstart[i + 1]; ++pos)
+        bnext[bent[pos].x] = pos == bstart[i] ? (pos + 1 < bstart[i + 1] ? bent[pos + 1].x : -1)
+                                              : -2;
+    // non-first entries point to the next one too: chain walk uses bnext of
+    // the first only for the head; encode followers as -(next)-3
+    for (int i = 0; i < L2; ++i)
+      for (int pos = bstart[i] + 1; pos < bstart[i + 1]; ++pos)
+        bnext[bent[pos].x] = pos + 1 < bstart[i + 1] ? -(bent[pos + 1].x) - 3 : -2;
   }
 }
 
@@ -289,6 +303,39 @@ __global__ void k_twiddles(double2* __restrict__ tw, int64_t n, int64_t count) {
   double sv, cv;
   sincospi(2.0 * double(k) / double(n), &sv, &cv);
   tw[k] = make_double2(cv, -sv);
+}
+
+// Stage-major twiddles of the register row FFT (fft.cuh R16Plan: radix 16
+// stages, then one radix-2/4/8 stage): for stage i >= 1 with span NS and
+// radix R, tws[off_i + (r-1)·NS + k] = ω_{NS·R}^{k·r}, k < NS, 1 <= r < R.
+__global__ void k_stage_twiddles(double2* __restrict__ tws, int N, int E) {
+  int ns = N >= E ? E : N, off = 0, rem = N / ns;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  while (rem > 1) {
+    const int R = rem >= E ? E : rem;
+    const int cnt = ns * (R - 1);
+    if (idx >= off && idx < off + cnt) {
+      const int r = (idx - off) / ns + 1, k = (idx - off) % ns;
+      double sv, cv;
+      sincospi(2.0 * double(k * r) / double(ns * R), &sv, &cv);
+      tws[idx] = make_double2(cv, -sv);
+    }
+    off += cnt;
+    ns *= R;
+    rem /= R;
+  }
+}
+
+// twj[f1·s + j] = ω_L^{(e_j·f1) mod L}: the twiddle of entry j in row f1 of
+// the scatter fused with the first DFT dimension (K1)
+__global__ void k_twj(const int32_t* __restrict__ e, int64_t s, int64_t L, int L1, double2* __restrict__ twj) {
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= s * L1) return;
+  const int64_t f1 = i / s, j = i % s;
+  const int64_t x = (int64_t(e[j]) * f1) % L;
+  double sv, cv;
+  sincospi(2.0 * double(x) / double(L), &sv, &cv);
+  twj[i] = make_double2(cv, -sv);
 }
 
 // W[f1*L2 + f2] = DFT_L(K)[f1 + L1·f2] / L with the correlation kernel
@@ -419,10 +466,30 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->stream = (cudaStream_t)stream;
   pl->ws = (char*)plan_ws;
   pl->ws_bytes = plan_ws_bytes;
-  pl->batch_pairs = std::max<int64_t>(1, std::min<int64_t>(256, (int64_t(40) << 20) / (sp.L * 16)));
-  int cb = 32;
-  while (cb > 1 && (int64_t(cb) * sp.L1 > 2048 || cb > sp.L2)) cb >>= 1;
-  pl->col_cb = cb;
+  {
+    // two scratch buffers of batch·L complex each, sized to stay in L2
+    // (~64 MB); at least two waves of row CTAs when that fits in ~96 MB
+    const int64_t per_pair = 32 * sp.L;
+    int64_t bp = std::max<int64_t>(1, (int64_t(64) << 20) / per_pair);
+    const int64_t want = (296 + sp.L1 - 1) / sp.L1;
+    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(96) << 20) / per_pair));
+    pl->batch_pairs = std::min<int64_t>(bp, 256);
+    if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
+      const long v = strtol(ev, nullptr, 10);
+      if (v > 0) pl->batch_pairs = v;
+    }
+  }
+  {
+    int cb = 32;
+    while (cb > 1 && (int64_t(cb) * sp.L1 > 2048 || cb > sp.L2)) cb >>= 1;
+    pl->col_cb_smem = cb;
+    const int64_t L1 = sp.L1;
+    const bool reg_len = L1 == 2 || L1 == 3 || L1 == 4 || L1 == 5 || L1 == 6 || L1 == 8 || L1 == 9 ||
+                         L1 == 10 || L1 == 12 || L1 == 15 || L1 == 16 || L1 == 20 || L1 == 24 || L1 == 25 ||
+                         L1 == 32;
+    pl->col_cb = 4;
+    pl->col_reg = reg_len && sp.L2 >= 4 && cols_reg_smem(L1, pl->batch_pairs) <= (200u << 10);
+  }
   rc = pick_radices(sp.L1, pl->rad1, &pl->nrad1);
   if (rc) { delete pl; return rc; }
   char* b = pl->ws;
@@ -432,13 +499,15 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_R = (int32_t*)(b + lay.off_R);
   pl->d_e = (int32_t*)(b + lay.off_e);
   pl->d_bstart = (int32_t*)(b + lay.off_bstart);
-  pl->d_bidx = (int32_t*)(b + lay.off_bidx);
-  pl->d_be1 = (int32_t*)(b + lay.off_be1);
+  pl->d_bent = (int4*)(b + lay.off_bent);
+  pl->d_bnext = (int32_t*)(b + lay.off_bnext);
   pl->d_zeta = (double*)(b + lay.off_zeta);
   pl->d_W = (double2*)(b + lay.off_W);
   pl->d_tw1 = (double2*)(b + lay.off_tw1);
   pl->d_tw2 = (double2*)(b + lay.off_tw2);
   pl->d_twL = (double2*)(b + lay.off_twL);
+  pl->d_tws = (double2*)(b + lay.off_tws);
+  pl->d_twj = (double2*)(b + lay.off_twj);
   pl->d_rad1 = (int32_t*)(b + lay.off_radix1);
   cudaStream_t st = pl->stream;
 
@@ -501,7 +570,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_colmap<<<blocks(s, 256), 256, 0, st>>>(d_z, s, pl->d_L, pl->d_e);
   QMC_PLAN_LAUNCHED();
-  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bidx, pl->d_be1);
+  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bent, pl->d_bnext);
   QMC_PLAN_LAUNCHED();
   k_rtable<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, m, pl->d_R);
   QMC_PLAN_LAUNCHED();
@@ -513,6 +582,10 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   k_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tw2, sp.L2, sp.L2);
   QMC_PLAN_LAUNCHED();
   k_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_twL, sp.L, sp.L2);
+  QMC_PLAN_LAUNCHED();
+  k_stage_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tws, int(sp.L2), QMC_ROW_E);
+  QMC_PLAN_LAUNCHED();
+  k_twj<<<blocks(sp.L1 * s, 256), 256, 0, st>>>(pl->d_e, s, sp.L, int(sp.L1), pl->d_twj);
   QMC_PLAN_LAUNCHED();
   QMC_PLAN_CHECK(spectrum_dispatch(pl));
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);

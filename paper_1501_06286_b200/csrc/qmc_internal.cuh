@@ -51,10 +51,13 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // Plan-workspace carve-up (device pointers), identical for the size query
 // and the create call.
 struct PlanLayout {
-  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bidx, off_be1, off_zeta, off_W,
-      off_tw1, off_tw2, off_twL, off_radix1, off_tmp, total;
+  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_bnext, off_zeta, off_W,
+      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_radix1, off_tmp, total;
 };
 PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
+
+// shared memory of the register column kernel for a batch of np pairs
+size_t cols_reg_smem(int64_t L1, int64_t np);
 
 }  // namespace qmc
 
@@ -67,7 +70,9 @@ struct qmc_plan {
   int64_t gen;
   qmc::Split sp;
   int64_t batch_pairs;  // column pairs per batch (scratch sized to stay in L2)
-  int col_cb;           // column-FFT block width (K2)
+  int col_reg;          // K2 register path (L1 <= 32, two direct radices)
+  int col_cb;           // K2 register path: columns e2 per CTA
+  int col_cb_smem;      // K2 shared-memory path: columns e2 per CTA
   int nrad1;            // radices of L1
   int rad1[24];
   cudaStream_t stream;
@@ -80,12 +85,16 @@ struct qmc_plan {
   int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1
   int32_t* d_e;      // [s]
   int32_t* d_bstart; // [L2+1]
-  int32_t* d_bidx;   // [s]   j in bucket order (e2 = e_j mod L2, then j)
-  int32_t* d_be1;    // [s]   e_j / L2 in bucket order
+  int32_t* d_bnext;  // [s]   per j: -2 if j is not the smallest index of its bucket
+                     //       (e2 = e_j mod L2), else the next j of the bucket (-1: none)
+  int4* d_bent;      // [s]   bucket order (e2 = e_j mod L2, then j): {j, e_j, e2,
+                     //       end of this bucket if the entry is its first, else -1}
   double* d_zeta;    // [m]
   double2* d_W;      // [L]   W[f1*L2 + f2] = DFT_L(K)[f1 + L1 f2] / L
   double2* d_tw1;    // [L1]  ω_{L1}^k
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
+  double2* d_tws;    // [L2]  row-FFT stage twiddles, stage-major (fft.cuh reg_stage)
+  double2* d_twj;    // [L1·s] twj[f1·s + j] = ω_L^{(e_j·f1) mod L} (K1 scatter twiddles)
   int32_t* d_rad1;   // [24]
 };
