@@ -182,12 +182,11 @@ def ours(args, rank, world, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    from paper_1501_06286_b200.dist import combine_means, shard_columns
     w = W.config(args.config)
     G = world
-    if w.t % G:
-        raise SystemExit(f"t={w.t} not divisible by {G}")
-    tl = w.t // G
-    c0, c1 = rank * tl, (rank + 1) * tl
+    c0, c1 = shard_columns(w.t, G, rank)
+    tl = c1 - c0
     plan = q.Plan.from_workload(w, device=dev)
     A_host = np.ascontiguousarray(w.A[:, c0:c1].T)          # (tl, s) row-major = A slab col-major
     A = torch.from_numpy(A_host).to(dev).t()
@@ -199,24 +198,20 @@ def ours(args, rank, world, local_rank):
         res = torch.empty(1, dtype=torch.float64, device=dev)
     elif f is not None:
         out = torch.empty(tl, dtype=torch.float64, device=dev)
-        res = torch.empty(w.t, dtype=torch.float64, device=dev)
     plan.call_workspace(tl, -1 if f is None else f)
 
     def step():
+        """One pass of the hot path over this rank's column slab + the
+        collective of the fused mean (dist.combine_means) + finalize."""
         if f is None:
             plan.matmul(A, X)
             return None
         plan.mean(A, f, fp, X=X, out=out)
+        red = combine_means(out, f, w.t, c0)
         if f == W.F_ROWMEAN_RELU:
-            if G > 1:
-                dist.all_reduce(out)
-            plan.finalize(f, out, w.t, out=res)
-        else:
-            if G > 1:
-                dist.all_gather_into_tensor(res, out)     # zero-padded allreduce == allgather (R11)
-            else:
-                res.copy_(out)
-        return res
+            plan.finalize(f, red, w.t, out=res)
+            return res
+        return red
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     for _ in range(args.warmup):

@@ -158,7 +158,7 @@ int64_t qmc_launch_count(void);
 
 /* Per-kernel-class timing for roofline reporting.  qmc_profile_enable(1)
  * makes every later hot-path call record CUDA events on its stream around
- * each launch class (k_pack, k_rows, k_cols, k_gather, k_colmean_reduce,
+ * each launch class (k_pack, k_rows, k_cols, k_gather, k_reduce,
  * k_finalize — qmc_profile_class_name(i) for i = 0..5).  qmc_profile_read
  * waits for those events and returns, per class i < n, the number of
  * timed launches (one "launch" of k_rows = the launch for one batch) and

@@ -24,7 +24,11 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
+
+#include <cooperative_groups.h>
 
 #include "fft.cuh"
 #include "qmc_internal.cuh"
@@ -93,12 +97,19 @@ extern "C" int qmc_debug_phases(long long* host, int n) {
   do {            \
   } while (0)
 #endif
-template <int L2>
-__global__ void __launch_bounds__(L2 / QMC_ROW_E, QMC_ROWS_MINB)
+// L1C = 0: write U[p][f1][e2] (the column pass runs in K2).
+// L1C = L1 > 0: the grid's x-dimension (f1) is one thread-block cluster of
+// L1 CTAs; after the row transforms every CTA keeps its row in shared memory
+// and computes, for its share of the columns e2, the twiddle
+// conj(ω_L^{e2 f1}) and the inverse DFT over f1 from the L1 rows read
+// through distributed shared memory, writing B'[p][L2·e1 + e2] (natural).
+template <int L2, int L1C>
+__global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : QMC_ROWS_MINB))
     k_rows16(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
              const int32_t* __restrict__ e, const int32_t* __restrict__ bnext, int64_t s,
              const double2* __restrict__ twj, const double2* __restrict__ tws,
-             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum) {
+             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum,
+             const double2* __restrict__ twL, const double2* __restrict__ tw1) {
   extern __shared__ double2 smem[];
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
@@ -166,9 +177,36 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, QMC_ROWS_MINB)
   QMC_TS(3);
   fftE<L2, E, +1>(v, S, tws, tid);
   QMC_TS(4);
-  double2* Ur = U + p * L + int64_t(f1) * L2;
+  if constexpr (L1C == 0) {
+    double2* Ur = U + p * L + int64_t(f1) * L2;
 #pragma unroll
-  for (int q = 0; q < E; ++q) Ur[tid + q * NT] = v[q];
+    for (int q = 0; q < E; ++q) Ur[tid + q * NT] = v[q];
+  } else {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    __syncthreads();  // every thread has finished reading S in the last stage
+    store_strided<L2, E>(v, S);
+    cluster.sync();
+    const double2* Sr[L1C];
+#pragma unroll
+    for (int r = 0; r < L1C; ++r) Sr[r] = cluster.map_shared_rank(S, r);
+    double2* Bp = U + p * L;
+    for (int c = f1 * NT + tid; c < L2; c += L1C * NT) {
+      double2 u[L1C], pw[L1C];
+      pw[0] = make_double2(1.0, 0.0);
+      if (L1C > 1) pw[1] = __ldg(&twL[c]);  // ω_L^{c}
+#pragma unroll
+      for (int r = 2; r < L1C; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
+#pragma unroll
+      for (int r = 0; r < L1C; ++r) u[r] = Sr[r][padE<E>(c)];
+#pragma unroll
+      for (int r = 1; r < L1C; ++r) u[r] = cmulc(u[r], pw[r]);
+      reg_dft<L1C, +1>(u, tw1);
+#pragma unroll
+      for (int r = 0; r < L1C; ++r) Bp[int64_t(r) * L2 + c] = u[r];
+    }
+    cluster.sync();  // keep this CTA's row alive until every reader is done
+  }
   QMC_TS(5);
 }
 
@@ -306,7 +344,7 @@ __global__ void __launch_bounds__(256)
 // Σ_k X[n,k] into rowsum[g·N + n] (reduced over g at the end of the call).
 template <int MODE>
 __global__ void __launch_bounds__(kGatherThreads)
-    k_gather(const double2* __restrict__ Y, int np, int ppg, int64_t pair0, int64_t t,
+    k_gather(const double2* __restrict__ Y, int64_t sE, int64_t sP, int np, int ppg, int64_t pair0, int64_t t,
              const int32_t* __restrict__ R, const double* __restrict__ colsum,
              const double* __restrict__ scal, int64_t N, double* __restrict__ X, int64_t ldx,
              double* __restrict__ rowsum, int first) {
@@ -329,11 +367,11 @@ __global__ void __launch_bounds__(kGatherThreads)
       if (has2) rs += v.y;
     }
   } else {
-    const double2* yp = Y + int64_t(__ldg(&R[n])) * np;
+    const double2* yp = Y + int64_t(__ldg(&R[n])) * sE;
     double* Xn = X ? X + n + 2 * pair0 * ldx : nullptr;
     int p = pb;
     constexpr int U8 = 8;
-    const bool al32 = ((np | pb) & 1) == 0;  // yp + p 32-byte aligned
+    const bool al32 = sP == 1 && ((np | pb) & 1) == 0;  // interleaved and yp + p 32-byte aligned
     for (; p + U8 <= pe && 2 * (pair0 + p + U8 - 1) + 1 < t; p += U8) {
       double2 v[U8];
       if (al32) {
@@ -341,7 +379,7 @@ __global__ void __launch_bounds__(kGatherThreads)
         for (int i = 0; i < U8; i += 2) QMC_LD2(&yp[p + i], v[i], v[i + 1]);
       } else {
 #pragma unroll
-        for (int i = 0; i < U8; ++i) v[i] = QMC_LD1(&yp[p + i]);
+        for (int i = 0; i < U8; ++i) v[i] = QMC_LD1(&yp[(p + i) * sP]);
       }
 #pragma unroll
       for (int i = 0; i < U8; ++i) {
@@ -356,7 +394,7 @@ __global__ void __launch_bounds__(kGatherThreads)
     for (; p < pe; ++p) {
       const int64_t k2 = 2 * (pair0 + p) + 1;
       const bool has2 = k2 < t;
-      const double2 v = __ldg(&yp[p]);
+      const double2 v = __ldg(&yp[p * sP]);
       if (Xn) {
         Xn[(2 * p) * ldx] = v.x;
         if (has2) Xn[(2 * p + 1) * ldx] = v.y;
@@ -384,7 +422,7 @@ __global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int64_
 // (warp shuffles, then a fixed-order sum over warps).
 template <int F>
 __global__ void __launch_bounds__(kGatherThreads)
-    k_gather_colmean(const double2* __restrict__ Y, int np, int ppg, int64_t pair0, int64_t t,
+    k_gather_colmean(const double2* __restrict__ Y, int64_t sE, int64_t sP, int np, int ppg, int64_t pair0, int64_t t,
                      const int32_t* __restrict__ R, const double* __restrict__ colsum,
                      const double* __restrict__ scal, int64_t N, double fparam,
                      double* __restrict__ X, int64_t ldx, double* __restrict__ partial) {
@@ -409,7 +447,7 @@ __global__ void __launch_bounds__(kGatherThreads)
 #pragma unroll
     for (int i = 0; i < RPT; ++i)
       vv[i] = rows[i] == 0 ? make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0)
-              : rows[i] < N ? __ldg(&Y[int64_t(rr[i]) * np + p]) : make_double2(0.0, 0.0);
+              : rows[i] < N ? __ldg(&Y[int64_t(rr[i]) * sE + p * sP]) : make_double2(0.0, 0.0);
     double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
@@ -501,7 +539,7 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
     return r;
   };
   c.off_U = take(size_t(pairs) * pl->sp.L * 16);
-  c.off_Y = take(size_t(pairs) * pl->sp.L * 16);
+  c.off_Y = take(pl->cluster || pl->sp.L1 == 1 ? 0 : size_t(pairs) * pl->sp.L * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int64_t nblocks = (pl->N + kColMeanRows - 1) / kColMeanRows;
@@ -517,28 +555,95 @@ static void set_smem_attr(K kernel) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
 }
 
-template <int L2>
+template <int L2, int L1C>
 static int launch_rows(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0,
                        double2* U, int npairs, double* colsum, cudaStream_t st) {
   const size_t smem = size_t(PadE<L2, QMC_ROW_E>::size) * sizeof(double2);
-  set_smem_attr(k_rows16<L2>);
+  auto kern = k_rows16<L2, L1C>;
+  set_smem_attr(kern);
   dim3 grid((unsigned)pl->sp.L1, (unsigned)npairs);
-  k_rows16<L2><<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj,
-                                                   pl->d_tws, pl->d_W, U, pl->sp.L, colsum);
+  if constexpr (L1C == 0) {
+    kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj, pl->d_tws,
+                                             pl->d_W, U, pl->sp.L, colsum, pl->d_twL, pl->d_tw1);
+  } else {
+    if (L1C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(L2 / QMC_ROW_E, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = L1C;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, A, lda, t, pair0, (const int32_t*)pl->d_e, (const int32_t*)pl->d_bnext,
+                           pl->s, (const double2*)pl->d_twj, (const double2*)pl->d_tws, (const double2*)pl->d_W, U,
+                           pl->sp.L, colsum, (const double2*)pl->d_twL, (const double2*)pl->d_tw1) != cudaSuccess) {
+      cudaGetLastError();
+      return QMC_ECUDA;
+    }
+  }
   QMC_LAUNCHED();
   return QMC_OK;
 }
 
+// (L2, L1) pairs with a cluster instantiation of K1
+#define QMC_CLUSTER_PAIRS(X)                                                                               \
+  X(1024, 2) X(1024, 4) X(1024, 5) X(1024, 8) X(1024, 10) X(1024, 16) X(2048, 2) X(2048, 4) X(2048, 5)    \
+  X(2048, 8) X(2048, 10) X(2048, 16) X(4096, 2) X(4096, 4) X(4096, 5) X(4096, 8) X(4096, 10) X(4096, 16)  \
+  X(8192, 2) X(8192, 4) X(8192, 5) X(8192, 8) X(8192, 10) X(8192, 16)
+
 static int rows_dispatch(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0, double2* U,
                          int np, double* colsum, cudaStream_t st) {
+  if (pl->cluster) {
+#define QMC_CL_CASE(A2, A1) \
+  if (pl->sp.L2 == A2 && pl->sp.L1 == A1) return launch_rows<A2, A1>(pl, A, lda, t, pair0, U, np, colsum, st);
+    QMC_CLUSTER_PAIRS(QMC_CL_CASE)
+#undef QMC_CL_CASE
+    return QMC_EINVAL_N;
+  }
   switch (pl->sp.L2) {
 #define QMC_ROWS_CASE(NN) \
-  case NN: return launch_rows<NN>(pl, A, lda, t, pair0, U, np, colsum, st);
+  case NN: return launch_rows<NN, 0>(pl, A, lda, t, pair0, U, np, colsum, st);
     QMC_ROWS_CASE(16) QMC_ROWS_CASE(32) QMC_ROWS_CASE(64) QMC_ROWS_CASE(128) QMC_ROWS_CASE(256)
     QMC_ROWS_CASE(512) QMC_ROWS_CASE(1024) QMC_ROWS_CASE(2048) QMC_ROWS_CASE(4096) QMC_ROWS_CASE(8192)
 #undef QMC_ROWS_CASE
   }
   return QMC_EINVAL_N;
+}
+
+// Can K1 run with the fused cluster column pass for this plan?  (an
+// instantiation exists and at least one cluster fits on the device)
+int rows_cluster_supported(const qmc_plan* pl) {
+#define QMC_CL_OCC(A2, A1)                                                                           \
+  if (pl->sp.L2 == A2 && pl->sp.L1 == A1) {                                                        \
+    auto kern = k_rows16<A2, A1>;                                                                  \
+    set_smem_attr(kern);                                                                           \
+    if (A1 > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);     \
+    cudaLaunchConfig_t cfg = {};                                                                   \
+    cfg.gridDim = dim3(A1, 1, 1);                                                                  \
+    cfg.blockDim = dim3(A2 / QMC_ROW_E, 1, 1);                                                     \
+    cfg.dynamicSmemBytes = size_t(PadE<A2, QMC_ROW_E>::size) * sizeof(double2);                    \
+    cudaLaunchAttribute attr[1];                                                                   \
+    attr[0].id = cudaLaunchAttributeClusterDimension;                                              \
+    attr[0].val.clusterDim.x = A1;                                                                 \
+    attr[0].val.clusterDim.y = 1;                                                                  \
+    attr[0].val.clusterDim.z = 1;                                                                  \
+    cfg.attrs = attr;                                                                              \
+    cfg.numAttrs = 1;                                                                              \
+    int nclusters = 0;                                                                             \
+    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) {                   \
+      cudaGetLastError();                                                                          \
+      return 0;                                                                                    \
+    }                                                                                              \
+    return nclusters > 0;                                                                          \
+  }
+  QMC_CLUSTER_PAIRS(QMC_CL_OCC)
+#undef QMC_CL_OCC
+  return 0;
 }
 
 static int ilog2(int64_t x) {
@@ -614,20 +719,17 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, st);
     if (rc) return rc;
     prof_end(KC_ROWS, st);
+    // B' of the batch: natural [p][e] (cluster K1, or L1 = 1) or pair-interleaved [e][p] (K2)
     const double2* Yb = U;
-    if (pl->sp.L1 > 1) {
+    int64_t sE = 1, sP = pl->sp.L;
+    if (!pl->cluster && pl->sp.L1 > 1) {
       prof_begin(KC_COLS, st);
       rc = cols_dispatch(pl, U, Y, np, st);
       if (rc) return rc;
       prof_end(KC_COLS, st);
       Yb = Y;
-    } else if (np > 1) {
-      // L1 = 1: B' = U; interleave pairs for the gather
-      prof_begin(KC_COLS, st);
-      rc = cols_dispatch(pl, U, Y, np, st);
-      if (rc) return rc;
-      prof_end(KC_COLS, st);
-      Yb = Y;
+      sE = np;
+      sP = 1;
     }
     prof_begin(KC_GATHER, st);
     const int ppg = cl.ppg;
@@ -638,26 +740,26 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
       switch (f) {
         case QMC_F_IDENTITY:
           k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, smem, st>>>(
-              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
           break;
         case QMC_F_AFFINE:
           k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, smem, st>>>(
-              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
           break;
         default:
           k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, smem, st>>>(
-              Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
       }
       QMC_LAUNCHED();
     } else if (f == QMC_F_ROWMEAN_RELU) {
       // groups absent from a short last batch keep their sums (first = 0)
       dim3 g(nblk(pl->N, kGatherThreads), ng);
-      k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
+      k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
                                                         pl->N, X, ldx, rowparts, pair0 == 0);
       QMC_LAUNCHED();
     } else {
       dim3 g(nblk(pl->N, kGatherThreads), ng);
-      k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
+      k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
                                                    ldx, nullptr, 0);
       QMC_LAUNCHED();
     }

@@ -93,8 +93,14 @@ static bool smooth235(int64_t x) {
 }
 
 bool choose_split(int64_t m, int64_t s, Split* out) {
-  const int64_t cap = s > 4096 ? 8192 : 4096;
+  int64_t cap_env = 0;
+  if (const char* ev = getenv("QMC_L2_CAP")) cap_env = strtol(ev, nullptr, 10);  // tuning override
   auto try_len = [&](int64_t len) -> bool {
+    // rows of 4096 unless the columns would then exceed 16 (cluster limit)
+    // or s > 4096 (keep buckets small): then rows of 8192
+    int64_t cap = s > 4096 ? 8192 : 4096;
+    if (cap == 4096 && len % 8192 == 0 && len / 4096 > 16) cap = 8192;
+    if (cap_env >= 16) cap = cap_env;
     int64_t l2 = 1;
     while (len % (l2 * 2) == 0 && l2 * 2 <= cap) l2 *= 2;
     if (l2 < 16 || (l2 < 256 && l2 != len)) return false;  // rows of >= 256, or one short row
@@ -479,6 +485,10 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       if (v > 0) pl->batch_pairs = v;
     }
   }
+  // K1 with the cluster-fused column pass is opt-in (QMC_CLUSTER=1): on B200
+  // it measured no faster than K1 + K2
+  pl->cluster = (sp.L1 > 1 && getenv("QMC_CLUSTER")) ? rows_cluster_supported(pl) : 0;
+  cudaGetLastError();
   {
     int cb = 32;
     while (cb > 1 && (int64_t(cb) * sp.L1 > 2048 || cb > sp.L2)) cb >>= 1;
@@ -679,7 +689,7 @@ int qmc_profile_read(int64_t* launches, double* ms, int n) {
 }
 
 const char* qmc_profile_class_name(int k) {
-  static const char* names[KC_COUNT] = {"k_pack", "k_rows", "k_cols", "k_gather", "k_colmean_reduce",
+  static const char* names[KC_COUNT] = {"k_pack", "k_rows", "k_cols", "k_gather", "k_reduce",
                                         "k_finalize"};
   return (k >= 0 && k < KC_COUNT) ? names[k] : "";
 }

@@ -58,6 +58,7 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
 
 // shared memory of the register column kernel for a batch of np pairs
 size_t cols_reg_smem(int64_t L1, int64_t np);
+int rows_cluster_supported(const qmc_plan* pl);
 
 }  // namespace qmc
 
@@ -70,6 +71,7 @@ struct qmc_plan {
   int64_t gen;
   qmc::Split sp;
   int64_t batch_pairs;  // column pairs per batch (scratch sized to stay in L2)
+  int cluster;          // K1 fuses the column pass (thread-block cluster of L1 CTAs)
   int col_reg;          // K2 register path (L1 <= 32, two direct radices)
   int col_cb;           // K2 register path: columns e2 per CTA
   int col_cb_smem;      // K2 shared-memory path: columns e2 per CTA
