@@ -58,6 +58,11 @@ __device__ __forceinline__ double2 ldcs(const double2* p) {
   return r;
 }
 __device__ __forceinline__ void stcs(double* p, double v) { asm volatile("st.global.cs.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory"); }
+// Drop a dead 128-byte line from L2 without writing it back (scratch data
+// that is never read again); p must be 128-byte aligned.
+__device__ __forceinline__ void discard_l2(const void* p) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
 // Read-only 16-byte load kept in program order (volatile): stops the compiler
 // from hoisting every stage's twiddles to the kernel start, which costs more
 // registers than the latency it hides.

@@ -41,6 +41,9 @@ constexpr int kColMeanRows = 1024;  // rows per CTA in the column-mean epilogue
 
 enum GatherMode { GM_X = 0, GM_ROWSUM = 1 };
 
+// column-block width of K1's output U (== K2's register-path CB)
+constexpr int kUB = 4;
+
 // cache policy of the epilogue: Y is dead after the gather and X is only
 // written, so both use evict-first (streaming) accesses unless disabled
 #ifndef QMC_NO_STREAMING
@@ -178,9 +181,15 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : Q
   fftE<L2, E, +1>(v, S, tws, tid);
   QMC_TS(4);
   if constexpr (L1C == 0) {
-    double2* Ur = U + p * L + int64_t(f1) * L2;
+    // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
+    // (and discards) whole contiguous lines
+    double2* Up = U + p * L + int64_t(f1) * kUB;
+    const int L1 = int(L / L2);
 #pragma unroll
-    for (int q = 0; q < E; ++q) Ur[tid + q * NT] = v[q];
+    for (int q = 0; q < E; ++q) {
+      const int e2 = tid + q * NT;
+      Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+    }
   } else {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();
@@ -215,16 +224,23 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : Q
 // of the batch, after the twiddle conj(ω_L^{e2 f1}); writes the batch
 // pair-interleaved: Y[(L2·e1 + e2)·np + p] = B'_p[L2·e1 + e2].
 // Register path (L1 = R·M, R, M direct radices): one thread per column.
-constexpr int kColCB = 4;  // columns e2 per CTA in the register path
+constexpr int kColCB = kUB;  // columns e2 per CTA in the register path
+// Grid (L2/CB column blocks, pair groups of kColPG): the shared tile does not
+// grow with the batch.
+constexpr int kColPG = 16;
 template <int L1>
 __global__ void __launch_bounds__(256)
-    k_cols_reg(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int np, int NPP,
-               const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Y) {
+    k_cols_reg(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int npb, int NPP,
+               const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Yb) {
   constexpr int CB = kColCB, SA = L1 + 2;  // SA ≡ 2 (mod 8) for even L1: phase A conflict-free
   extern __shared__ double2 sm[];
+  const int pg0 = blockIdx.y * kColPG;
+  const int np = min(kColPG, npb - pg0);   // pairs of this CTA
+  U += int64_t(pg0) * L;
+  double2* Y = Yb + pg0;                   // Y[e·npb + pg0 + p]
   double2* tcta = sm;                      // [L1][CB] ω_L^{e2·f1}
   double2* tileA = sm + L1 * CB;           // [p·CB + c][SA]
-  double2* tileC = tileA + np * CB * SA;   // [e1·CB + c][NPP], NPP ≡ 2 (mod 8)
+  double2* tileC = tileA + kColPG * CB * SA;  // [e1·CB + c][NPP], NPP ≡ 2 (mod 8)
   const int e2_0 = blockIdx.x * CB;
   for (int i = threadIdx.x; i < L1 * CB; i += blockDim.x) {
     const int f1 = i / CB, c = i % CB;
@@ -242,7 +258,7 @@ __global__ void __launch_bounds__(256)
       if (idx < tot) {
         const int c = idx % CB, r = idx / CB;
         const int f1 = r % L1, p = r / L1;
-        u[k] = __ldg(&U[int64_t(p) * L + int64_t(f1) * L2 + e2_0 + c]);
+        u[k] = __ldg(&U[int64_t(p) * L + int64_t(blockIdx.x) * (L1 * CB) + f1 * CB + c]);
       }
     }
 #pragma unroll
@@ -256,6 +272,14 @@ __global__ void __launch_bounds__(256)
     }
   }
   __syncthreads();
+  // this CTA's block of U (L1·CB complex per pair, contiguous) is dead now
+  {
+    constexpr int LPB = (L1 * CB * 16) / 128;  // whole lines per pair block
+    for (int i = threadIdx.x; i < np * LPB; i += blockDim.x) {
+      const int p = i / LPB, l = i % LPB;
+      discard_l2(reinterpret_cast<const char*>(U + int64_t(p) * L + int64_t(blockIdx.x) * (L1 * CB)) + 128 * l);
+    }
+  }
   for (int col = threadIdx.x; col < np * CB; col += blockDim.x) {
     double2 v[L1];
 #pragma unroll
@@ -266,12 +290,89 @@ __global__ void __launch_bounds__(256)
     for (int e1 = 0; e1 < L1; ++e1) tileC[(e1 * CB + c) * NPP + p] = v[e1];
   }
   __syncthreads();
-  const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int rc = wrp; rc < L1 * CB; rc += nw) {
+  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {  // p fastest: coalesced rows of Y
+    const int p = idx % np, rc = idx / np;
     const int e1 = rc / CB, c = rc % CB;
-    double2* Yr = Y + (int64_t(e1) * L2 + e2_0 + c) * np;
-    for (int p = lane; p < np; p += 32) Yr[p] = tileC[rc * NPP + p];
+    Y[(int64_t(e1) * L2 + e2_0 + c) * npb + p] = tileC[rc * NPP + p];
   }
+}
+
+// Persistent, software-pipelined register path.  A tile is (column block of
+// kUB columns, kPipePG pairs): kPipePG contiguous blocks of L1·kUB complex
+// (K1's blocked layout), copied into shared memory with cp.async while the
+// previous tile is transformed and stored.  One thread per column (p, c).
+constexpr int kPipePG = 16;
+constexpr int kPipeThreads = kPipePG * kUB;  // 64
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+template <int L1>
+__global__ void __launch_bounds__(kPipeThreads)
+    k_cols_pipe(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int npb, int NPP,
+                const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Y) {
+  constexpr int CB = kUB, BLK = L1 * CB, BLKP = BLK + 4;  // pair stride padded: conflict-free reads
+  extern __shared__ double2 sm[];
+  double2* buf[2] = {sm, sm + kPipePG * BLKP};
+  double2* tileC = sm + 2 * kPipePG * BLKP;  // [e1·CB + c][NPP]
+  const int nblk = L2 / CB, ngrp = (npb + kPipePG - 1) / kPipePG;
+  const int ntiles = nblk * ngrp;
+  const int tid = threadIdx.x;
+  auto issue = [&](int tile, double2* dst) {
+    const int b = tile % nblk, g = tile / nblk;
+    const int np = min(kPipePG, npb - g * kPipePG);
+    for (int i = tid; i < np * BLK; i += kPipeThreads) {
+      const int p = i / BLK, o = i % BLK;
+      cp_async16(dst + p * BLKP + o, U + int64_t(g * kPipePG + p) * L + int64_t(b) * BLK + o);
+    }
+  };
+  int tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, buf[0]);
+  cp_async_commit();
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int nxt = tile + gridDim.x;
+    if (nxt < ntiles) issue(nxt, buf[(it + 1) & 1]);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+    const double2* cur = buf[it & 1];
+    const int b = tile % nblk, g = tile / nblk;
+    const int np = min(kPipePG, npb - g * kPipePG);
+    const int p = tid / CB, c = tid % CB;
+    if (p < np) {
+      const int e2 = b * CB + c;
+      // twiddles conj(ω_L^{e2·f1}) = conj(w^f1), w = ω_L^{e2}: product tree
+      double2 pw[L1], v[L1];
+      pw[0] = make_double2(1.0, 0.0);
+      if (L1 > 1) pw[1] = __ldg(&twL[e2]);
+#pragma unroll
+      for (int r = 2; r < L1; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
+#pragma unroll
+      for (int f1 = 0; f1 < L1; ++f1) v[f1] = cmulc(cur[p * BLKP + f1 * CB + c], pw[f1]);
+      reg_dft<L1, +1>(v, tw1);
+#pragma unroll
+      for (int e1 = 0; e1 < L1; ++e1) tileC[(e1 * CB + c) * NPP + p] = v[e1];
+    }
+    __syncthreads();
+    // the U block of this tile is dead: drop it from L2 without write-back
+    for (int i = tid; i < np * (BLK * 16 / 128); i += kPipeThreads) {
+      const int pp = i / (BLK * 16 / 128), l = i % (BLK * 16 / 128);
+      discard_l2(reinterpret_cast<const char*>(U + int64_t(g * kPipePG + pp) * L + int64_t(b) * BLK) + 128 * l);
+    }
+    double2* Yg = Y + g * kPipePG;
+    for (int i = tid; i < BLK * np; i += kPipeThreads) {  // p fastest: coalesced rows of Y
+      const int pp = i % np, rc = i / np;
+      const int e1 = rc / CB, cc = rc % CB;
+      Yg[(int64_t(e1) * L2 + b * CB + cc) * npb + pp] = tileC[rc * NPP + pp];
+    }
+    __syncthreads();  // tileC and buf[it & 1] are reused
+  }
+  cp_async_wait<0>();
 }
 
 // Generic path (any smooth L1 <= 1024): one CTA per (CB columns, pair),
@@ -306,13 +407,14 @@ __global__ void __launch_bounds__(256)
   double2* out = smem + L1 * CB;
   const int p = blockIdx.y;
   const int c0 = blockIdx.x * CB;
-  const double2* Up = U + int64_t(p) * L + c0;
+  const double2* Up = U + int64_t(p) * L;
   const int tot = L1 * CB;
   for (int q = threadIdx.x; q < tot; q += blockDim.x) {
     const int f1 = q / CB, c = q - f1 * CB;
-    const int x = (c0 + c) * f1;
+    const int e2 = c0 + c;
+    const int x = e2 * f1;
     const double2 w = cmul(__ldg(&tw1[x / L2]), __ldg(&twL[x % L2]));
-    in[q] = cmulc(Up[int64_t(f1) * L2 + c], w);
+    in[q] = cmulc(Up[int64_t(e2 / kUB) * (L1 * kUB) + f1 * kUB + (e2 % kUB)], w);
   }
   __syncthreads();
   int Ns = 1;
@@ -402,6 +504,13 @@ __global__ void __launch_bounds__(kGatherThreads)
       rs += v.x;
       if (has2) rs += v.y;
     }
+    // interleaved layout: whole lines inside [pb, pe) were read only by this
+    // thread and are dead now
+    if (sP == 1) {
+      const uintptr_t b0 = (reinterpret_cast<uintptr_t>(yp + pb) + 127) & ~uintptr_t(127);
+      const uintptr_t b1 = reinterpret_cast<uintptr_t>(yp + pe) & ~uintptr_t(127);
+      for (uintptr_t b = b0; b < b1; b += 128) discard_l2(reinterpret_cast<const void*>(b));
+    }
   }
   if (MODE == GM_ROWSUM) {
     double* rsg = rowsum + int64_t(g) * N;
@@ -409,11 +518,13 @@ __global__ void __launch_bounds__(kGatherThreads)
   }
 }
 
-__global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int64_t N, double* __restrict__ out) {
+__global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int ngstride, int nsets, int64_t N,
+                                double* __restrict__ out) {
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
   double s = 0.0;
-  for (int g = 0; g < ng; ++g) s += parts[int64_t(g) * N + n];
+  for (int k = 0; k < nsets; ++k)
+    for (int g = 0; g < ng; ++g) s += parts[(int64_t(k) * ngstride + g) * N + n];
   out[n] = s;
 }
 
@@ -517,7 +628,7 @@ __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int
 // ---------------------------------------------------------------- host side
 struct CallLayout {
   size_t off_U, off_Y, off_colsum, off_partial, off_rowsum, total;
-  int ngroups, ppg;
+  int ngroups, ppg, nsets;
 };
 
 // pair groups of the gather: enough rows × groups for ~2 waves of threads
@@ -538,14 +649,17 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
     o = align_up(o + b);
     return r;
   };
-  c.off_U = take(size_t(pairs) * pl->sp.L * 16);
-  c.off_Y = take(pl->cluster || pl->sp.L1 == 1 ? 0 : size_t(pairs) * pl->sp.L * 16);
+  // one scratch set (U, Y, row-sum parts) per internal stream in use
+  const int64_t nbatch = ((t + 1) / 2 + pl->batch_pairs - 1) / pl->batch_pairs;
+  c.nsets = (pl->nstreams == 2 && nbatch > 1) ? 2 : 1;
+  c.off_U = take(size_t(c.nsets) * pairs * pl->sp.L * 16);
+  c.off_Y = take(pl->cluster || pl->sp.L1 == 1 ? 0 : size_t(c.nsets) * pairs * pl->sp.L * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int64_t nblocks = (pl->N + kColMeanRows - 1) / kColMeanRows;
   c.off_partial = take(colmean ? size_t(nblocks) * std::max<int64_t>(t, 1) * 8 : 0);
   gather_groups(pl, pairs, &c.ngroups, &c.ppg);
-  c.off_rowsum = take(f == QMC_F_ROWMEAN_RELU ? size_t(c.ngroups) * pl->N * 8 : 0);
+  c.off_rowsum = take(f == QMC_F_ROWMEAN_RELU ? size_t(c.nsets) * c.ngroups * pl->N * 8 : 0);
   c.total = o;
   return c;
 }
@@ -652,19 +766,39 @@ static int ilog2(int64_t x) {
   return r;
 }
 
-size_t cols_reg_smem(int64_t L1, int64_t np) {
-  const int64_t npp = np + ((2 - np % 8) + 8) % 8;  // ≡ 2 (mod 8)
+size_t cols_reg_smem(int64_t L1, int64_t /*np*/) {
+  const int64_t np = kColPG, npp = np + ((2 - np % 8) + 8) % 8;  // ≡ 2 (mod 8)
   return size_t(L1 * kColCB + np * kColCB * (L1 + 2) + L1 * kColCB * npp) * 16;
 }
 
 template <int L1>
 static int launch_cols_reg(const qmc_plan* pl, const double2* U, double2* Y, int np, cudaStream_t st) {
-  const size_t smem = cols_reg_smem(L1, np);
-  const int npp = np + ((2 - np % 8) + 8) % 8;
-  set_smem_attr(k_cols_reg<L1>);
-  dim3 g((unsigned)(pl->sp.L2 / kColCB), 1);
-  k_cols_reg<L1><<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp, pl->d_tw1,
-                                       pl->d_twL, Y);
+  if (getenv("QMC_COLS_OLD")) {
+    const size_t smem = cols_reg_smem(L1, np);
+    const int npp = kColPG + ((2 - kColPG % 8) + 8) % 8;
+    set_smem_attr(k_cols_reg<L1>);
+    dim3 g((unsigned)(pl->sp.L2 / kColCB), (unsigned)((np + kColPG - 1) / kColPG));
+    k_cols_reg<L1><<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp, pl->d_tw1,
+                                         pl->d_twL, Y);
+    QMC_LAUNCHED();
+    return QMC_OK;
+  }
+  constexpr int BLKP = L1 * kUB + 4;
+  const int npp = kPipePG + ((2 - kPipePG % 8) + 8) % 8;
+  const size_t smem = size_t(2 * kPipePG * BLKP + L1 * kUB * npp) * sizeof(double2);
+  set_smem_attr(k_cols_pipe<L1>);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cols_pipe<L1>, kPipeThreads, smem);
+  const int64_t ntiles = (pl->sp.L2 / kUB) * ((np + kPipePG - 1) / kPipePG);
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
+  k_cols_pipe<L1><<<grid, kPipeThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp,
+                                                    pl->d_tw1, pl->d_twL, Y);
   QMC_LAUNCHED();
   return QMC_OK;
 }
@@ -705,70 +839,101 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   const CallLayout cl = call_layout(pl, t, f);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
-  double2* U = (double2*)(ws + cl.off_U);
-  double2* Y = (double2*)(ws + cl.off_Y);
+  const int64_t pairs_b = std::max<int64_t>(1, std::min<int64_t>(pl->batch_pairs, (t + 1) / 2));
   double* colsum = (double*)(ws + cl.off_colsum);
   double* partial = (double*)(ws + cl.off_partial);
-  double* rowparts = (double*)(ws + cl.off_rowsum);
   const int64_t npairs_total = (t + 1) / 2;
   const int64_t nb3 = (pl->N + kColMeanRows - 1) / kColMeanRows;
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
-  for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs) {
+  const int nsets = cl.nsets;
+  std::unique_lock<std::mutex> lock;
+  if (nsets == 2) {  // fork: both internal streams start after the caller's prior work
+    lock = std::unique_lock<std::mutex>(*pl->mu);
+    if (cudaEventRecord(pl->ev_fork, st) != cudaSuccess ||
+        cudaStreamWaitEvent(pl->ist[0], pl->ev_fork, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(pl->ist[1], pl->ev_fork, 0) != cudaSuccess) {
+      cudaGetLastError();
+      return QMC_ECUDA;
+    }
+  }
+  int64_t bidx = 0;
+  for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs, ++bidx) {
     const int np = int(std::min<int64_t>(pl->batch_pairs, npairs_total - pair0));
-    prof_begin(KC_ROWS, st);
-    int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, st);
-    if (rc) return rc;
-    prof_end(KC_ROWS, st);
-    // B' of the batch: natural [p][e] (cluster K1, or L1 = 1) or pair-interleaved [e][p] (K2)
-    const double2* Yb = U;
-    int64_t sE = 1, sP = pl->sp.L;
-    if (!pl->cluster && pl->sp.L1 > 1) {
-      prof_begin(KC_COLS, st);
-      rc = cols_dispatch(pl, U, Y, np, st);
+    const int set = nsets == 2 ? int(bidx & 1) : 0;
+    const cudaStream_t bs = nsets == 2 ? pl->ist[set] : st;
+    double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
+    double2* Y = (double2*)(ws + cl.off_Y) + size_t(set) * pairs_b * pl->sp.L;
+    double* rowparts = (double*)(ws + cl.off_rowsum) + size_t(set) * cl.ngroups * pl->N;
+    const int first = bidx < nsets;  // first batch of this scratch set
+    {
+      const cudaStream_t st = bs;
+      prof_begin(KC_ROWS, st);
+      int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, st);
       if (rc) return rc;
-      prof_end(KC_COLS, st);
-      Yb = Y;
-      sE = np;
-      sP = 1;
-    }
-    prof_begin(KC_GATHER, st);
-    const int ppg = cl.ppg;
-    const unsigned ng = unsigned((np + ppg - 1) / ppg);
-    if (colmean) {
-      const size_t smem = size_t(kGatherThreads / 32) * ppg * sizeof(double2);
-      dim3 g((unsigned)nb3, ng);
-      switch (f) {
-        case QMC_F_IDENTITY:
-          k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, smem, st>>>(
-              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
-          break;
-        case QMC_F_AFFINE:
-          k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, smem, st>>>(
-              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
-          break;
-        default:
-          k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, smem, st>>>(
-              Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+      prof_end(KC_ROWS, st);
+      // B' of the batch: natural [p][e] (cluster K1, or L1 = 1) or pair-interleaved [e][p] (K2)
+      const double2* Yb = U;
+      int64_t sE = 1, sP = pl->sp.L;
+      if (!pl->cluster && pl->sp.L1 > 1) {
+        prof_begin(KC_COLS, st);
+        rc = cols_dispatch(pl, U, Y, np, st);
+        if (rc) return rc;
+        prof_end(KC_COLS, st);
+        Yb = Y;
+        sE = np;
+        sP = 1;
       }
-      QMC_LAUNCHED();
-    } else if (f == QMC_F_ROWMEAN_RELU) {
-      // groups absent from a short last batch keep their sums (first = 0)
-      dim3 g(nblk(pl->N, kGatherThreads), ng);
-      k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
-                                                        pl->N, X, ldx, rowparts, pair0 == 0);
-      QMC_LAUNCHED();
-    } else {
-      dim3 g(nblk(pl->N, kGatherThreads), ng);
-      k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
-                                                   ldx, nullptr, 0);
-      QMC_LAUNCHED();
+      prof_begin(KC_GATHER, st);
+      const int ppg = cl.ppg;
+      const unsigned ng = unsigned((np + ppg - 1) / ppg);
+      if (colmean) {
+        const size_t smem = size_t(kGatherThreads / 32) * ppg * sizeof(double2);
+        dim3 g((unsigned)nb3, ng);
+        switch (f) {
+          case QMC_F_IDENTITY:
+            k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, smem, st>>>(
+                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+            break;
+          case QMC_F_AFFINE:
+            k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, smem, st>>>(
+                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+            break;
+          default:
+            k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, smem, st>>>(
+                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
+        }
+        QMC_LAUNCHED();
+      } else if (f == QMC_F_ROWMEAN_RELU) {
+        // groups absent from a short last batch keep their sums (first = 0)
+        dim3 g(nblk(pl->N, kGatherThreads), ng);
+        k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
+                                                          pl->N, X, ldx, rowparts, first);
+        QMC_LAUNCHED();
+      } else {
+        dim3 g(nblk(pl->N, kGatherThreads), ng);
+        k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
+                                                     ldx, nullptr, 0);
+        QMC_LAUNCHED();
+      }
+      prof_end(KC_GATHER, st);
     }
-    prof_end(KC_GATHER, st);
+  }
+  if (nsets == 2) {  // join
+    if (cudaEventRecord(pl->ev_join[0], pl->ist[0]) != cudaSuccess ||
+        cudaEventRecord(pl->ev_join[1], pl->ist[1]) != cudaSuccess ||
+        cudaStreamWaitEvent(st, pl->ev_join[0], 0) != cudaSuccess ||
+        cudaStreamWaitEvent(st, pl->ev_join[1], 0) != cudaSuccess) {
+      cudaGetLastError();
+      return QMC_ECUDA;
+    }
   }
   if (f == QMC_F_ROWMEAN_RELU) {
     prof_begin(KC_REDUCE, st);
+    // parts [set][group][N]; every written group of every set, fixed order
     const int ngr = int(std::min<int64_t>(cl.ngroups, (npairs_total + cl.ppg - 1) / cl.ppg));
-    k_rowsum_reduce<<<nblk(pl->N, 256), 256, 0, st>>>(rowparts, ngr, pl->N, out);
+    const int nsets_used = int(std::min<int64_t>(nsets, (npairs_total + pl->batch_pairs - 1) / pl->batch_pairs));
+    k_rowsum_reduce<<<nblk(pl->N, 256), 256, 0, st>>>((double*)(ws + cl.off_rowsum), ngr, cl.ngroups,
+                                                      nsets_used, pl->N, out);
     QMC_LAUNCHED();
     prof_end(KC_REDUCE, st);
   }

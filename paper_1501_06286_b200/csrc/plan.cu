@@ -475,10 +475,12 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   {
     // two scratch buffers of batch·L complex each, sized to stay in L2
     // (~64 MB); at least two waves of row CTAs when that fits in ~96 MB
+    // U + Y of one batch ~128 MB: measured best on B200 for config 2 (fewer,
+    // longer launches outweigh the L2 overflow, which discards keep small)
     const int64_t per_pair = 32 * sp.L;
-    int64_t bp = std::max<int64_t>(1, (int64_t(64) << 20) / per_pair);
-    const int64_t want = (296 + sp.L1 - 1) / sp.L1;
-    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(96) << 20) / per_pair));
+    int64_t bp = std::max<int64_t>(1, (int64_t(128) << 20) / per_pair);
+    const int64_t want = (296 + sp.L1 - 1) / sp.L1;  // >= 2 waves of K1 CTAs
+    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(192) << 20) / per_pair));
     pl->batch_pairs = std::min<int64_t>(bp, 256);
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
@@ -601,6 +603,16 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
 #undef QMC_PLAN_CHECK
 #undef QMC_PLAN_LAUNCHED
+  pl->nstreams = 1;
+  pl->mu = new (std::nothrow) std::mutex();
+  if (!getenv("QMC_ONE_STREAM") && pl->mu &&
+      cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_join[1], cudaEventDisableTiming) == cudaSuccess)
+    pl->nstreams = 2;
+  cudaGetLastError();
   *out = pl;
   return QMC_OK;
 }
@@ -694,7 +706,18 @@ const char* qmc_profile_class_name(int k) {
   return (k >= 0 && k < KC_COUNT) ? names[k] : "";
 }
 
-void qmc_plan_destroy(qmc_plan_t pl) { delete pl; }
+void qmc_plan_destroy(qmc_plan_t pl) {
+  if (!pl) return;
+  if (pl->nstreams == 2) {
+    cudaStreamDestroy(pl->ist[0]);
+    cudaStreamDestroy(pl->ist[1]);
+    cudaEventDestroy(pl->ev_fork);
+    cudaEventDestroy(pl->ev_join[0]);
+    cudaEventDestroy(pl->ev_join[1]);
+  }
+  delete pl->mu;
+  delete pl;
+}
 
 const char* qmc_strerror(int code) {
   switch (code) {

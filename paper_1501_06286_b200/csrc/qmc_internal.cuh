@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <mutex>
 
 #include "../../include/qmc.h"
 
@@ -78,6 +79,12 @@ struct qmc_plan {
   int nrad1;            // radices of L1
   int rad1[24];
   cudaStream_t stream;
+  // batches alternate over nstreams internal streams (fork/join from the
+  // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3
+  int nstreams;
+  cudaStream_t ist[2];
+  cudaEvent_t ev_fork, ev_join[2];
+  std::mutex* mu;
   // device pointers into plan_ws
   char* ws;
   size_t ws_bytes;
