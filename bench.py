@@ -190,7 +190,7 @@ def ours(args, rank, world, local_rank):
     plan = q.Plan.from_workload(w, device=dev)
     A_host = np.ascontiguousarray(w.A[:, c0:c1].T)          # (tl, s) row-major = A slab col-major
     A = torch.from_numpy(A_host).to(dev).t()
-    X = q.colmajor_empty(w.N, tl, dev)
+    X = q.x_empty(w.N, tl, dev)
     f, fp = w.f, w.f_param
     N = w.N
     if f == W.F_ROWMEAN_RELU:
@@ -314,7 +314,7 @@ def ours(args, rank, world, local_rank):
         ws = plan.call_workspace(tl, f_e2e)
         st = stream.cuda_stream
         def e2e_step():
-            abi.qmc_mean_host(plan.handle, A_pin, w.s, tl, f_e2e, fp, out_pin, A_dev2, X, N,
+            abi.qmc_mean_host(plan.handle, A_pin, w.s, tl, f_e2e, fp, out_pin, A_dev2, X, max(tl, 1),
                               out_dev, ws, ws.numel(), st)
         for _ in range(max(1, args.warmup)):
             e2e_step()

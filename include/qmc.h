@@ -40,8 +40,12 @@
  *     outlive it.  A plan is immutable after creation; concurrent calls on
  *     one plan are safe if each uses its own call workspace.
  *   - Layouts: A is column-major s×t with leading dimension lda >= s
- *     (column k at A + k*lda); X is column-major N×t with ldx >= N.  A
- *     column shard is a pointer offset.
+ *     (column k at A + k*lda); X is ROW-major N×t with ldx >= t (row n, the
+ *     t outputs of QMC point n, at X + n*ldx).  A column shard of either is
+ *     a pointer offset (A + k0*lda, X + k0) with the same leading dimension.
+ *     Row-major X lets the column pass write each reordered output row i
+ *     straight to its conventional row n as one contiguous chunk (DESIGN.md
+ *     §5).  Fastest with ldx even and X 16-byte aligned.
  */
 #ifndef QMC_H
 #define QMC_H
@@ -81,7 +85,7 @@ enum {
   QMC_EINVAL_N = -1,      /* N not prime / out of range / unsupported length  */
   QMC_EINVAL_Z = -2,      /* z_j not in [1, N-1] (q_j not in [1, 2^D-1])      */
   QMC_EINVAL_POLY = -3,   /* p not of degree D, or not primitive              */
-  QMC_EINVAL_DIM = -4,    /* s < 1, t < 0, lda < s, ldx < N                   */
+  QMC_EINVAL_DIM = -4,    /* s < 1, t < 0, lda < s, ldx < t                   */
   QMC_EINVAL_PHI = -5,    /* unknown φ                                        */
   QMC_ENULL = -6,         /* required pointer is NULL                         */
   QMC_ECUDA = -7,         /* CUDA launch / runtime error                      */
@@ -114,7 +118,8 @@ int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host
 int qmc_plan_create_poly(qmc_plan_t* out, int D, uint64_t p, int64_t s, const int64_t* q_host,
                          int phi, void* plan_ws, size_t plan_ws_bytes, void* stream);
 
-/* X = Y·A (device pointers).  t >= 0 columns; t = 0 is a no-op. */
+/* X = Y·A (device pointers; X row-major, ldx >= t).  t >= 0 columns;
+ * t = 0 is a no-op. */
 int qmc_matmul(qmc_plan_t plan, const double* A, int64_t lda, int64_t t, double* X, int64_t ldx,
                void* call_ws, size_t call_ws_bytes, void* stream);
 
@@ -137,7 +142,8 @@ int qmc_mean_finalize(qmc_plan_t plan, int f, const double* reduced, int64_t t_t
  * column-major s×t, lda) into A_dev (device, s*t doubles, ld = s), runs
  * qmc_mean (+ finalize), and copies the result to out_host (1 double for
  * ROWMEAN_RELU, else t doubles); X_dev (device, ldx) receives X.  out_dev
- * (device) must hold max(N, t) doubles.  Synchronises `stream`. */
+ * (device) must hold max(N, t) doubles.  X_dev is row-major with ldx >= t.
+ * Synchronises `stream`. */
 int qmc_mean_host(qmc_plan_t plan, const double* A_host, int64_t lda, int64_t t, int f,
                   double f_param, double* out_host, double* A_dev, double* X_dev, int64_t ldx,
                   double* out_dev, void* call_ws, size_t call_ws_bytes, void* stream);
@@ -159,7 +165,8 @@ int64_t qmc_launch_count(void);
 /* Per-kernel-class timing for roofline reporting.  qmc_profile_enable(1)
  * makes every later hot-path call record CUDA events on its stream around
  * each launch class (k_pack, k_rows, k_cols, k_gather, k_reduce,
- * k_finalize — qmc_profile_class_name(i) for i = 0..5).  qmc_profile_read
+ * k_finalize — qmc_profile_class_name(i) for i = 0..5; k_pack and k_gather
+ * are retired classes and stay empty).  qmc_profile_read
  * waits for those events and returns, per class i < n, the number of
  * timed launches (one "launch" of k_rows = the launch for one batch) and
  * their summed device time in ms (host arrays of n entries); it then clears

@@ -3,9 +3,10 @@ tensors — PyTorch supplies device memory and streams only) and forwards to
 the C ABI.  Argument marshalling only; every step of X = Y·A runs in the
 library's CUDA kernels.
 
-Layouts: A is (s, t) column-major (``A.stride(0) == 1``), X is (N, t)
-column-major, both fp64 CUDA tensors.  ``colmajor`` / ``to_device_colmajor``
-build such tensors.
+Layouts (fp64 CUDA tensors): A is (s, t) column-major (``A.stride(0) == 1``,
+column k contiguous); X is (N, t) row-major (``X.stride(1) == 1``, row n =
+point n's t outputs contiguous, ``ldx = X.stride(0) >= t``).  A column slab of
+either is a view.  ``to_device_colmajor`` / ``x_empty`` build such tensors.
 """
 from __future__ import annotations
 
@@ -25,7 +26,13 @@ def to_device_colmajor(A: np.ndarray, device) -> torch.Tensor:
     return torch.from_numpy(At).to(device).t()
 
 
+def x_empty(N: int, t: int, device, dtype=torch.float64) -> torch.Tensor:
+    """Uninitialised (N, t) row-major X."""
+    return torch.empty((N, t), dtype=dtype, device=device)
+
+
 def _ld(x: torch.Tensor, rows: int) -> int:
+    """Leading dimension of a column-major (rows, t) A."""
     if x.dtype != torch.float64:
         raise TypeError("fp64 tensors required")
     if x.dim() != 2 or x.shape[0] != rows:
@@ -33,6 +40,17 @@ def _ld(x: torch.Tensor, rows: int) -> int:
     if x.shape[1] > 1 and x.stride(0) != 1:
         raise ValueError("column-major (stride(0) == 1) tensor required")
     return max(x.stride(1), rows) if x.shape[1] > 1 else rows
+
+
+def _ldx(x: torch.Tensor, N: int, t: int) -> int:
+    """Leading dimension of a row-major (N, t) X."""
+    if x.dtype != torch.float64:
+        raise TypeError("fp64 tensors required")
+    if x.dim() != 2 or x.shape[0] != N or x.shape[1] != t:
+        raise ValueError(f"expected X of shape ({N}, {t}), got {tuple(x.shape)}")
+    if t > 1 and x.stride(1) != 1:
+        raise ValueError("row-major (stride(1) == 1) X required")
+    return max(x.stride(0), t, 1) if N > 1 else max(t, 1)
 
 
 def _stream(device) -> int:
@@ -84,8 +102,8 @@ class Plan:
         lda = _ld(A, self.s)
         t = A.shape[1]
         if X is None:
-            X = colmajor_empty(self.N, t, self.device)
-        ldx = _ld(X, self.N)
+            X = x_empty(self.N, t, self.device)
+        ldx = _ldx(X, self.N, t)
         ws = self.call_workspace(t)
         abi.qmc_matmul(self.handle, A, lda, t, X, ldx, ws, ws.numel(), _stream(self.device))
         return X
@@ -97,7 +115,7 @@ class Plan:
         n_out = self.N if f == abi.QMC_F_ROWMEAN_RELU else t
         if out is None:
             out = torch.empty(max(n_out, 1), dtype=torch.float64, device=self.device)
-        ldx = _ld(X, self.N) if X is not None else self.N
+        ldx = _ldx(X, self.N, t) if X is not None else max(t, 1)
         ws = self.call_workspace(t, f)
         abi.qmc_mean(self.handle, A, lda, t, f, f_param, out, X, ldx, ws, ws.numel(),
                      _stream(self.device))

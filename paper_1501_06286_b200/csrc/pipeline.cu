@@ -6,20 +6,22 @@
 // one complex correlation serves two real columns), with the plan's split
 // L = L1·L2 (e = L2·e1 + e2, f = f1 + L1·f2):
 //
-//   K0 k_pack      a in bucket order (e2-major) + column sums Σ_j a_j
-//   K1 k_rows      T[f1,e2] = Σ_{j: e_j ≡ e2} a_j ω_L^{e_j f1}   (scatter a' = P a
+//   K1 k_rows16    T[f1,e2] = Σ_{j: e_j ≡ e2} a_j ω_L^{e_j f1}   (scatter a' = P a
 //                  fused with the first FFT dimension)
-//                  → FFT_L2 → ·W → IFFT_L2 → ·ω_L^{-e2 f1}            (smem)
-//   K2 k_cols      IFFT_L1 over f1 → B'[e] in natural order           (skipped if L1 = 1)
-//   K3 k_gather_*  X[0,k] = φ(0) Σ_j A[j,k],
-//                  X[n,k] = B'_k[R[n]], R[n] = (m - L[n]) mod m, n >= 1,
-//                  + optional f / row sums / per-column partial means
-//   K4 k_colmean_reduce   fixed-order reduction of the partial means
+//                  → FFT_L2 → ·W → IFFT_L2 → U[p][f1][e2]           (registers)
+//   K2 k_cols_x    ·conj(ω_L^{e2 f1}), IFFT_L1 over f1 → B'[L2 e1 + e2]; the
+//                  reordered row i = L2 e1 + e2 is conventional row
+//                  n = β^{-i} = P[(m - i) mod m], so K2
+//                  writes the row chunk X[n, 2p..2p+1 of the pair group]
+//                  directly (X row-major); X[0,k] = φ(0) Σ_j A[j,k]
+//                  (PAPER.md:305-311); fused f, per-column partial sums or
+//                  per-row partial sums
+//   K3 k_colpart_reduce / k_rowsum_reduce   fixed-order reductions
 //
 // B'[i] = Σ_j a_j ζ[(e_j - i) mod m] = (Z P a)_i is a cyclic correlation,
 // computed as IDFT(DFT(a') · DFT(K)), K[d] = ζ[(-d) mod m] (zero-padded to
-// L >= 2m-1 when m does not split into supported radices).  Scratch for a
-// batch of column pairs is sized (plan->batch_pairs) to stay in L2.
+// L >= 2m-1 when m does not split into supported radices).  U of a batch of
+// column pairs is sized (plan->batch_pairs) to stay in L2.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -28,33 +30,18 @@
 
 #include <algorithm>
 
-#include <cooperative_groups.h>
-
 #include "fft.cuh"
 #include "qmc_internal.cuh"
 #include "rowcfg.cuh"
 
 namespace qmc {
 
-constexpr int kGatherThreads = 256;
-constexpr int kColMeanRows = 1024;  // rows per CTA in the column-mean epilogue
-
-enum GatherMode { GM_X = 0, GM_ROWSUM = 1 };
-
-// column-block width of K1's output U (== K2's register-path CB)
+// column-block width of K1's output U: U[p] is [e2 / kUB][f1][e2 % kUB]
 constexpr int kUB = 4;
+constexpr int kColThreads = 256;  // K2 CTA size
 
-// cache policy of the epilogue: Y is dead after the gather and X is only
-// written, so both use evict-first (streaming) accesses unless disabled
-#ifndef QMC_NO_STREAMING
-#define QMC_LD2(p, a, b) ldcs2_256(p, a, b)
-#define QMC_LD1(p) ldcs(p)
-#define QMC_ST(p, v) stcs(p, v)
-#else
-#define QMC_LD2(p, a, b) ldg2_256(p, a, b)
-#define QMC_LD1(p) __ldg(p)
-#define QMC_ST(p, v) (*(p) = (v))
-#endif
+// K2 epilogue (runtime, CTA-uniform)
+enum Epilogue { EP_X = 0, EP_ROWSUM = 1, EP_SUM = 2, EP_AFFINE = 3, EP_EXP = 4 };
 
 // deterministic block sum (fixed shuffle tree, then warp 0 over warps)
 template <int NT>
@@ -100,19 +87,12 @@ extern "C" int qmc_debug_phases(long long* host, int n) {
   do {            \
   } while (0)
 #endif
-// L1C = 0: write U[p][f1][e2] (the column pass runs in K2).
-// L1C = L1 > 0: the grid's x-dimension (f1) is one thread-block cluster of
-// L1 CTAs; after the row transforms every CTA keeps its row in shared memory
-// and computes, for its share of the columns e2, the twiddle
-// conj(ω_L^{e2 f1}) and the inverse DFT over f1 from the L1 rows read
-// through distributed shared memory, writing B'[p][L2·e1 + e2] (natural).
-template <int L2, int L1C>
+template <int L2>
 __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : QMC_ROWS_MINB))
     k_rows16(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
              const int32_t* __restrict__ e, const int32_t* __restrict__ bnext, int64_t s,
              const double2* __restrict__ twj, const double2* __restrict__ tws,
-             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum,
-             const double2* __restrict__ twL, const double2* __restrict__ tw1) {
+             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum) {
   extern __shared__ double2 smem[];
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
@@ -180,435 +160,257 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : Q
   QMC_TS(3);
   fftE<L2, E, +1>(v, S, tws, tid);
   QMC_TS(4);
-  if constexpr (L1C == 0) {
-    // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
-    // (and discards) whole contiguous lines
-    double2* Up = U + p * L + int64_t(f1) * kUB;
-    const int L1 = int(L / L2);
+  // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
+  // whole sectors of kUB·16 bytes per f1
+  double2* Up = U + p * L + int64_t(f1) * kUB;
+  const int L1 = int(L / L2);
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int e2 = tid + q * NT;
-      Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
-    }
-  } else {
-    namespace cg = cooperative_groups;
-    cg::cluster_group cluster = cg::this_cluster();
-    __syncthreads();  // every thread has finished reading S in the last stage
-    store_strided<L2, E>(v, S);
-    cluster.sync();
-    const double2* Sr[L1C];
-#pragma unroll
-    for (int r = 0; r < L1C; ++r) Sr[r] = cluster.map_shared_rank(S, r);
-    double2* Bp = U + p * L;
-    for (int c = f1 * NT + tid; c < L2; c += L1C * NT) {
-      double2 u[L1C], pw[L1C];
-      pw[0] = make_double2(1.0, 0.0);
-      if (L1C > 1) pw[1] = __ldg(&twL[c]);  // ω_L^{c}
-#pragma unroll
-      for (int r = 2; r < L1C; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
-#pragma unroll
-      for (int r = 0; r < L1C; ++r) u[r] = Sr[r][padE<E>(c)];
-#pragma unroll
-      for (int r = 1; r < L1C; ++r) u[r] = cmulc(u[r], pw[r]);
-      reg_dft<L1C, +1>(u, tw1);
-#pragma unroll
-      for (int r = 0; r < L1C; ++r) Bp[int64_t(r) * L2 + c] = u[r];
-    }
-    cluster.sync();  // keep this CTA's row alive until every reader is done
+  for (int q = 0; q < E; ++q) {
+    const int e2 = tid + q * NT;
+    Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
   }
   QMC_TS(5);
 }
 
 // ---------------------------------------------------------------- K2
-// Inverse DFT of length L1 along f1 for CB adjacent columns e2 of every pair
-// of the batch, after the twiddle conj(ω_L^{e2 f1}); writes the batch
-// pair-interleaved: Y[(L2·e1 + e2)·np + p] = B'_p[L2·e1 + e2].
-// Register path (L1 = R·M, R, M direct radices): one thread per column.
-constexpr int kColCB = kUB;  // columns e2 per CTA in the register path
-// Grid (L2/CB column blocks, pair groups of kColPG): the shared tile does not
-// grow with the batch.
-constexpr int kColPG = 16;
-template <int L1>
-__global__ void __launch_bounds__(256)
-    k_cols_reg(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int npb, int NPP,
-               const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Yb) {
-  constexpr int CB = kColCB, SA = L1 + 2;  // SA ≡ 2 (mod 8) for even L1: phase A conflict-free
-  extern __shared__ double2 sm[];
-  const int pg0 = blockIdx.y * kColPG;
-  const int np = min(kColPG, npb - pg0);   // pairs of this CTA
-  U += int64_t(pg0) * L;
-  double2* Y = Yb + pg0;                   // Y[e·npb + pg0 + p]
-  double2* tcta = sm;                      // [L1][CB] ω_L^{e2·f1}
-  double2* tileA = sm + L1 * CB;           // [p·CB + c][SA]
-  double2* tileC = tileA + kColPG * CB * SA;  // [e1·CB + c][NPP], NPP ≡ 2 (mod 8)
-  const int e2_0 = blockIdx.x * CB;
-  for (int i = threadIdx.x; i < L1 * CB; i += blockDim.x) {
-    const int f1 = i / CB, c = i % CB;
-    const int x = (e2_0 + c) * f1;
-    tcta[i] = cmul(__ldg(&tw1[x >> lg2L2]), __ldg(&twL[x & (L2 - 1)]));
+// Column pass, un-permutation and epilogue; X is row-major (X[n·ldx + k]).
+//
+// Tile: CB columns e2 (blockIdx.x) × PG pairs (blockIdx.y) of the batch,
+// lane = pair within the group fastest, so the PG pairs of one output row
+// (2·PG consecutive doubles of X) are written by PG adjacent lanes.
+// L1 = R·M:
+//   R = 1 — one item (p, c) per thread: the L1 values u[f1] = U[p][f1][e2]
+//           times conj(ω_L^{e2 f1}), the L1-point inverse DFT in registers;
+//   R > 1 — stage A, item (p, c, r): M-point inverse DFT over f1 = r + R·mm,
+//           times ω_{L1}^{r k2} → shared memory; stage B, item (p, c, k2):
+//           R-point inverse DFT over r → outputs e1 = k2 + M·k1.
+// Output i = L2·e1 + e2 < m is reordered row i, conventional row
+// n = P[(m - i) mod m] (i = 0 → n = 1).
+struct EpiArgs {
+  int ep;
+  double fparam;
+  double* X;
+  int64_t ldx;
+  int xvec;          // X + n·ldx + k 16-byte aligned for even k
+  int64_t t;
+  int64_t kbase;     // first column of the CTA's pair group: 2·(pair0 + pg0)
+  double* rowpart;   // EP_ROWSUM: partial row sums [pair group of the call][N]
+  int64_t N;
+};
+
+// One output value v (columns k = kbase + 2p, k + 1) of row n.  Must be
+// called by all 32 lanes of the warp together (EP_ROWSUM shuffles).
+__device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, int p, int PG, bool okp, bool okrow,
+                                     double2& acc) {
+  const int64_t k = E.kbase + 2 * p;
+  const bool has2 = k + 1 < E.t;
+  if (E.ep == EP_AFFINE) {
+    v.x += E.fparam;
+    v.y += E.fparam;
   }
-  __syncthreads();
-  const int tot = np * L1 * CB;
-  constexpr int UA = 8;  // loads in flight per thread
-  for (int i0 = 0; i0 < tot; i0 += 256 * UA) {
-    double2 u[UA];
-#pragma unroll
-    for (int k = 0; k < UA; ++k) {
-      const int idx = i0 + k * 256 + threadIdx.x;
-      if (idx < tot) {
-        const int c = idx % CB, r = idx / CB;
-        const int f1 = r % L1, p = r / L1;
-        u[k] = __ldg(&U[int64_t(p) * L + int64_t(blockIdx.x) * (L1 * CB) + f1 * CB + c]);
+  const bool ok = okp && okrow;
+  if (ok) {
+    if (E.X) {
+      double* xp = E.X + n * E.ldx + k;
+      if (E.xvec && has2) {
+        *reinterpret_cast<double2*>(xp) = v;
+      } else {
+        xp[0] = v.x;
+        if (has2) xp[1] = v.y;
       }
     }
-#pragma unroll
-    for (int k = 0; k < UA; ++k) {
-      const int idx = i0 + k * 256 + threadIdx.x;
-      if (idx < tot) {
-        const int c = idx % CB, r = idx / CB;
-        const int f1 = r % L1, p = r / L1;
-        tileA[(p * CB + c) * SA + f1] = cmulc(u[k], tcta[f1 * CB + c]);
-      }
+    if (E.ep == EP_SUM || E.ep == EP_AFFINE) {
+      acc.x += v.x;
+      if (has2) acc.y += v.y;
+    } else if (E.ep == EP_EXP) {
+      acc.x += exp(v.x);
+      if (has2) acc.y += exp(v.y);
     }
   }
-  __syncthreads();
-  // this CTA's block of U (L1·CB complex per pair, contiguous) is dead now
-  {
-    constexpr int LPB = (L1 * CB * 16) / 128;  // whole lines per pair block
-    for (int i = threadIdx.x; i < np * LPB; i += blockDim.x) {
-      const int p = i / LPB, l = i % LPB;
-      discard_l2(reinterpret_cast<const char*>(U + int64_t(p) * L + int64_t(blockIdx.x) * (L1 * CB)) + 128 * l);
-    }
-  }
-  for (int col = threadIdx.x; col < np * CB; col += blockDim.x) {
-    double2 v[L1];
-#pragma unroll
-    for (int f1 = 0; f1 < L1; ++f1) v[f1] = tileA[col * SA + f1];
-    reg_dft<L1, +1>(v, tw1);
-    const int p = col / CB, c = col % CB;
-#pragma unroll
-    for (int e1 = 0; e1 < L1; ++e1) tileC[(e1 * CB + c) * NPP + p] = v[e1];
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < tot; idx += blockDim.x) {  // p fastest: coalesced rows of Y
-    const int p = idx % np, rc = idx / np;
-    const int e1 = rc / CB, c = rc % CB;
-    Y[(int64_t(e1) * L2 + e2_0 + c) * npb + p] = tileC[rc * NPP + p];
+  if (E.ep == EP_ROWSUM) {
+    double r = ok ? v.x + (has2 ? v.y : 0.0) : 0.0;
+    for (int o = PG >> 1; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (okrow && p == 0) E.rowpart[n] = r;
   }
 }
 
-// Persistent, software-pipelined register path.  A tile is (column block of
-// kUB columns, kPipePG pairs): kPipePG contiguous blocks of L1·kUB complex
-// (K1's blocked layout), copied into shared memory with cp.async while the
-// previous tile is transformed and stored.  One thread per column (p, c).
-constexpr int kPipePG = 16;
-constexpr int kPipeThreads = kPipePG * kUB;  // 64
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+// ω_L^x for 0 <= x < L from ω_{L1} (tw1) and ω_L^k, k < L2 (twL)
+__device__ __forceinline__ double2 omegaL(int64_t x, int lg2L2, int L2, const double2* __restrict__ tw1,
+                                          const double2* __restrict__ twL) {
+  return cmul(__ldg(&tw1[x >> lg2L2]), __ldg(&twL[x & (L2 - 1)]));
 }
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-template <int L1>
-__global__ void __launch_bounds__(kPipeThreads)
-    k_cols_pipe(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int npb, int NPP,
-                const double2* __restrict__ tw1, const double2* __restrict__ twL, double2* __restrict__ Y) {
-  constexpr int CB = kUB, BLK = L1 * CB, BLKP = BLK + 4;  // pair stride padded: conflict-free reads
+template <int R, int M>
+__global__ void __launch_bounds__(kColThreads, 2)
+    k_cols_x(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int64_t m, int np, int PG,
+             const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
+             const double2* __restrict__ tw1, const double2* __restrict__ twL, int64_t pair0, EpiArgs E,
+             double* __restrict__ part, int part_stride) {
+  constexpr int L1 = R * M;
+  constexpr int LP = L1 | 1;  // odd pitch (in 16-B units): conflict-free stage exchange
   extern __shared__ double2 sm[];
-  double2* buf[2] = {sm, sm + kPipePG * BLKP};
-  double2* tileC = sm + 2 * kPipePG * BLKP;  // [e1·CB + c][NPP]
-  const int nblk = L2 / CB, ngrp = (npb + kPipePG - 1) / kPipePG;
-  const int ntiles = nblk * ngrp;
   const int tid = threadIdx.x;
-  auto issue = [&](int tile, double2* dst) {
-    const int b = tile % nblk, g = tile / nblk;
-    const int np = min(kPipePG, npb - g * kPipePG);
-    for (int i = tid; i < np * BLK; i += kPipeThreads) {
-      const int p = i / BLK, o = i % BLK;
-      cp_async16(dst + p * BLKP + o, U + int64_t(g * kPipePG + p) * L + int64_t(b) * BLK + o);
+  const int CB = (R == 1 ? kColThreads : 32) / PG;
+  const int pg0 = blockIdx.y * PG;
+  const int p = tid % PG;
+  const int pair = pg0 + p;
+  const bool okp = pair < np;
+  const double2* Up = U + int64_t(okp ? pair : 0) * L;
+  E.kbase = 2 * (pair0 + pg0);
+  if (E.ep == EP_ROWSUM) E.rowpart += (pair0 / PG + blockIdx.y) * E.N;  // this group's row sums
+  double2 acc = make_double2(0.0, 0.0);
+  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
+  if (blockIdx.x == 0 && tid < 32) {
+    const bool okrow = tid < PG;
+    double2 v0 = make_double2(0.0, 0.0);
+    const int64_t k = E.kbase + 2 * p;
+    if (okp && okrow) {
+      const double phi0 = __ldg(scal);
+      v0.x = phi0 * colsum[k];
+      v0.y = k + 1 < E.t ? phi0 * colsum[k + 1] : 0.0;
     }
-  };
-  int tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, buf[0]);
-  cp_async_commit();
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int nxt = tile + gridDim.x;
-    if (nxt < ntiles) issue(nxt, buf[(it + 1) & 1]);
-    cp_async_commit();
-    cp_async_wait<1>();
-    __syncthreads();
-    const double2* cur = buf[it & 1];
-    const int b = tile % nblk, g = tile / nblk;
-    const int np = min(kPipePG, npb - g * kPipePG);
-    const int p = tid / CB, c = tid % CB;
-    if (p < np) {
-      const int e2 = b * CB + c;
-      // twiddles conj(ω_L^{e2·f1}) = conj(w^f1), w = ω_L^{e2}: product tree
-      double2 pw[L1], v[L1];
-      pw[0] = make_double2(1.0, 0.0);
-      if (L1 > 1) pw[1] = __ldg(&twL[e2]);
-#pragma unroll
-      for (int r = 2; r < L1; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
-#pragma unroll
-      for (int f1 = 0; f1 < L1; ++f1) v[f1] = cmulc(cur[p * BLKP + f1 * CB + c], pw[f1]);
-      reg_dft<L1, +1>(v, tw1);
-#pragma unroll
-      for (int e1 = 0; e1 < L1; ++e1) tileC[(e1 * CB + c) * NPP + p] = v[e1];
-    }
-    __syncthreads();
-    // the U block of this tile is dead: drop it from L2 without write-back
-    for (int i = tid; i < np * (BLK * 16 / 128); i += kPipeThreads) {
-      const int pp = i / (BLK * 16 / 128), l = i % (BLK * 16 / 128);
-      discard_l2(reinterpret_cast<const char*>(U + int64_t(g * kPipePG + pp) * L + int64_t(b) * BLK) + 128 * l);
-    }
-    double2* Yg = Y + g * kPipePG;
-    for (int i = tid; i < BLK * np; i += kPipeThreads) {  // p fastest: coalesced rows of Y
-      const int pp = i % np, rc = i / np;
-      const int e1 = rc / CB, cc = rc % CB;
-      Yg[(int64_t(e1) * L2 + b * CB + cc) * npb + pp] = tileC[rc * NPP + pp];
-    }
-    __syncthreads();  // tileC and buf[it & 1] are reused
+    emit(E, v0, 0, p, PG, okp, okrow, acc);
   }
-  cp_async_wait<0>();
-}
-
-// Generic path (any smooth L1 <= 1024): one CTA per (CB columns, pair),
-// Stockham stages over shared memory with runtime radices.
-template <int R>
-__device__ __forceinline__ void col_stage(const double2* in, double2* out, int L1, int CB, int Ns,
-                                          const double2* __restrict__ tw1) {
-  const int NB = L1 / R, nbf = NB * CB, step = L1 / (Ns * R);
-  for (int q = threadIdx.x; q < nbf; q += blockDim.x) {
-    const int j = q / CB, c = q - j * CB;
-    double2 v[R];
+  if constexpr (R == 1) {
+    const int c = tid / PG;
+    const int e2 = blockIdx.x * CB + c;
+    const bool okc = e2 < L2;
+    // rows first: every load of the tile is issued before the first store
+    int nrow[L1];
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[r] = in[(j + r * NB) * CB + c];
-    const int k = j % Ns;
-    if (Ns > 1) {
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[r] = cmul(v[r], twid<+1>(__ldg(&tw1[k * r * step])));
+    for (int e1 = 0; e1 < L1; ++e1) {
+      const int64_t i = int64_t(L2) * e1 + e2;
+      nrow[e1] = (okc && i < m) ? __ldg(&P[i == 0 ? 0 : m - i]) : -1;
     }
-    Dft<R, +1>::run(v);
-    const int base = (j / Ns) * Ns * R + k;
+    double2 v[L1];
+    const double2* ub = Up + int64_t(e2 >> 2) * (L1 * kUB) + (e2 & 3);
+    if (okp && okc) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) out[(base + r * Ns) * CB + c] = v[r];
-  }
-}
-
-__global__ void __launch_bounds__(256)
-    k_cols_smem(const double2* __restrict__ U, int64_t L, int L1, int L2, int CB, int np,
-                const int32_t* __restrict__ rad, int nrad, const double2* __restrict__ tw1,
-                const double2* __restrict__ twL, double2* __restrict__ Y) {
-  extern __shared__ double2 smem[];
-  double2* in = smem;
-  double2* out = smem + L1 * CB;
-  const int p = blockIdx.y;
-  const int c0 = blockIdx.x * CB;
-  const double2* Up = U + int64_t(p) * L;
-  const int tot = L1 * CB;
-  for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-    const int f1 = q / CB, c = q - f1 * CB;
-    const int e2 = c0 + c;
-    const int x = e2 * f1;
-    const double2 w = cmul(__ldg(&tw1[x / L2]), __ldg(&twL[x % L2]));
-    in[q] = cmulc(Up[int64_t(e2 / kUB) * (L1 * kUB) + f1 * kUB + (e2 % kUB)], w);
-  }
-  __syncthreads();
-  int Ns = 1;
-  for (int st = 0; st < nrad; ++st) {
-    const int R = __ldg(&rad[st]);
-    switch (R) {
-      case 2: col_stage<2>(in, out, L1, CB, Ns, tw1); break;
-      case 3: col_stage<3>(in, out, L1, CB, Ns, tw1); break;
-      case 4: col_stage<4>(in, out, L1, CB, Ns, tw1); break;
-      case 5: col_stage<5>(in, out, L1, CB, Ns, tw1); break;
-      default: col_stage<8>(in, out, L1, CB, Ns, tw1); break;
+      for (int f1 = 0; f1 < L1; ++f1) v[f1] = __ldg(&ub[f1 * kUB]);
+    } else {
+#pragma unroll
+      for (int f1 = 0; f1 < L1; ++f1) v[f1] = make_double2(0.0, 0.0);
     }
-    __syncthreads();
-    double2* tmp = in;
-    in = out;
-    out = tmp;
-    Ns *= R;
-  }
-  for (int q = threadIdx.x; q < tot; q += blockDim.x) {
-    const int e1 = q / CB, c = q - e1 * CB;
-    Y[(int64_t(e1) * L2 + c0 + c) * np + p] = in[q];
-  }
-}
-
-// ---------------------------------------------------------------- K3
-// Grid (row blocks, pair groups): thread = conventional row n, looping over
-// the pairs [g·ppg, (g+1)·ppg) of the batch; B' of all pairs of the batch at
-// reordered index R[n] is contiguous in Y.  ROWSUM mode accumulates
-// Σ_k X[n,k] into rowsum[g·N + n] (reduced over g at the end of the call).
-template <int MODE>
-__global__ void __launch_bounds__(kGatherThreads)
-    k_gather(const double2* __restrict__ Y, int64_t sE, int64_t sP, int np, int ppg, int64_t pair0, int64_t t,
-             const int32_t* __restrict__ R, const double* __restrict__ colsum,
-             const double* __restrict__ scal, int64_t N, double* __restrict__ X, int64_t ldx,
-             double* __restrict__ rowsum, int first) {
-  const int64_t n = int64_t(blockIdx.x) * kGatherThreads + threadIdx.x;
-  if (n >= N) return;
-  const int g = blockIdx.y;
-  const int pb = g * ppg, pe = min(np, pb + ppg);
-  double rs = 0.0;
-  if (n == 0) {
-    const double phi0 = __ldg(scal);
-    for (int p = pb; p < pe; ++p) {
-      const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-      const bool has2 = k2 < t;
-      const double2 v = make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0);
-      if (X) {
-        X[k1 * ldx] = v.x;
-        if (has2) X[k2 * ldx] = v.y;
+    if (L1 > 1) {
+      // conj(ω_L^{e2 f1}) = conj(w^f1), w = ω_L^{e2}, as w^{4a}·w^b (f1 = 4a + b):
+      // products of depth <= 3, six live twiddles
+      const double2 w1 = __ldg(&twL[okc ? e2 : 0]);
+      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+      const double2 w4 = cmul(w2, w2);
+      double2 hi = w4;
+#pragma unroll
+      for (int f1 = 1; f1 < L1; ++f1) {
+        const int b = f1 & 3;
+        if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
+        const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
+        const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
+        v[f1] = cmulc(v[f1], tw);
       }
-      rs += v.x;
-      if (has2) rs += v.y;
     }
-  } else {
-    const double2* yp = Y + int64_t(__ldg(&R[n])) * sE;
-    double* Xn = X ? X + n + 2 * pair0 * ldx : nullptr;
-    int p = pb;
-    constexpr int U8 = 8;
-    const bool al32 = sP == 1 && ((np | pb) & 1) == 0;  // interleaved and yp + p 32-byte aligned
-    for (; p + U8 <= pe && 2 * (pair0 + p + U8 - 1) + 1 < t; p += U8) {
-      double2 v[U8];
-      if (al32) {
+    reg_dft<L1, +1>(v, tw1);
 #pragma unroll
-        for (int i = 0; i < U8; i += 2) QMC_LD2(&yp[p + i], v[i], v[i + 1]);
+    for (int e1 = 0; e1 < L1; ++e1)
+      emit(E, v[e1], nrow[e1] < 0 ? 0 : nrow[e1], p, PG, okp, nrow[e1] >= 0, acc);
+  } else {
+    double2* T = sm;  // [(p + PG·c)·LP + r·M + k2]
+    const int nA = 32 * R;  // = PG·CB·R items
+    for (int it = tid; it < nA; it += kColThreads) {
+      const int rest = it / PG;
+      const int r = rest % R, c = rest / R;
+      const int e2 = blockIdx.x * CB + c;
+      const bool ok = okp && e2 < L2;
+      double2 x[M];
+      if (ok) {
+        const double2* ub = Up + int64_t(e2 >> 2) * (L1 * kUB) + (e2 & 3);
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm) x[mm] = __ldg(&ub[(r + R * mm) * kUB]);
+        // conj(ω_L^{e2 (r + R mm)}) = conj(b0 · st^mm)
+        const double2 b0 = omegaL(int64_t(e2) * r, lg2L2, L2, tw1, twL);
+        double2 pw[M];
+        pw[0] = make_double2(1.0, 0.0);
+        if (M > 1) pw[1] = omegaL(int64_t(e2) * R, lg2L2, L2, tw1, twL);
+#pragma unroll
+        for (int q = 2; q < M; ++q) pw[q] = cmul(pw[q / 2], pw[q - q / 2]);
+#pragma unroll
+        for (int mm = 0; mm < M; ++mm) x[mm] = cmulc(x[mm], cmul(b0, pw[mm]));
       } else {
 #pragma unroll
-        for (int i = 0; i < U8; ++i) v[i] = QMC_LD1(&yp[(p + i) * sP]);
+        for (int mm = 0; mm < M; ++mm) x[mm] = make_double2(0.0, 0.0);
       }
+      reg_dft<M, +1>(x, tw1, L1 / M);
 #pragma unroll
-      for (int i = 0; i < U8; ++i) {
-        if (Xn) {
-          QMC_ST(&Xn[(2 * (p + i)) * ldx], v[i].x);
-          QMC_ST(&Xn[(2 * (p + i) + 1) * ldx], v[i].y);
-        }
-        rs += v[i].x;
-        rs += v[i].y;
-      }
+      for (int k2 = 1; k2 < M; ++k2)
+        if (r) x[k2] = cmul(x[k2], twid<+1>(__ldg(&tw1[r * k2])));
+      double2* Tp = T + (p + PG * c) * LP + r * M;
+#pragma unroll
+      for (int k2 = 0; k2 < M; ++k2) Tp[k2] = x[k2];
     }
-    for (; p < pe; ++p) {
-      const int64_t k2 = 2 * (pair0 + p) + 1;
-      const bool has2 = k2 < t;
-      const double2 v = __ldg(&yp[p * sP]);
-      if (Xn) {
-        Xn[(2 * p) * ldx] = v.x;
-        if (has2) Xn[(2 * p + 1) * ldx] = v.y;
+    __syncthreads();
+    const int nB = 32 * M;  // = PG·CB·M items (a multiple of 32: warp-uniform loop)
+    for (int it = tid; it < nB; it += kColThreads) {
+      const int rest = it / PG;
+      const int k2 = rest % M, c = rest / M;
+      const int e2 = blockIdx.x * CB + c;
+      const bool okc = e2 < L2;
+      int nrow[R];
+#pragma unroll
+      for (int k1 = 0; k1 < R; ++k1) {
+        const int64_t i = int64_t(L2) * (k2 + M * k1) + e2;
+        nrow[k1] = (okc && i < m) ? __ldg(&P[i == 0 ? 0 : m - i]) : -1;
       }
-      rs += v.x;
-      if (has2) rs += v.y;
-    }
-    // interleaved layout: whole lines inside [pb, pe) were read only by this
-    // thread and are dead now
-    if (sP == 1) {
-      const uintptr_t b0 = (reinterpret_cast<uintptr_t>(yp + pb) + 127) & ~uintptr_t(127);
-      const uintptr_t b1 = reinterpret_cast<uintptr_t>(yp + pe) & ~uintptr_t(127);
-      for (uintptr_t b = b0; b < b1; b += 128) discard_l2(reinterpret_cast<const void*>(b));
+      double2 z[R];
+      const double2* Tp = T + (p + PG * c) * LP + k2;
+#pragma unroll
+      for (int r = 0; r < R; ++r) z[r] = Tp[r * M];
+      reg_dft<R, +1>(z, tw1, L1 / R);
+#pragma unroll
+      for (int k1 = 0; k1 < R; ++k1)
+        emit(E, z[k1], nrow[k1] < 0 ? 0 : nrow[k1], p, PG, okp, nrow[k1] >= 0, acc);
     }
   }
-  if (MODE == GM_ROWSUM) {
-    double* rsg = rowsum + int64_t(g) * N;
-    rsg[n] = (first ? 0.0 : rsg[n]) + rs;
+  // per-column partial sums of this CTA: lanes with equal p, then warps in order
+  if (E.ep == EP_SUM || E.ep == EP_AFFINE || E.ep == EP_EXP) {
+    for (int o = PG; o < 32; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    __shared__ double2 red[kColThreads / 32][16];
+    const int w = tid >> 5, l = tid & 31;
+    if (l < PG) red[w][l] = acc;
+    __syncthreads();
+    if (tid < PG && okp) {
+      double2 s = red[0][tid];
+      for (int ww = 1; ww < kColThreads / 32; ++ww) s = cadd(s, red[ww][tid]);
+      double* dst = part + int64_t(blockIdx.x) * part_stride + 2 * pair;
+      dst[0] = s.x;
+      dst[1] = s.y;
+    }
   }
 }
 
-__global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int ngstride, int nsets, int64_t N,
-                                double* __restrict__ out) {
+// out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
+// lane-strided partial sums, then a fixed shuffle tree (deterministic)
+__global__ void k_colpart_reduce(const double* __restrict__ part, int nbx, int part_stride, int ncols, int64_t k0,
+                                 int64_t t, int64_t N, double* __restrict__ out) {
+  const int kk = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+  const int l = threadIdx.x & 31;
+  if (kk >= ncols || k0 + kk >= t) return;  // warp-uniform
+  double s = 0.0;
+  for (int b = l; b < nbx; b += 32) s += __ldg(&part[int64_t(b) * part_stride + kk]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (l == 0) out[k0 + kk] = s / double(N);
+}
+
+__global__ void k_rowsum_reduce(const double* __restrict__ parts, int ng, int64_t N, double* __restrict__ out) {
   const int64_t n = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (n >= N) return;
   double s = 0.0;
-  for (int k = 0; k < nsets; ++k)
-    for (int g = 0; g < ng; ++g) s += parts[(int64_t(k) * ngstride + g) * N + n];
+  for (int g = 0; g < ng; ++g) s += __ldg(&parts[int64_t(g) * N + n]);
   out[n] = s;
 }
 
-// Grid (row blocks of kColMeanRows, pair groups): writes X (c + X for
-// AFFINE) and the per-column block sums of f(X) into partial[nb·t + k]
-// (warp shuffles, then a fixed-order sum over warps).
-template <int F>
-__global__ void __launch_bounds__(kGatherThreads)
-    k_gather_colmean(const double2* __restrict__ Y, int64_t sE, int64_t sP, int np, int ppg, int64_t pair0, int64_t t,
-                     const int32_t* __restrict__ R, const double* __restrict__ colsum,
-                     const double* __restrict__ scal, int64_t N, double fparam,
-                     double* __restrict__ X, int64_t ldx, double* __restrict__ partial) {
-  extern __shared__ double2 red[];  // [kGatherThreads/32][ppg]
-  constexpr int RPT = kColMeanRows / kGatherThreads;
-  const int64_t nb = blockIdx.x;
-  const int g = blockIdx.y;
-  const int pb = g * ppg, pe = min(np, pb + ppg);
-  const double phi0 = __ldg(scal);
-  int64_t rows[RPT];
-  int rr[RPT];
-#pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    rows[i] = nb * kColMeanRows + i * kGatherThreads + threadIdx.x;
-    rr[i] = (rows[i] > 0 && rows[i] < N) ? __ldg(&R[rows[i]]) : 0;
-  }
-  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-  for (int p = pb; p < pe; ++p) {
-    const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-    const bool has2 = k2 < t;
-    double2 vv[RPT];
-#pragma unroll
-    for (int i = 0; i < RPT; ++i)
-      vv[i] = rows[i] == 0 ? make_double2(phi0 * colsum[k1], has2 ? phi0 * colsum[k2] : 0.0)
-              : rows[i] < N ? __ldg(&Y[int64_t(rr[i]) * sE + p * sP]) : make_double2(0.0, 0.0);
-    double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-    for (int i = 0; i < RPT; ++i) {
-      const int64_t n = rows[i];
-      if (n < N) {
-        double2 v = vv[i];
-        if (F == QMC_F_AFFINE) {
-          v.x += fparam;
-          v.y += fparam;
-        }
-        if (X) {
-          X[n + k1 * ldx] = v.x;
-          if (has2) X[n + k2 * ldx] = v.y;
-        }
-        if (F == QMC_F_EXP) {
-          acc.x += exp(v.x);
-          if (has2) acc.y += exp(v.y);
-        } else {
-          acc.x += v.x;
-          if (has2) acc.y += v.y;
-        }
-      }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      acc.x += __shfl_down_sync(0xffffffffu, acc.x, o);
-      acc.y += __shfl_down_sync(0xffffffffu, acc.y, o);
-    }
-    if (l == 0) red[w * ppg + (p - pb)] = acc;
-  }
-  __syncthreads();
-  for (int p = pb + threadIdx.x; p < pe; p += kGatherThreads) {
-    double2 sacc = make_double2(0.0, 0.0);
-    for (int ww = 0; ww < kGatherThreads / 32; ++ww) sacc = cadd(sacc, red[ww * ppg + (p - pb)]);
-    const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-    partial[nb * t + k1] = sacc.x;
-    if (k2 < t) partial[nb * t + k2] = sacc.y;
-  }
-}
-
-// ---------------------------------------------------------------- K4 / finalize
-__global__ void k_colmean_reduce(const double* __restrict__ partial, int64_t nblocks, int64_t t,
-                                 int64_t N, double* __restrict__ out) {
-  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k >= t) return;
-  double s = 0.0;
-  for (int64_t b = 0; b < nblocks; ++b) s += partial[b * t + k];
-  out[k] = s / double(N);
-}
-
+// ---------------------------------------------------------------- finalize
 __global__ void __launch_bounds__(1024)
     k_rowmean_relu_finalize(const double* reduced, int64_t N, int64_t t_total, double* out) {
   __shared__ double2 red[32];
@@ -626,19 +428,15 @@ __global__ void k_copy(const double* __restrict__ a, double* __restrict__ b, int
 }
 
 // ---------------------------------------------------------------- host side
-struct CallLayout {
-  size_t off_U, off_Y, off_colsum, off_partial, off_rowsum, total;
-  int ngroups, ppg, nsets;
-};
+static int pair_group(int64_t pairs_b) { return pairs_b >= 16 ? 16 : pairs_b >= 8 ? 8 : 4; }
 
-// pair groups of the gather: enough rows × groups for ~2 waves of threads
-static void gather_groups(const qmc_plan* pl, int64_t pairs, int* ngroups, int* ppg) {
-  int64_t g = std::max<int64_t>(1, (int64_t(148) * 2048 * 2) / std::max<int64_t>(pl->N, 1));
-  g = std::min<int64_t>(g, pairs);
-  const int64_t per = (pairs + g - 1) / g;
-  *ppg = int(per);
-  *ngroups = int((pairs + per - 1) / per);
-}
+// K2 tile width (columns e2 per CTA) and grid x for the plan's split
+static int cols_cb(const qmc_plan* pl, int PG) { return (k2_split_R(pl->sp.L1) == 1 ? kColThreads : 32) / PG; }
+
+struct CallLayout {
+  size_t off_U, off_colsum, off_part, off_rowsum, total;
+  int PG, ngroups, ngroups_all, nbx, nsets, part_stride;
+};
 
 static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   CallLayout c;
@@ -649,115 +447,53 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
     o = align_up(o + b);
     return r;
   };
-  // one scratch set (U, Y, row-sum parts) per internal stream in use
+  // one scratch set (U, partial sums) per internal stream in use
   const int64_t nbatch = ((t + 1) / 2 + pl->batch_pairs - 1) / pl->batch_pairs;
   c.nsets = (pl->nstreams == 2 && nbatch > 1) ? 2 : 1;
+  c.PG = pair_group(pairs);
+  c.ngroups = int((pairs + c.PG - 1) / c.PG);
+  const int CB = cols_cb(pl, c.PG);
+  c.nbx = int((pl->sp.L2 + CB - 1) / CB);
+  c.part_stride = int(2 * c.ngroups * c.PG);
   c.off_U = take(size_t(c.nsets) * pairs * pl->sp.L * 16);
-  c.off_Y = take(pl->cluster || pl->sp.L1 == 1 ? 0 : size_t(c.nsets) * pairs * pl->sp.L * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
-  const int64_t nblocks = (pl->N + kColMeanRows - 1) / kColMeanRows;
-  c.off_partial = take(colmean ? size_t(nblocks) * std::max<int64_t>(t, 1) * 8 : 0);
-  gather_groups(pl, pairs, &c.ngroups, &c.ppg);
-  c.off_rowsum = take(f == QMC_F_ROWMEAN_RELU ? size_t(c.nsets) * c.ngroups * pl->N * 8 : 0);
+  c.off_part = take(colmean ? size_t(c.nsets) * c.nbx * c.part_stride * 8 : 0);
+  // row sums: one N-vector per pair group of the whole call (no read-modify-write)
+  c.ngroups_all = int(((t + 1) / 2 + c.PG - 1) / c.PG);
+  c.off_rowsum = take(f == QMC_F_ROWMEAN_RELU ? size_t(c.ngroups_all) * pl->N * 8 : 0);
   c.total = o;
   return c;
 }
 
 template <typename K>
-static void set_smem_attr(K kernel) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+static void set_smem_attr(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
-template <int L2, int L1C>
+template <int L2>
 static int launch_rows(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0,
                        double2* U, int npairs, double* colsum, cudaStream_t st) {
   const size_t smem = size_t(PadE<L2, QMC_ROW_E>::size) * sizeof(double2);
-  auto kern = k_rows16<L2, L1C>;
-  set_smem_attr(kern);
+  auto kern = k_rows16<L2>;
+  set_smem_attr(kern, smem);
   dim3 grid((unsigned)pl->sp.L1, (unsigned)npairs);
-  if constexpr (L1C == 0) {
-    kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj, pl->d_tws,
-                                             pl->d_W, U, pl->sp.L, colsum, pl->d_twL, pl->d_tw1);
-  } else {
-    if (L1C > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(L2 / QMC_ROW_E, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = L1C;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    if (cudaLaunchKernelEx(&cfg, kern, A, lda, t, pair0, (const int32_t*)pl->d_e, (const int32_t*)pl->d_bnext,
-                           pl->s, (const double2*)pl->d_twj, (const double2*)pl->d_tws, (const double2*)pl->d_W, U,
-                           pl->sp.L, colsum, (const double2*)pl->d_twL, (const double2*)pl->d_tw1) != cudaSuccess) {
-      cudaGetLastError();
-      return QMC_ECUDA;
-    }
-  }
+  kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj, pl->d_tws,
+                                           pl->d_W, U, pl->sp.L, colsum);
   QMC_LAUNCHED();
   return QMC_OK;
 }
 
-// (L2, L1) pairs with a cluster instantiation of K1
-#define QMC_CLUSTER_PAIRS(X)                                                                               \
-  X(1024, 2) X(1024, 4) X(1024, 5) X(1024, 8) X(1024, 10) X(1024, 16) X(2048, 2) X(2048, 4) X(2048, 5)    \
-  X(2048, 8) X(2048, 10) X(2048, 16) X(4096, 2) X(4096, 4) X(4096, 5) X(4096, 8) X(4096, 10) X(4096, 16)  \
-  X(8192, 2) X(8192, 4) X(8192, 5) X(8192, 8) X(8192, 10) X(8192, 16)
-
 static int rows_dispatch(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0, double2* U,
                          int np, double* colsum, cudaStream_t st) {
-  if (pl->cluster) {
-#define QMC_CL_CASE(A2, A1) \
-  if (pl->sp.L2 == A2 && pl->sp.L1 == A1) return launch_rows<A2, A1>(pl, A, lda, t, pair0, U, np, colsum, st);
-    QMC_CLUSTER_PAIRS(QMC_CL_CASE)
-#undef QMC_CL_CASE
-    return QMC_EINVAL_N;
-  }
   switch (pl->sp.L2) {
 #define QMC_ROWS_CASE(NN) \
-  case NN: return launch_rows<NN, 0>(pl, A, lda, t, pair0, U, np, colsum, st);
+  case NN: return launch_rows<NN>(pl, A, lda, t, pair0, U, np, colsum, st);
     QMC_ROWS_CASE(16) QMC_ROWS_CASE(32) QMC_ROWS_CASE(64) QMC_ROWS_CASE(128) QMC_ROWS_CASE(256)
     QMC_ROWS_CASE(512) QMC_ROWS_CASE(1024) QMC_ROWS_CASE(2048) QMC_ROWS_CASE(4096) QMC_ROWS_CASE(8192)
 #undef QMC_ROWS_CASE
   }
   return QMC_EINVAL_N;
-}
-
-// Can K1 run with the fused cluster column pass for this plan?  (an
-// instantiation exists and at least one cluster fits on the device)
-int rows_cluster_supported(const qmc_plan* pl) {
-#define QMC_CL_OCC(A2, A1)                                                                           \
-  if (pl->sp.L2 == A2 && pl->sp.L1 == A1) {                                                        \
-    auto kern = k_rows16<A2, A1>;                                                                  \
-    set_smem_attr(kern);                                                                           \
-    if (A1 > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);     \
-    cudaLaunchConfig_t cfg = {};                                                                   \
-    cfg.gridDim = dim3(A1, 1, 1);                                                                  \
-    cfg.blockDim = dim3(A2 / QMC_ROW_E, 1, 1);                                                     \
-    cfg.dynamicSmemBytes = size_t(PadE<A2, QMC_ROW_E>::size) * sizeof(double2);                    \
-    cudaLaunchAttribute attr[1];                                                                   \
-    attr[0].id = cudaLaunchAttributeClusterDimension;                                              \
-    attr[0].val.clusterDim.x = A1;                                                                 \
-    attr[0].val.clusterDim.y = 1;                                                                  \
-    attr[0].val.clusterDim.z = 1;                                                                  \
-    cfg.attrs = attr;                                                                              \
-    cfg.numAttrs = 1;                                                                              \
-    int nclusters = 0;                                                                             \
-    if (cudaOccupancyMaxActiveClusters(&nclusters, kern, &cfg) != cudaSuccess) {                   \
-      cudaGetLastError();                                                                          \
-      return 0;                                                                                    \
-    }                                                                                              \
-    return nclusters > 0;                                                                          \
-  }
-  QMC_CLUSTER_PAIRS(QMC_CL_OCC)
-#undef QMC_CL_OCC
-  return 0;
 }
 
 static int ilog2(int64_t x) {
@@ -766,62 +502,28 @@ static int ilog2(int64_t x) {
   return r;
 }
 
-size_t cols_reg_smem(int64_t L1, int64_t /*np*/) {
-  const int64_t np = kColPG, npp = np + ((2 - np % 8) + 8) % 8;  // ≡ 2 (mod 8)
-  return size_t(L1 * kColCB + np * kColCB * (L1 + 2) + L1 * kColCB * npp) * 16;
-}
-
-template <int L1>
-static int launch_cols_reg(const qmc_plan* pl, const double2* U, double2* Y, int np, cudaStream_t st) {
-  if (getenv("QMC_COLS_OLD")) {
-    const size_t smem = cols_reg_smem(L1, np);
-    const int npp = kColPG + ((2 - kColPG % 8) + 8) % 8;
-    set_smem_attr(k_cols_reg<L1>);
-    dim3 g((unsigned)(pl->sp.L2 / kColCB), (unsigned)((np + kColPG - 1) / kColPG));
-    k_cols_reg<L1><<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp, pl->d_tw1,
-                                         pl->d_twL, Y);
-    QMC_LAUNCHED();
-    return QMC_OK;
-  }
-  constexpr int BLKP = L1 * kUB + 4;
-  const int npp = kPipePG + ((2 - kPipePG % 8) + 8) % 8;
-  const size_t smem = size_t(2 * kPipePG * BLKP + L1 * kUB * npp) * sizeof(double2);
-  set_smem_attr(k_cols_pipe<L1>);
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_cols_pipe<L1>, kPipeThreads, smem);
-  const int64_t ntiles = (pl->sp.L2 / kUB) * ((np + kPipePG - 1) / kPipePG);
-  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
-  k_cols_pipe<L1><<<grid, kPipeThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), np, npp,
-                                                    pl->d_tw1, pl->d_twL, Y);
+template <int R, int M>
+static int launch_cols(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
+                       const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+  constexpr int L1 = R * M;
+  const size_t smem = R == 1 ? 0 : size_t(32) * (L1 | 1) * sizeof(double2);
+  auto kern = k_cols_x<R, M>;
+  set_smem_attr(kern, smem);
+  dim3 g((unsigned)cl.nbx, (unsigned)((np + cl.PG - 1) / cl.PG));
+  kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
+                                     colsum, pl->d_scal, pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
   QMC_LAUNCHED();
   return QMC_OK;
 }
 
-static int cols_dispatch(const qmc_plan* pl, const double2* U, double2* Y, int np, cudaStream_t st) {
-  if (pl->col_reg) {
-    switch (pl->sp.L1) {
-#define QMC_COLS_CASE(NN) \
-  case NN: return launch_cols_reg<NN>(pl, U, Y, np, st);
-      QMC_COLS_CASE(2) QMC_COLS_CASE(3) QMC_COLS_CASE(4) QMC_COLS_CASE(5) QMC_COLS_CASE(6) QMC_COLS_CASE(8)
-      QMC_COLS_CASE(9) QMC_COLS_CASE(10) QMC_COLS_CASE(12) QMC_COLS_CASE(15) QMC_COLS_CASE(16) QMC_COLS_CASE(20)
-      QMC_COLS_CASE(24) QMC_COLS_CASE(25) QMC_COLS_CASE(32)
+static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
+                         const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+  const int R = k2_split_R(pl->sp.L1), M = int(pl->sp.L1) / std::max(R, 1);
+#define QMC_COLS_CASE(RR, MM) \
+  if (R == RR && M == MM) return launch_cols<RR, MM>(pl, cl, U, np, pair0, E, part, colsum, st);
+  QMC_K2_SPLITS(QMC_COLS_CASE)
 #undef QMC_COLS_CASE
-    }
-  }
-  const int CB = pl->col_cb_smem;
-  const size_t smem = size_t(2) * pl->sp.L1 * CB * sizeof(double2);
-  set_smem_attr(k_cols_smem);
-  dim3 g((unsigned)(pl->sp.L2 / CB), (unsigned)np);
-  k_cols_smem<<<g, 256, smem, st>>>(U, pl->sp.L, int(pl->sp.L1), int(pl->sp.L2), CB, np, pl->d_rad1, pl->nrad1,
-                                    pl->d_tw1, pl->d_twL, Y);
-  QMC_LAUNCHED();
-  return QMC_OK;
+  return QMC_EINVAL_N;
 }
 
 static unsigned nblk(int64_t n, int b) { return unsigned((n + b - 1) / b); }
@@ -831,7 +533,7 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
                double* out, double* X, int64_t ldx, void* call_ws, size_t call_ws_bytes, cudaStream_t st) {
   if (!pl) return QMC_ENULL;
   if (t < 0 || lda < pl->s) return QMC_EINVAL_DIM;
-  if (X && ldx < pl->N) return QMC_EINVAL_DIM;
+  if (X && ldx < t) return QMC_EINVAL_DIM;
   if (t == 0) return QMC_OK;
   if (!A || !call_ws) return QMC_ENULL;
   if (f >= 0 && !out) return QMC_ENULL;
@@ -841,11 +543,21 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   char* ws = (char*)call_ws;
   const int64_t pairs_b = std::max<int64_t>(1, std::min<int64_t>(pl->batch_pairs, (t + 1) / 2));
   double* colsum = (double*)(ws + cl.off_colsum);
-  double* partial = (double*)(ws + cl.off_partial);
   const int64_t npairs_total = (t + 1) / 2;
-  const int64_t nb3 = (pl->N + kColMeanRows - 1) / kColMeanRows;
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int nsets = cl.nsets;
+  EpiArgs E;
+  E.ep = f == QMC_F_ROWMEAN_RELU ? EP_ROWSUM
+         : f == QMC_F_IDENTITY   ? EP_SUM
+         : f == QMC_F_AFFINE     ? EP_AFFINE
+         : f == QMC_F_EXP        ? EP_EXP
+                                 : EP_X;
+  E.fparam = fparam;
+  E.X = X;
+  E.ldx = ldx;
+  E.xvec = X && (ldx % 2 == 0) && (uintptr_t(X) % 16 == 0);
+  E.t = t;
+  E.N = pl->N;
   std::unique_lock<std::mutex> lock;
   if (nsets == 2) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
@@ -862,60 +574,22 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     const int set = nsets == 2 ? int(bidx & 1) : 0;
     const cudaStream_t bs = nsets == 2 ? pl->ist[set] : st;
     double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
-    double2* Y = (double2*)(ws + cl.off_Y) + size_t(set) * pairs_b * pl->sp.L;
-    double* rowparts = (double*)(ws + cl.off_rowsum) + size_t(set) * cl.ngroups * pl->N;
-    const int first = bidx < nsets;  // first batch of this scratch set
-    {
-      const cudaStream_t st = bs;
-      prof_begin(KC_ROWS, st);
-      int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, st);
-      if (rc) return rc;
-      prof_end(KC_ROWS, st);
-      // B' of the batch: natural [p][e] (cluster K1, or L1 = 1) or pair-interleaved [e][p] (K2)
-      const double2* Yb = U;
-      int64_t sE = 1, sP = pl->sp.L;
-      if (!pl->cluster && pl->sp.L1 > 1) {
-        prof_begin(KC_COLS, st);
-        rc = cols_dispatch(pl, U, Y, np, st);
-        if (rc) return rc;
-        prof_end(KC_COLS, st);
-        Yb = Y;
-        sE = np;
-        sP = 1;
-      }
-      prof_begin(KC_GATHER, st);
-      const int ppg = cl.ppg;
-      const unsigned ng = unsigned((np + ppg - 1) / ppg);
-      if (colmean) {
-        const size_t smem = size_t(kGatherThreads / 32) * ppg * sizeof(double2);
-        dim3 g((unsigned)nb3, ng);
-        switch (f) {
-          case QMC_F_IDENTITY:
-            k_gather_colmean<QMC_F_IDENTITY><<<g, kGatherThreads, smem, st>>>(
-                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
-            break;
-          case QMC_F_AFFINE:
-            k_gather_colmean<QMC_F_AFFINE><<<g, kGatherThreads, smem, st>>>(
-                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
-            break;
-          default:
-            k_gather_colmean<QMC_F_EXP><<<g, kGatherThreads, smem, st>>>(
-                Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, fparam, X, ldx, partial);
-        }
-        QMC_LAUNCHED();
-      } else if (f == QMC_F_ROWMEAN_RELU) {
-        // groups absent from a short last batch keep their sums (first = 0)
-        dim3 g(nblk(pl->N, kGatherThreads), ng);
-        k_gather<GM_ROWSUM><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal,
-                                                          pl->N, X, ldx, rowparts, first);
-        QMC_LAUNCHED();
-      } else {
-        dim3 g(nblk(pl->N, kGatherThreads), ng);
-        k_gather<GM_X><<<g, kGatherThreads, 0, st>>>(Yb, sE, sP, np, ppg, pair0, t, pl->d_R, colsum, pl->d_scal, pl->N, X,
-                                                     ldx, nullptr, 0);
-        QMC_LAUNCHED();
-      }
-      prof_end(KC_GATHER, st);
+    double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
+    E.rowpart = (double*)(ws + cl.off_rowsum);
+    prof_begin(KC_ROWS, bs);
+    int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, bs);
+    if (rc) return rc;
+    prof_end(KC_ROWS, bs);
+    prof_begin(KC_COLS, bs);
+    rc = cols_dispatch(pl, cl, U, np, pair0, E, part, colsum, bs);
+    if (rc) return rc;
+    prof_end(KC_COLS, bs);
+    if (colmean) {
+      prof_begin(KC_REDUCE, bs);
+      k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, cl.nbx, cl.part_stride, 2 * np, 2 * pair0, t,
+                                                         pl->N, out);
+      QMC_LAUNCHED();
+      prof_end(KC_REDUCE, bs);
     }
   }
   if (nsets == 2) {  // join
@@ -929,17 +603,8 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   }
   if (f == QMC_F_ROWMEAN_RELU) {
     prof_begin(KC_REDUCE, st);
-    // parts [set][group][N]; every written group of every set, fixed order
-    const int ngr = int(std::min<int64_t>(cl.ngroups, (npairs_total + cl.ppg - 1) / cl.ppg));
-    const int nsets_used = int(std::min<int64_t>(nsets, (npairs_total + pl->batch_pairs - 1) / pl->batch_pairs));
-    k_rowsum_reduce<<<nblk(pl->N, 256), 256, 0, st>>>((double*)(ws + cl.off_rowsum), ngr, cl.ngroups,
-                                                      nsets_used, pl->N, out);
-    QMC_LAUNCHED();
-    prof_end(KC_REDUCE, st);
-  }
-  if (colmean) {
-    prof_begin(KC_REDUCE, st);
-    k_colmean_reduce<<<nblk(t, 256), 256, 0, st>>>(partial, nb3, t, pl->N, out);
+    // parts [group][N], every pair group of the call, fixed order
+    k_rowsum_reduce<<<nblk(pl->N, 256), 256, 0, st>>>((double*)(ws + cl.off_rowsum), cl.ngroups_all, pl->N, out);
     QMC_LAUNCHED();
     prof_end(KC_REDUCE, st);
   }

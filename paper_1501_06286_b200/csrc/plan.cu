@@ -96,8 +96,8 @@ bool choose_split(int64_t m, int64_t s, Split* out) {
   int64_t cap_env = 0;
   if (const char* ev = getenv("QMC_L2_CAP")) cap_env = strtol(ev, nullptr, 10);  // tuning override
   auto try_len = [&](int64_t len) -> bool {
-    // rows of 4096 unless the columns would then exceed 16 (cluster limit)
-    // or s > 4096 (keep buckets small): then rows of 8192
+    // rows of 4096 unless the columns would then exceed 16 (one register
+    // stage in K2) or s > 4096 (keep buckets small): then rows of 8192
     int64_t cap = s > 4096 ? 8192 : 4096;
     if (cap == 4096 && len % 8192 == 0 && len / 4096 > 16) cap = 8192;
     if (cap_env >= 16) cap = cap_env;
@@ -105,7 +105,7 @@ bool choose_split(int64_t m, int64_t s, Split* out) {
     while (len % (l2 * 2) == 0 && l2 * 2 <= cap) l2 *= 2;
     if (l2 < 16 || (l2 < 256 && l2 != len)) return false;  // rows of >= 256, or one short row
     int64_t l1 = len / l2;
-    if (l1 > 1024 || !smooth235(l1)) return false;
+    if (!k2_split_R(l1)) return false;  // a column length K2 instantiates
     out->L = len;
     out->L1 = l1;
     out->L2 = l2;
@@ -146,7 +146,6 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_twL = take(size_t(sp.L2) * 16);
   l.off_tws = take(size_t(sp.L2) * 16);
   l.off_twj = take(size_t(sp.L1) * size_t(s) * 16);
-  l.off_radix1 = take(24 * 4);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
   l.total = o;
   return l;
@@ -426,18 +425,6 @@ static int validate_family(int family, int64_t N_or_D, int64_t s, int64_t* N, in
   return QMC_OK;
 }
 
-static int pick_radices(int64_t L1, int* r, int* n) {
-  int k = 0;
-  int64_t x = L1;
-  while (x % 8 == 0) { r[k++] = 8; x /= 8; }
-  while (x % 4 == 0) { r[k++] = 4; x /= 4; }
-  while (x % 2 == 0) { r[k++] = 2; x /= 2; }
-  while (x % 5 == 0) { r[k++] = 5; x /= 5; }
-  while (x % 3 == 0) { r[k++] = 3; x /= 3; }
-  *n = k;
-  return x == 1 ? QMC_OK : QMC_EINVAL_N;
-}
-
 static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p, int64_t s,
                          const int64_t* z_host, int phi, void* plan_ws, size_t plan_ws_bytes,
                          void* stream) {
@@ -473,37 +460,21 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->ws = (char*)plan_ws;
   pl->ws_bytes = plan_ws_bytes;
   {
-    // two scratch buffers of batch·L complex each, sized to stay in L2
-    // (~64 MB); at least two waves of row CTAs when that fits in ~96 MB
-    // U + Y of one batch ~128 MB: measured best on B200 for config 2 (fewer,
-    // longer launches outweigh the L2 overflow, which discards keep small)
-    const int64_t per_pair = 32 * sp.L;
-    int64_t bp = std::max<int64_t>(1, (int64_t(128) << 20) / per_pair);
+    // U of one batch (16·L bytes per pair) ~32 MB per scratch set, so that
+    // both sets stay in L2 next to the streamed X; at least two waves of K1
+    // CTAs; a multiple of the K2 pair group (16, 8 or 4 pairs)
+    const int64_t per_pair = 16 * sp.L;
+    int64_t bp = std::max<int64_t>(1, (int64_t(32) << 20) / per_pair);
     const int64_t want = (296 + sp.L1 - 1) / sp.L1;  // >= 2 waves of K1 CTAs
-    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(192) << 20) / per_pair));
-    pl->batch_pairs = std::min<int64_t>(bp, 256);
+    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(64) << 20) / per_pair));
+    bp = std::min<int64_t>(bp, 256);
+    bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
+    pl->batch_pairs = bp;
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
       if (v > 0) pl->batch_pairs = v;
     }
   }
-  // K1 with the cluster-fused column pass is opt-in (QMC_CLUSTER=1): on B200
-  // it measured no faster than K1 + K2
-  pl->cluster = (sp.L1 > 1 && getenv("QMC_CLUSTER")) ? rows_cluster_supported(pl) : 0;
-  cudaGetLastError();
-  {
-    int cb = 32;
-    while (cb > 1 && (int64_t(cb) * sp.L1 > 2048 || cb > sp.L2)) cb >>= 1;
-    pl->col_cb_smem = cb;
-    const int64_t L1 = sp.L1;
-    const bool reg_len = L1 == 2 || L1 == 3 || L1 == 4 || L1 == 5 || L1 == 6 || L1 == 8 || L1 == 9 ||
-                         L1 == 10 || L1 == 12 || L1 == 15 || L1 == 16 || L1 == 20 || L1 == 24 || L1 == 25 ||
-                         L1 == 32;
-    pl->col_cb = 4;
-    pl->col_reg = reg_len && sp.L2 >= 4 && cols_reg_smem(L1, pl->batch_pairs) <= (200u << 10);
-  }
-  rc = pick_radices(sp.L1, pl->rad1, &pl->nrad1);
-  if (rc) { delete pl; return rc; }
   char* b = pl->ws;
   pl->d_scal = (double*)(b + lay.off_scal);
   pl->d_P = (int32_t*)(b + lay.off_P);
@@ -520,7 +491,6 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_twL = (double2*)(b + lay.off_twL);
   pl->d_tws = (double2*)(b + lay.off_tws);
   pl->d_twj = (double2*)(b + lay.off_twj);
-  pl->d_rad1 = (int32_t*)(b + lay.off_radix1);
   cudaStream_t st = pl->stream;
 
   auto fail = [&](int code) {
@@ -547,7 +517,6 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_CHECK(cudaMemcpyAsync(d_z, z_host, sizeof(int64_t) * s, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
   if (!qf.empty())
     QMC_PLAN_CHECK(cudaMemcpyAsync(d_qf, qf.data(), sizeof(int64_t) * qf.size(), cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
-  QMC_PLAN_CHECK(cudaMemcpyAsync(pl->d_rad1, pl->rad1, sizeof(int32_t) * 24, cudaMemcpyHostToDevice, st) ? QMC_ECUDA : 0);
 
   // a0: generator
   if (family == QMC_FAMILY_LATTICE) {

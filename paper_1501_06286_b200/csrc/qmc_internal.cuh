@@ -57,9 +57,21 @@ struct PlanLayout {
 };
 PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
 
-// shared memory of the register column kernel for a batch of np pairs
-size_t cols_reg_smem(int64_t L1, int64_t np);
-int rows_cluster_supported(const qmc_plan* pl);
+// K2 column-pass splits L1 = R·M (pipeline.cu k_cols_x): R = 1 is one thread
+// per column with L1 values in registers; R > 1 is two register stages
+// through shared memory.  X(R, M) for every supported L1.
+#define QMC_K2_SPLITS(X)                                                                       \
+  X(1, 1) X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 8) X(1, 9) X(1, 10) X(1, 12) X(1, 15)   \
+  X(1, 16) X(2, 10) X(2, 12) X(5, 5) X(2, 16) X(4, 10) X(3, 16) X(4, 16) X(5, 16) X(6, 16)       \
+  X(8, 16) X(10, 16) X(12, 16) X(16, 16)
+// R of the K2 split of L1 (0: L1 not supported)
+inline int k2_split_R(int64_t L1) {
+#define QMC_K2_R(RR, MM) \
+  if (L1 == RR * MM) return RR;
+  QMC_K2_SPLITS(QMC_K2_R)
+#undef QMC_K2_R
+  return 0;
+}
 
 }  // namespace qmc
 
@@ -71,13 +83,7 @@ struct qmc_plan {
   uint64_t p;
   int64_t gen;
   qmc::Split sp;
-  int64_t batch_pairs;  // column pairs per batch (scratch sized to stay in L2)
-  int cluster;          // K1 fuses the column pass (thread-block cluster of L1 CTAs)
-  int col_reg;          // K2 register path (L1 <= 32, two direct radices)
-  int col_cb;           // K2 register path: columns e2 per CTA
-  int col_cb_smem;      // K2 shared-memory path: columns e2 per CTA
-  int nrad1;            // radices of L1
-  int rad1[24];
+  int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
   // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3
@@ -91,7 +97,7 @@ struct qmc_plan {
   double* d_scal;    // [0] = φ(0), [1] = generator (as double), [2] = status flags
   int32_t* d_P;      // [m]
   int32_t* d_L;      // [N]
-  int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1
+  int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1 (tables / tests)
   int32_t* d_e;      // [s]
   int32_t* d_bstart; // [L2+1]
   int32_t* d_bnext;  // [s]   per j: -2 if j is not the smallest index of its bucket
@@ -105,5 +111,4 @@ struct qmc_plan {
   double2* d_twL;    // [L2]  ω_L^k, k < L2
   double2* d_tws;    // [L2]  row-FFT stage twiddles, stage-major (fft.cuh reg_stage)
   double2* d_twj;    // [L1·s] twj[f1·s + j] = ω_L^{(e_j·f1) mod L} (K1 scatter twiddles)
-  int32_t* d_rad1;   // [24]
 };

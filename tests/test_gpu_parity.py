@@ -132,18 +132,19 @@ def test_edge_cases(qmc):
     A0 = torch.empty((0, 2), dtype=torch.float64, device="cuda").t()
     X0 = plan.matmul(A0)
     assert X0.shape == (13, 0)
-    # lda > s and ldx > N: padding rows of X untouched
+    # lda > s and ldx > t: padding columns of X untouched; odd ldx (scalar stores)
     w = W.custom_lattice(101, 30, 6, W.PHI_SHIFT_HALF, seed=9)
     plan = q.Plan.from_workload(w)
     Abig = torch.zeros((6, 40), dtype=torch.float64, device="cuda")
     Abig[:, :30] = torch.from_numpy(np.ascontiguousarray(w.A.T)).cuda()
     A = Abig.t()[:30]                       # (30, 6), lda = 40
-    Xbig = torch.full((6, 128), 7.5, dtype=torch.float64, device="cuda")
-    X = Xbig.t()[:101]                      # (101, 6), ldx = 128
-    plan.matmul(A, X)
-    Xh = Xbig.cpu().numpy()
-    assert np.all(Xh[:, 101:] == 7.5)
-    check_X(w, Xh[:, :101].T, X_full(w))
+    for ldx in (16, 9):
+        Xbig = torch.full((101, ldx), 7.5, dtype=torch.float64, device="cuda")
+        X = Xbig[:, :6]                     # (101, 6), row-major, ldx
+        plan.matmul(A, X)
+        Xh = Xbig.cpu().numpy()
+        assert np.all(Xh[:, 6:] == 7.5)
+        check_X(w, Xh[:, :6], X_full(w))
 
 
 def test_invalid_arguments(qmc):
@@ -174,7 +175,7 @@ def test_deterministic_and_shard_invariant(qmc):
     X1 = plan.matmul(A).clone()
     X2 = plan.matmul(A).clone()
     assert torch.equal(X1, X2)
-    Xs = qmc.colmajor_empty(plan.N, 64, "cuda")
+    Xs = qmc.x_empty(plan.N, 64, "cuda")
     plan.matmul(A[:, :24], Xs[:, :24])
     plan.matmul(A[:, 24:], Xs[:, 24:])
     assert torch.equal(X1, Xs)
@@ -188,7 +189,7 @@ def test_config2_full_and_rowmean_relu(qmc):
     w = W.config(2)
     plan = qmc.Plan.from_workload(w)
     A = qmc.to_device_colmajor(w.A, "cuda")
-    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    X = qmc.x_empty(plan.N, w.t, "cuda")
     rs = plan.mean(A, W.F_ROWMEAN_RELU, 0.0, X=X)
     Q = plan.finalize(W.F_ROWMEAN_RELU, rs, w.t)
     Xg = X.cpu().numpy()
@@ -210,7 +211,7 @@ def test_config3_sampled(qmc):
     w = W.config(3)
     plan = qmc.Plan.from_workload(w)
     A = qmc.to_device_colmajor(w.A, "cuda")
-    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    X = qmc.x_empty(plan.N, w.t, "cuda")
     means = plan.mean(A, W.F_AFFINE, 1.0, X=X)
     rows = sample_rows(w.N, 256, seed=3)
     idx = torch.from_numpy(rows).cuda()
@@ -250,7 +251,7 @@ def test_config5_sampled(qmc):
     w = W.config(5)
     plan = qmc.Plan.from_workload(w)
     A = qmc.to_device_colmajor(w.A, "cuda")
-    X = qmc.colmajor_empty(plan.N, w.t, "cuda")
+    X = qmc.x_empty(plan.N, w.t, "cuda")
     means = plan.mean(A, W.F_EXP, 0.0, X=X)
     rows = sample_rows(w.N, 256, seed=5)
     Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()

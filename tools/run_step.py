@@ -19,7 +19,7 @@ def main():
     w = W.config(a.config, t_override=a.t or None)
     plan = q.Plan.from_workload(w)
     A = q.to_device_colmajor(w.A, "cuda")
-    X = q.colmajor_empty(plan.N, w.t, "cuda")
+    X = q.x_empty(plan.N, w.t, "cuda")
     for _ in range(a.steps):
         if w.f is None:
             plan.matmul(A, X)

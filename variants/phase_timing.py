@@ -10,7 +10,7 @@ for bp in (1, 8, 32):
     w = W.config(2, t_override=2 * bp)
     plan = q.Plan.from_workload(w)
     A = q.to_device_colmajor(w.A, "cuda")
-    X = q.colmajor_empty(plan.N, w.t, "cuda")
+    X = q.x_empty(plan.N, w.t, "cuda")
     for _ in range(3):
         plan.matmul(A, X)
     torch.cuda.synchronize()
