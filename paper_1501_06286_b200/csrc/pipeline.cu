@@ -40,8 +40,6 @@ namespace qmc {
 constexpr int kUB = 4;
 constexpr int kColThreads = 256;  // K2 CTA size
 
-// K2 epilogue (runtime, CTA-uniform)
-enum Epilogue { EP_X = 0, EP_ROWSUM = 1, EP_SUM = 2, EP_AFFINE = 3, EP_EXP = 4 };
 
 // deterministic block sum (fixed shuffle tree, then warp 0 over warps)
 template <int NT>
@@ -65,19 +63,38 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* red) {
   return v;  // valid in thread 0
 }
 
+// ---------------------------------------------------------------- K0
+// a of the batch in bucket order: asort[p·s + q] = (A[j_q, k1], A[j_q, k2]),
+// j_q = bent[q].x (the entries of one bucket e2 = e_j mod L2 are adjacent,
+// in increasing j)
+__global__ void k_pack(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0, int np,
+                       const int4* __restrict__ bent, int64_t s, double2* __restrict__ asort) {
+  const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
+  if (q >= s || p >= np) return;
+  const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+  const int64_t j = __ldg(&bent[q].x);
+  asort[int64_t(p) * s + q] = make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
+}
+
 // ---------------------------------------------------------------- K1
-// One CTA per (row f1, pair p): L2/16 threads, 16 points per thread.
+// Persistent: CTA b takes the items (f1, p) = b, b + gridDim.x, ... (f1
+// fastest) of the batch; L2/16 threads, 16 points per thread.  Per item:
 //   T[f1,e2] = Σ_{j in bucket(e2)} a_j ω_L^{e_j f1}     (a_j = A[j,k1] + i A[j,k2])
 //   forward FFT_L2 → ·W[f1,:] → inverse FFT_L2 → U[p][f1][e2]
-// The twiddle conj(ω_L^{e2 f1}) of the second FFT dimension is applied by K2.
-// CTA f1 = 0 also writes the row-0 sums Σ_j a_j = DC term of the spectrum.
+// The scatter input of an item — (a, twiddle, e2) for the s entries in bucket
+// order — is staged in shared memory by cp.async in chunks of CH entries; the
+// next item's first chunk is in flight while this item's FFTs run.  A bucket
+// is summed in j order by the thread of its first entry in the chunk
+// (deterministic).  The twiddle conj(ω_L^{e2 f1}) of the second FFT dimension
+// is applied by K2.  Item f1 = 0 also writes the row-0 sums Σ_j a_j = DC term
+// of the spectrum.
 #ifdef QMC_PHASE_TIMING
 __device__ long long g_phase[4096][8];
-#define QMC_TS(i)                                                                                      \
-  do {                                                                                               \
-    __syncthreads();                                                                                 \
-    if (threadIdx.x == 0 && blockIdx.x + gridDim.x * blockIdx.y < 4096)                              \
-      g_phase[blockIdx.x + gridDim.x * blockIdx.y][i] = clock64();                                   \
+#define QMC_TS(i)                                                          \
+  do {                                                                     \
+    __syncthreads();                                                       \
+    if (threadIdx.x == 0 && item < 4096) g_phase[item][i] = clock64();     \
   } while (0)
 extern "C" int qmc_debug_phases(long long* host, int n) {
   return cudaMemcpyFromSymbol(host, g_phase, sizeof(long long) * 8 * n) == cudaSuccess ? 0 : -7;
@@ -87,89 +104,122 @@ extern "C" int qmc_debug_phases(long long* host, int n) {
   do {            \
   } while (0)
 #endif
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// shared memory of K1: the padded row, then the staging of CH entries
 template <int L2>
-__global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : QMC_ROWS_MINB))
-    k_rows16(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
-             const int32_t* __restrict__ e, const int32_t* __restrict__ bnext, int64_t s,
-             const double2* __restrict__ twj, const double2* __restrict__ tws,
-             const double2* __restrict__ W, double2* __restrict__ U, int64_t L, double* __restrict__ colsum) {
+__host__ __device__ constexpr size_t rows_smem(int CH) {
+  return size_t(PadE<L2, QMC_ROW_E>::size) * 16 + size_t(CH) * (16 + 16 + 4);
+}
+
+template <int L2>
+__global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_ROWS_MINB512 : QMC_ROWS_MINB))
+    k_rows16(const double2* __restrict__ asort, const int32_t* __restrict__ e2q, const uint32_t* __restrict__ occ,
+             int64_t s, int CH,
+             const double2* __restrict__ twj, const double2* __restrict__ tws, const double2* __restrict__ W,
+             double2* __restrict__ U, int64_t L, int L1, int np, int64_t pair0, int64_t t,
+             double* __restrict__ colsum) {
   extern __shared__ double2 smem[];
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
   double2* S = smem;
+  double2* stA = smem + PadE<L2, E>::size;
+  double2* stW = stA + CH;
+  int32_t* stE = reinterpret_cast<int32_t*>(stW + CH);
   const int tid = threadIdx.x;
-  const int f1 = blockIdx.x;
-  const int64_t p = blockIdx.y;
-  const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-  const bool has2 = k2 < t;
-  const double* a1 = A + k1 * lda;
-  const double* a2 = A + (has2 ? k2 : k1) * lda;
-  QMC_TS(0);
-  // scatter a' = P a fused with the first DFT dimension:
-  //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
-  // Entries in natural j order (coalesced, independent loads, issued before
-  // the shared row is cleared); the smallest j of each bucket sums the bucket
-  // along its collision chain in increasing j -> deterministic.
-  constexpr int UE = 4;
-  const double2* twr = twj + int64_t(f1) * s;
-  for (int j0 = 0; j0 < s; j0 += NT * UE) {
-    int ej[UE], nx[UE];
-    double2 a[UE], w[UE];
-#pragma unroll
-    for (int u = 0; u < UE; ++u) {
-      const int j = j0 + tid + u * NT;
-      nx[u] = -2;
-      if (j < s) {
-        ej[u] = __ldg(&e[j]);
-        nx[u] = __ldg(&bnext[j]);
-        a[u] = make_double2(__ldg(a1 + j), has2 ? __ldg(a2 + j) : 0.0);
-        w[u] = __ldg(&twr[j]);
-      }
+  const int nitems = L1 * np;
+  const int nch = int((s + CH - 1) / CH);
+  // stage chunk c of item it (all threads issue, one commit group)
+  auto issue = [&](int it, int c) {
+    const int f1 = it % L1, p = it / L1;
+    const int64_t q0 = int64_t(c) * CH;
+    const int n = int((CH < s - q0 ? CH : s - q0));
+    const double2* ga = asort + int64_t(p) * s + q0;
+    const double2* gw = twj + int64_t(f1) * s + q0;
+    for (int i = tid; i < n; i += NT) {
+      cp_async16(stA + i, ga + i);
+      cp_async16(stW + i, gw + i);
+      cp_async4(stE + i, e2q + q0 + i);
     }
-    if (j0 == 0) {
-#pragma unroll
-      for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = make_double2(0.0, 0.0);
-      __syncthreads();
-    }
-#pragma unroll
-    for (int u = 0; u < UE; ++u) {
-      if (nx[u] >= -1) {
-        double2 acc = cmul(a[u], w[u]);
-        for (int jj = nx[u]; jj >= 0;) {  // collisions (rare)
-          acc = cadd(acc, cmul(make_double2(__ldg(a1 + jj), has2 ? __ldg(a2 + jj) : 0.0), __ldg(&twr[jj])));
-          const int v = __ldg(&bnext[jj]);
-          jj = v <= -3 ? -3 - v : -1;
+    cp_async_commit();
+  };
+  int item = blockIdx.x;
+  if (item < nitems) issue(item, 0);
+  for (; item < nitems; item += gridDim.x) {
+    const int f1 = item % L1, p = item / L1;
+    QMC_TS(0);
+    for (int c = 0; c < nch; ++c) {
+      cp_async_wait_all();
+      __syncthreads();  // staging complete; every use of S by the previous item is done
+      // scatter a' = P a fused with the first DFT dimension:
+      //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
+      // The first entry of a bucket (size in e2q >> 13) sums it in j order and
+      // stores T (S holds the previous item's data elsewhere: only nonempty
+      // buckets are read back, by the occupancy mask); a bucket continued from
+      // the previous chunk is added to by this chunk's entry 0.
+      const int n = int(CH < s - int64_t(c) * CH ? CH : s - int64_t(c) * CH);
+      for (int i = tid; i < n; i += NT) {
+        const int pk = stE[i];
+        const int len = pk >> 13, e2 = pk & 8191;
+        if (len > 0) {
+          double2 acc = cmul(stA[i], stW[i]);
+          const int end = min(n, i + len);
+          for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(stA[k], stW[k]));
+          S[padE<E>(e2)] = acc;
+        } else if (i == 0) {  // continuation of a bucket from the previous chunk
+          double2 acc = cmul(stA[0], stW[0]);
+          for (int k = 1; k < n && stE[k] == pk; ++k) acc = cadd(acc, cmul(stA[k], stW[k]));
+          S[padE<E>(e2)] = cadd(S[padE<E>(e2)], acc);
         }
-        S[padE<E>(ej[u] & (L2 - 1))] = acc;
+      }
+      __syncthreads();  // staging consumed
+      if (c + 1 < nch) {
+        issue(item, c + 1);
+      } else if (item + gridDim.x < nitems) {
+        issue(item + gridDim.x, 0);  // overlaps this item's FFTs
       }
     }
-  }
-  __syncthreads();
-  QMC_TS(1);
-  double2 v[E];
-  load_strided<L2, E>(v, S);
-  fftE<L2, E, -1>(v, S, tws, tid);
-  QMC_TS(2);
-  if (f1 == 0 && tid == 0) {
-    colsum[k1] = v[0].x;
-    if (has2) colsum[k2] = v[0].y;
-  }
-  const double2* Wr = W + int64_t(f1) * L2;
+    QMC_TS(1);
+    double2 v[E];
 #pragma unroll
-  for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid + q * NT]));
-  QMC_TS(3);
-  fftE<L2, E, +1>(v, S, tws, tid);
-  QMC_TS(4);
-  // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
-  // whole sectors of kUB·16 bytes per f1
-  double2* Up = U + p * L + int64_t(f1) * kUB;
-  const int L1 = int(L / L2);
+    for (int q = 0; q < E; ++q) {  // nonempty buckets only (the rest of S is stale)
+      const int e2 = tid_fresh() + q * NT;
+      v[q] = (__ldg(&occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
+    }
+    fftE<L2, E, -1>(v, S, tws, tid);
+    QMC_TS(2);
+    if (f1 == 0 && tid == 0) {
+      const int64_t k1 = 2 * (pair0 + p);
+      colsum[k1] = v[0].x;
+      if (k1 + 1 < t) colsum[k1 + 1] = v[0].y;
+    }
+    const double2* Wr = W + int64_t(f1) * L2;
 #pragma unroll
-  for (int q = 0; q < E; ++q) {
-    const int e2 = tid + q * NT;
-    Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+    for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid + q * NT]));
+    QMC_TS(3);
+    fftE<L2, E, +1>(v, S, tws, tid);
+    QMC_TS(4);
+    // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
+    // whole sectors of kUB·16 bytes per f1
+    double2* Up = U + int64_t(p) * L + int64_t(f1) * kUB;
+#pragma unroll
+    for (int q = 0; q < E; ++q) {
+      const int e2 = tid + q * NT;
+      Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+    }
+    QMC_TS(5);
   }
-  QMC_TS(5);
+  cp_async_wait_all();
 }
 
 // ---------------------------------------------------------------- K2
@@ -186,52 +236,79 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? 1 : Q
 //           R-point inverse DFT over r → outputs e1 = k2 + M·k1.
 // Output i = L2·e1 + e2 < m is reordered row i, conventional row
 // n = P[(m - i) mod m] (i = 0 → n = 1).
+//
+// Epilogue EP (compile time): LIN writes c + X (c = 0 unless AFFINE) and
+// sums it per column; EXP writes X and sums exp(X) per column; ROWSUM writes
+// X and the row sums over the pair group (warp transpose through shared
+// memory, then a fixed-order sum).
+enum { EPK_LIN = 0, EPK_EXP = 1, EPK_ROWSUM = 2 };
+
 struct EpiArgs {
-  int ep;
-  double fparam;
-  double* X;
+  double fparam;     // c of AFFINE (0 otherwise)
+  double* X;         // may be NULL (means only)
   int64_t ldx;
   int xvec;          // X + n·ldx + k 16-byte aligned for even k
   int64_t t;
-  int64_t kbase;     // first column of the CTA's pair group: 2·(pair0 + pg0)
-  double* rowpart;   // EP_ROWSUM: partial row sums [pair group of the call][N]
+  double* rowpart;   // ROWSUM: partial row sums [pair group of the call][N]
   int64_t N;
 };
 
-// One output value v (columns k = kbase + 2p, k + 1) of row n.  Must be
-// called by all 32 lanes of the warp together (EP_ROWSUM shuffles).
-__device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, int p, int PG, bool okp, bool okrow,
-                                     double2& acc) {
-  const int64_t k = E.kbase + 2 * p;
-  const bool has2 = k + 1 < E.t;
-  if (E.ep == EP_AFFINE) {
+// one output value v of columns (k, k + 1), row n (ok: a real row and pair)
+template <int EP>
+__device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, bool ok, bool has2, double* xk,
+                                     double2& acc, double& rsum) {
+  if (EP == EPK_LIN) {
     v.x += E.fparam;
     v.y += E.fparam;
   }
-  const bool ok = okp && okrow;
-  if (ok) {
-    if (E.X) {
-      double* xp = E.X + n * E.ldx + k;
-      if (E.xvec && has2) {
-        *reinterpret_cast<double2*>(xp) = v;
-      } else {
-        xp[0] = v.x;
-        if (has2) xp[1] = v.y;
-      }
+  if (!has2) v.y = 0.0;
+  if (ok && xk) {
+    double* xp = xk + n * E.ldx;
+    if (E.xvec && has2) {
+      *reinterpret_cast<double2*>(xp) = v;
+    } else {
+      xp[0] = v.x;
+      if (has2) xp[1] = v.y;
     }
-    if (E.ep == EP_SUM || E.ep == EP_AFFINE) {
+  }
+  if (EP == EPK_LIN) {
+    if (ok) {
       acc.x += v.x;
-      if (has2) acc.y += v.y;
-    } else if (E.ep == EP_EXP) {
+      acc.y += v.y;
+    }
+  } else if (EP == EPK_EXP) {
+    if (ok) {
       acc.x += exp(v.x);
       if (has2) acc.y += exp(v.y);
     }
+  } else {
+    rsum = ok ? v.x + v.y : 0.0;
   }
-  if (E.ep == EP_ROWSUM) {
-    double r = ok ? v.x + (has2 ? v.y : 0.0) : 0.0;
-    for (int o = PG >> 1; o > 0; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
-    if (okrow && p == 0) E.rowpart[n] = r;
+}
+
+// ROWSUM: the NR row values of every lane of the warp → per (lane group of
+// PG pairs, row slot) sums over the group's lanes in lane order → rowpart[n].
+// Tw: this warp's NR·33 doubles of shared memory, Tn: NR·8 ints.
+template <int NR>
+__device__ __forceinline__ void rowsum_flush(const double (&r)[NR], const int (&nrow)[NR], int PG, double* Tw,
+                                             int* Tn, double* rowpart) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int k = 0; k < NR; ++k) {
+    Tw[k * 33 + lane] = r[k];
+    if (lane % PG == 0) Tn[k * 8 + lane / PG] = nrow[k];
   }
+  __syncwarp();
+  const int G = 32 / PG;
+  for (int rr = lane; rr < G * NR; rr += 32) {
+    const int q = rr / NR, k = rr - q * NR;
+    const double* src = Tw + k * 33 + q * PG;
+    double sum = 0.0;
+    for (int p = 0; p < PG; ++p) sum += src[p];
+    const int n = Tn[k * 8 + q];
+    if (n >= 0) rowpart[n] = sum;
+  }
+  __syncwarp();
 }
 
 // ω_L^x for 0 <= x < L from ω_{L1} (tw1) and ω_L^k, k < L2 (twL)
@@ -240,7 +317,7 @@ __device__ __forceinline__ double2 omegaL(int64_t x, int lg2L2, int L2, const do
   return cmul(__ldg(&tw1[x >> lg2L2]), __ldg(&twL[x & (L2 - 1)]));
 }
 
-template <int R, int M>
+template <int R, int M, int EP>
 __global__ void __launch_bounds__(kColThreads, 2)
     k_cols_x(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int64_t m, int np, int PG,
              const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
@@ -248,28 +325,35 @@ __global__ void __launch_bounds__(kColThreads, 2)
              double* __restrict__ part, int part_stride) {
   constexpr int L1 = R * M;
   constexpr int LP = L1 | 1;  // odd pitch (in 16-B units): conflict-free stage exchange
+  constexpr int NR = R == 1 ? L1 : R;  // output rows per item
   extern __shared__ double2 sm[];
-  const int tid = threadIdx.x;
+  __shared__ double rsT[EP == EPK_ROWSUM ? kColThreads / 32 : 1][EP == EPK_ROWSUM ? NR * 33 : 1];
+  __shared__ int rsN[EP == EPK_ROWSUM ? kColThreads / 32 : 1][EP == EPK_ROWSUM ? NR * 8 : 1];
+  const int tid = threadIdx.x, warp = tid >> 5;
   const int CB = (R == 1 ? kColThreads : 32) / PG;
   const int pg0 = blockIdx.y * PG;
   const int p = tid % PG;
   const int pair = pg0 + p;
   const bool okp = pair < np;
   const double2* Up = U + int64_t(okp ? pair : 0) * L;
-  E.kbase = 2 * (pair0 + pg0);
-  if (E.ep == EP_ROWSUM) E.rowpart += (pair0 / PG + blockIdx.y) * E.N;  // this group's row sums
+  const int64_t k = 2 * (pair0 + pair);  // this lane's columns k, k + 1
+  const bool has2 = k + 1 < E.t;
+  double* xk = E.X ? E.X + k : nullptr;
+  double* rowpart = EP == EPK_ROWSUM ? E.rowpart + (pair0 / PG + blockIdx.y) * E.N : nullptr;
   double2 acc = make_double2(0.0, 0.0);
   // row 0: X[0, k] = φ(0) Σ_j A[j, k]
-  if (blockIdx.x == 0 && tid < 32) {
+  if (blockIdx.x == 0 && warp == 0) {
     const bool okrow = tid < PG;
     double2 v0 = make_double2(0.0, 0.0);
-    const int64_t k = E.kbase + 2 * p;
     if (okp && okrow) {
       const double phi0 = __ldg(scal);
       v0.x = phi0 * colsum[k];
-      v0.y = k + 1 < E.t ? phi0 * colsum[k + 1] : 0.0;
+      v0.y = has2 ? phi0 * colsum[k + 1] : 0.0;
     }
-    emit(E, v0, 0, p, PG, okp, okrow, acc);
+    double r0[1];
+    int n0[1] = {okrow ? 0 : -1};
+    emit<EP>(E, v0, 0, okp && okrow, has2, xk, acc, r0[0]);
+    if (EP == EPK_ROWSUM) rowsum_flush<1>(r0, n0, PG, &rsT[0][0], &rsN[0][0], rowpart);
   }
   if constexpr (R == 1) {
     const int c = tid / PG;
@@ -308,9 +392,10 @@ __global__ void __launch_bounds__(kColThreads, 2)
       }
     }
     reg_dft<L1, +1>(v, tw1);
+    double r[L1];
 #pragma unroll
-    for (int e1 = 0; e1 < L1; ++e1)
-      emit(E, v[e1], nrow[e1] < 0 ? 0 : nrow[e1], p, PG, okp, nrow[e1] >= 0, acc);
+    for (int e1 = 0; e1 < L1; ++e1) emit<EP>(E, v[e1], nrow[e1], okp && nrow[e1] >= 0, has2, xk, acc, r[e1]);
+    if (EP == EPK_ROWSUM) rowsum_flush<L1>(r, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
   } else {
     double2* T = sm;  // [(p + PG·c)·LP + r·M + k2]
     const int nA = 32 * R;  // = PG·CB·R items
@@ -363,27 +448,28 @@ __global__ void __launch_bounds__(kColThreads, 2)
 #pragma unroll
       for (int r = 0; r < R; ++r) z[r] = Tp[r * M];
       reg_dft<R, +1>(z, tw1, L1 / R);
+      double rr[R];
 #pragma unroll
-      for (int k1 = 0; k1 < R; ++k1)
-        emit(E, z[k1], nrow[k1] < 0 ? 0 : nrow[k1], p, PG, okp, nrow[k1] >= 0, acc);
+      for (int k1 = 0; k1 < R; ++k1) emit<EP>(E, z[k1], nrow[k1], okp && nrow[k1] >= 0, has2, xk, acc, rr[k1]);
+      if (EP == EPK_ROWSUM) rowsum_flush<R>(rr, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
     }
   }
   // per-column partial sums of this CTA: lanes with equal p, then warps in order
-  if (E.ep == EP_SUM || E.ep == EP_AFFINE || E.ep == EP_EXP) {
+  if (EP != EPK_ROWSUM) {
     for (int o = PG; o < 32; o <<= 1) {
       acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
       acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
     }
     __shared__ double2 red[kColThreads / 32][16];
-    const int w = tid >> 5, l = tid & 31;
-    if (l < PG) red[w][l] = acc;
+    const int l = tid & 31;
+    if (l < PG) red[warp][l] = acc;
     __syncthreads();
-    if (tid < PG && okp) {
-      double2 s = red[0][tid];
-      for (int ww = 1; ww < kColThreads / 32; ++ww) s = cadd(s, red[ww][tid]);
+    if (tid < PG && okp && part) {
+      double2 sacc = red[0][tid];
+      for (int ww = 1; ww < kColThreads / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
       double* dst = part + int64_t(blockIdx.x) * part_stride + 2 * pair;
-      dst[0] = s.x;
-      dst[1] = s.y;
+      dst[0] = sacc.x;
+      dst[1] = sacc.y;
     }
   }
 }
@@ -434,7 +520,7 @@ static int pair_group(int64_t pairs_b) { return pairs_b >= 16 ? 16 : pairs_b >= 
 static int cols_cb(const qmc_plan* pl, int PG) { return (k2_split_R(pl->sp.L1) == 1 ? kColThreads : 32) / PG; }
 
 struct CallLayout {
-  size_t off_U, off_colsum, off_part, off_rowsum, total;
+  size_t off_U, off_asort, off_colsum, off_part, off_rowsum, total;
   int PG, ngroups, ngroups_all, nbx, nsets, part_stride;
 };
 
@@ -456,6 +542,7 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   c.nbx = int((pl->sp.L2 + CB - 1) / CB);
   c.part_stride = int(2 * c.ngroups * c.PG);
   c.off_U = take(size_t(c.nsets) * pairs * pl->sp.L * 16);
+  c.off_asort = take(size_t(c.nsets) * pairs * pl->s * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   c.off_part = take(colmean ? size_t(c.nsets) * c.nbx * c.part_stride * 8 : 0);
@@ -471,24 +558,42 @@ static void set_smem_attr(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
+// staging entries of K1 per chunk: the whole scatter input when it fits
+// next to the row at the kernel's residency (2 CTAs per SM for L2 <= 4096)
+static int rows_chunk(int64_t L2, int64_t s) {
+  const int64_t cap = L2 >= 8192 ? 2048 : 1024;
+  return int(std::min<int64_t>(cap, (s + 31) / 32 * 32));
+}
+
 template <int L2>
-static int launch_rows(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0,
-                       double2* U, int npairs, double* colsum, cudaStream_t st) {
-  const size_t smem = size_t(PadE<L2, QMC_ROW_E>::size) * sizeof(double2);
+static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
+                       double* colsum, cudaStream_t st) {
+  const int CH = rows_chunk(L2, pl->s);
+  const size_t smem = rows_smem<L2>(CH);
   auto kern = k_rows16<L2>;
   set_smem_attr(kern, smem);
-  dim3 grid((unsigned)pl->sp.L1, (unsigned)npairs);
-  kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(A, lda, t, pair0, pl->d_e, pl->d_bnext, pl->s, pl->d_twj, pl->d_tws,
-                                           pl->d_W, U, pl->sp.L, colsum);
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2 / QMC_ROW_E, smem);
+  if (pl->k1_per_sm > 0) per_sm = std::min(per_sm, pl->k1_per_sm);
+  const int64_t items = pl->sp.L1 * int64_t(np);
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, int64_t(nsm) * std::max(per_sm, 1))));
+  kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(asort, pl->d_e2q, pl->d_occ, pl->s, CH, pl->d_twj, pl->d_tws, pl->d_W, U, pl->sp.L,
+                                           int(pl->sp.L1), np, pair0, t, colsum);
   QMC_LAUNCHED();
   return QMC_OK;
 }
 
-static int rows_dispatch(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int64_t pair0, double2* U,
-                         int np, double* colsum, cudaStream_t st) {
+static int rows_dispatch(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
+                         double* colsum, cudaStream_t st) {
   switch (pl->sp.L2) {
 #define QMC_ROWS_CASE(NN) \
-  case NN: return launch_rows<NN>(pl, A, lda, t, pair0, U, np, colsum, st);
+  case NN: return launch_rows<NN>(pl, asort, t, pair0, U, np, colsum, st);
     QMC_ROWS_CASE(16) QMC_ROWS_CASE(32) QMC_ROWS_CASE(64) QMC_ROWS_CASE(128) QMC_ROWS_CASE(256)
     QMC_ROWS_CASE(512) QMC_ROWS_CASE(1024) QMC_ROWS_CASE(2048) QMC_ROWS_CASE(4096) QMC_ROWS_CASE(8192)
 #undef QMC_ROWS_CASE
@@ -502,12 +607,12 @@ static int ilog2(int64_t x) {
   return r;
 }
 
-template <int R, int M>
-static int launch_cols(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
-                       const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+template <int R, int M, int EP>
+static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
+                          const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
   constexpr int L1 = R * M;
   const size_t smem = R == 1 ? 0 : size_t(32) * (L1 | 1) * sizeof(double2);
-  auto kern = k_cols_x<R, M>;
+  auto kern = k_cols_x<R, M, EP>;
   set_smem_attr(kern, smem);
   dim3 g((unsigned)cl.nbx, (unsigned)((np + cl.PG - 1) / cl.PG));
   kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
@@ -516,11 +621,21 @@ static int launch_cols(const qmc_plan* pl, const CallLayout& cl, const double2* 
   return QMC_OK;
 }
 
-static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
+template <int R, int M>
+static int launch_cols(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0, int ep,
+                       const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+  switch (ep) {
+    case EPK_EXP: return launch_cols_ep<R, M, EPK_EXP>(pl, cl, U, np, pair0, E, part, colsum, st);
+    case EPK_ROWSUM: return launch_cols_ep<R, M, EPK_ROWSUM>(pl, cl, U, np, pair0, E, part, colsum, st);
+    default: return launch_cols_ep<R, M, EPK_LIN>(pl, cl, U, np, pair0, E, part, colsum, st);
+  }
+}
+
+static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0, int ep,
                          const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
   const int R = k2_split_R(pl->sp.L1), M = int(pl->sp.L1) / std::max(R, 1);
 #define QMC_COLS_CASE(RR, MM) \
-  if (R == RR && M == MM) return launch_cols<RR, MM>(pl, cl, U, np, pair0, E, part, colsum, st);
+  if (R == RR && M == MM) return launch_cols<RR, MM>(pl, cl, U, np, pair0, ep, E, part, colsum, st);
   QMC_K2_SPLITS(QMC_COLS_CASE)
 #undef QMC_COLS_CASE
   return QMC_EINVAL_N;
@@ -547,12 +662,8 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int nsets = cl.nsets;
   EpiArgs E;
-  E.ep = f == QMC_F_ROWMEAN_RELU ? EP_ROWSUM
-         : f == QMC_F_IDENTITY   ? EP_SUM
-         : f == QMC_F_AFFINE     ? EP_AFFINE
-         : f == QMC_F_EXP        ? EP_EXP
-                                 : EP_X;
-  E.fparam = fparam;
+  const int ep = f == QMC_F_ROWMEAN_RELU ? EPK_ROWSUM : f == QMC_F_EXP ? EPK_EXP : EPK_LIN;
+  E.fparam = f == QMC_F_AFFINE ? fparam : 0.0;
   E.X = X;
   E.ldx = ldx;
   E.xvec = X && (ldx % 2 == 0) && (uintptr_t(X) % 16 == 0);
@@ -576,12 +687,17 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
     double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
     E.rowpart = (double*)(ws + cl.off_rowsum);
+    double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->s;
+    prof_begin(KC_PACK, bs);
+    k_pack<<<dim3(nblk(pl->s, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_bent, pl->s, asort);
+    QMC_LAUNCHED();
+    prof_end(KC_PACK, bs);
     prof_begin(KC_ROWS, bs);
-    int rc = rows_dispatch(pl, A, lda, t, pair0, U, np, colsum, bs);
+    int rc = rows_dispatch(pl, asort, t, pair0, U, np, colsum, bs);
     if (rc) return rc;
     prof_end(KC_ROWS, bs);
     prof_begin(KC_COLS, bs);
-    rc = cols_dispatch(pl, cl, U, np, pair0, E, part, colsum, bs);
+    rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs);
     if (rc) return rc;
     prof_end(KC_COLS, bs);
     if (colmean) {

@@ -138,7 +138,8 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_e = take(size_t(s) * 4);
   l.off_bstart = take(size_t(sp.L2 + 1) * 4);
   l.off_bent = take(size_t(s) * 16);
-  l.off_bnext = take(size_t(s) * 4);
+  l.off_e2q = take(size_t(s) * 4);
+  l.off_occ = take(size_t(sp.L2 / 32 + 1) * 4);
   l.off_zeta = take(size_t(m) * 8);
   l.off_W = take(size_t(sp.L) * 16);
   l.off_tw1 = take(size_t(sp.L1) * 16);
@@ -255,9 +256,12 @@ __global__ void k_colmap(const int64_t* __restrict__ z, int64_t s, const int32_t
   if (j < s) e[j] = L[z[j]];
 }
 
-// Stable counting sort of j by e2 = e_j mod L2 (one CTA; plan time only).
+// Stable counting sort of j by e2 = e_j mod L2 (one CTA; plan time only):
+// bent[q] = {j, e_j, e2, end of the bucket if q is its first entry else -1};
+// e2q[q] = e2 | (bucket size << 13) if q is the first entry of its bucket,
+// else e2 (K1 stages e2q; L2 <= 8192); occ = bitmap of the nonempty buckets.
 __global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ bstart,
-                          int4* __restrict__ bent, int32_t* __restrict__ bnext) {
+                          int4* __restrict__ bent, int32_t* __restrict__ e2q, uint32_t* __restrict__ occ) {
   extern __shared__ int32_t cursor[];
   for (int i = threadIdx.x; i <= L2; i += blockDim.x) bstart[i] = 0;
   __syncthreads();
@@ -271,17 +275,11 @@ __global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int3
       const int pos = cursor[ej & (L2 - 1)]++;
       const int e2 = ej & (L2 - 1);
       bent[pos] = make_int4(int(j), ej, e2, pos == bstart[e2] ? bstart[e2 + 1] : -1);
+      e2q[pos] = pos == bstart[e2] ? e2 | ((bstart[e2 + 1] - bstart[e2]) << 13) : e2;
     }
-    // collision chains in increasing j (entries of a bucket are in j order)
+    for (int w = 0; w <= L2 / 32; ++w) occ[w] = 0u;
     for (int i = 0; i < L2; ++i)
-      for (int pos = bstart[i]; pos < bstart[i + 1]; ++pos)
-        bnext[bent[pos].x] = pos == bstart[i] ? (pos + 1 < bstart[i + 1] ? bent[pos + 1].x : -1)
-                                              : -2;
-    // non-first entries point to the next one too: chain walk uses bnext of
-    // the first only for the head; encode followers as -(next)-3
-    for (int i = 0; i < L2; ++i)
-      for (int pos = bstart[i] + 1; pos < bstart[i + 1]; ++pos)
-        bnext[bent[pos].x] = pos + 1 < bstart[i + 1] ? -(bent[pos + 1].x) - 3 : -2;
+      if (bstart[i + 1] > bstart[i]) occ[i >> 5] |= 1u << (i & 31);
   }
 }
 
@@ -331,13 +329,14 @@ __global__ void k_stage_twiddles(double2* __restrict__ tws, int N, int E) {
   }
 }
 
-// twj[f1·s + j] = ω_L^{(e_j·f1) mod L}: the twiddle of entry j in row f1 of
-// the scatter fused with the first DFT dimension (K1)
-__global__ void k_twj(const int32_t* __restrict__ e, int64_t s, int64_t L, int L1, double2* __restrict__ twj) {
+// twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x: the twiddle of the
+// q-th entry (bucket order) in row f1 of the scatter fused with the first DFT
+// dimension (K1)
+__global__ void k_twj(const int4* __restrict__ bent, int64_t s, int64_t L, int L1, double2* __restrict__ twj) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= s * L1) return;
-  const int64_t f1 = i / s, j = i % s;
-  const int64_t x = (int64_t(e[j]) * f1) % L;
+  const int64_t f1 = i / s, q = i % s;
+  const int64_t x = (int64_t(bent[q].y) * f1) % L;
   double sv, cv;
   sincospi(2.0 * double(x) / double(L), &sv, &cv);
   twj[i] = make_double2(cv, -sv);
@@ -460,16 +459,18 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->ws = (char*)plan_ws;
   pl->ws_bytes = plan_ws_bytes;
   {
-    // U of one batch (16·L bytes per pair) ~32 MB per scratch set, so that
-    // both sets stay in L2 next to the streamed X; at least two waves of K1
-    // CTAs; a multiple of the K2 pair group (16, 8 or 4 pairs)
+    // U of one batch (16·L bytes per pair) ~64 MB per scratch set (measured
+    // best for config 2: fewer, longer K1 launches keep more items per
+    // persistent CTA); at least two waves of K1 CTAs; a multiple of the K2
+    // pair group (16, 8 or 4 pairs)
     const int64_t per_pair = 16 * sp.L;
-    int64_t bp = std::max<int64_t>(1, (int64_t(32) << 20) / per_pair);
+    int64_t bp = std::max<int64_t>(1, (int64_t(64) << 20) / per_pair);
     const int64_t want = (296 + sp.L1 - 1) / sp.L1;  // >= 2 waves of K1 CTAs
     if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(64) << 20) / per_pair));
     bp = std::min<int64_t>(bp, 256);
     bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
     pl->batch_pairs = bp;
+    if (const char* ev = getenv("QMC_K1_PER_SM")) pl->k1_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
       if (v > 0) pl->batch_pairs = v;
@@ -483,7 +484,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_e = (int32_t*)(b + lay.off_e);
   pl->d_bstart = (int32_t*)(b + lay.off_bstart);
   pl->d_bent = (int4*)(b + lay.off_bent);
-  pl->d_bnext = (int32_t*)(b + lay.off_bnext);
+  pl->d_e2q = (int32_t*)(b + lay.off_e2q);
+  pl->d_occ = (uint32_t*)(b + lay.off_occ);
   pl->d_zeta = (double*)(b + lay.off_zeta);
   pl->d_W = (double2*)(b + lay.off_W);
   pl->d_tw1 = (double2*)(b + lay.off_tw1);
@@ -551,7 +553,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_colmap<<<blocks(s, 256), 256, 0, st>>>(d_z, s, pl->d_L, pl->d_e);
   QMC_PLAN_LAUNCHED();
-  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bent, pl->d_bnext);
+  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bent, pl->d_e2q,
+                                                 pl->d_occ);
   QMC_PLAN_LAUNCHED();
   k_rtable<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, m, pl->d_R);
   QMC_PLAN_LAUNCHED();
@@ -566,7 +569,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_stage_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tws, int(sp.L2), QMC_ROW_E);
   QMC_PLAN_LAUNCHED();
-  k_twj<<<blocks(sp.L1 * s, 256), 256, 0, st>>>(pl->d_e, s, sp.L, int(sp.L1), pl->d_twj);
+  k_twj<<<blocks(sp.L1 * s, 256), 256, 0, st>>>(pl->d_bent, s, sp.L, int(sp.L1), pl->d_twj);
   QMC_PLAN_LAUNCHED();
   QMC_PLAN_CHECK(spectrum_dispatch(pl));
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
@@ -574,7 +577,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
 #undef QMC_PLAN_LAUNCHED
   pl->nstreams = 1;
   pl->mu = new (std::nothrow) std::mutex();
-  if (!getenv("QMC_ONE_STREAM") && pl->mu &&
+  const char* one = getenv("QMC_ONE_STREAM");
+  if (!(one && one[0] == '1') && pl->mu &&
       cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
       cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
       cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&

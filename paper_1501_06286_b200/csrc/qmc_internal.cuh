@@ -52,8 +52,8 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // Plan-workspace carve-up (device pointers), identical for the size query
 // and the create call.
 struct PlanLayout {
-  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_bnext, off_zeta, off_W,
-      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_radix1, off_tmp, total;
+  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_zeta, off_W,
+      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_tmp, total;
 };
 PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
 
@@ -84,6 +84,7 @@ struct qmc_plan {
   int64_t gen;
   qmc::Split sp;
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
+  int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
   // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3
@@ -100,8 +101,9 @@ struct qmc_plan {
   int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1 (tables / tests)
   int32_t* d_e;      // [s]
   int32_t* d_bstart; // [L2+1]
-  int32_t* d_bnext;  // [s]   per j: -2 if j is not the smallest index of its bucket
-                     //       (e2 = e_j mod L2), else the next j of the bucket (-1: none)
+  int32_t* d_e2q;    // [s]   e2 = e_j mod L2 of the q-th entry in bucket order, | (bucket
+                     //       size << 13) on the first entry of each bucket
+  uint32_t* d_occ;   // [L2/32+1] bitmap of the nonempty buckets e2
   int4* d_bent;      // [s]   bucket order (e2 = e_j mod L2, then j): {j, e_j, e2,
                      //       end of this bucket if the entry is its first, else -1}
   double* d_zeta;    // [m]
@@ -110,5 +112,6 @@ struct qmc_plan {
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
   double2* d_tws;    // [L2]  row-FFT stage twiddles, stage-major (fft.cuh reg_stage)
-  double2* d_twj;    // [L1·s] twj[f1·s + j] = ω_L^{(e_j·f1) mod L} (K1 scatter twiddles)
+  double2* d_twj;    // [L1·s] twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x (K1 scatter
+                     //        twiddles in bucket order)
 };

@@ -8,3 +8,7 @@
 #ifndef QMC_ROWS_MINB
 #define QMC_ROWS_MINB 2
 #endif
+// ... for K1 CTAs of 512 or more threads
+#ifndef QMC_ROWS_MINB512
+#define QMC_ROWS_MINB512 1
+#endif
