@@ -42,6 +42,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--t", type=int, default=0, help="override the config's t (diagnostics only)")
     return ap.parse_args()
 
 
@@ -144,7 +145,7 @@ def reference_arm(args, rank, world):
     import qmc_workloads as W
     if rank != 0:
         return
-    w = W.config(args.config)
+    w = W.config(args.config, t_override=args.t or None)
     rows = 1024
     # warmup + timed steps, each a bounded sample of `rows` rows × all t columns
     for _ in range(args.warmup):
@@ -183,7 +184,7 @@ def ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     from paper_1501_06286_b200.dist import combine_means, shard_columns
-    w = W.config(args.config)
+    w = W.config(args.config, t_override=args.t or None)
     G = world
     c0, c1 = shard_columns(w.t, G, rank)
     tl = c1 - c0

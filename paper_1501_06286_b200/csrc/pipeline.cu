@@ -40,6 +40,16 @@ namespace qmc {
 constexpr int kUB = 4;
 constexpr int kColThreads = 256;  // K2 CTA size
 
+// X is written once and never read back by the library: evict-first stores
+// keep it from pushing the batch's U out of L2 (QMC_X_PLAIN_STORES: plain)
+#ifndef QMC_X_PLAIN_STORES
+#define QMC_XST2(p, v) stcs2(p, v)
+#define QMC_XST(p, v) stcs(p, v)
+#else
+#define QMC_XST2(p, v) (*reinterpret_cast<double2*>(p) = (v))
+#define QMC_XST(p, v) (*(p) = (v))
+#endif
+
 
 // deterministic block sum (fixed shuffle tree, then warp 0 over warps)
 template <int NT>
@@ -212,10 +222,17 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
     // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
     // whole sectors of kUB·16 bytes per f1
     double2* Up = U + int64_t(p) * L + int64_t(f1) * kUB;
+#ifdef QMC_U_HINTS
+    const uint64_t pol = policy_evict_last();
+#endif
 #pragma unroll
     for (int q = 0; q < E; ++q) {
       const int e2 = tid + q * NT;
+#ifdef QMC_U_HINTS
+      st_hint(&Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)], v[q], pol);
+#else
       Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+#endif
     }
     QMC_TS(5);
   }
@@ -265,10 +282,10 @@ __device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, boo
   if (ok && xk) {
     double* xp = xk + n * E.ldx;
     if (E.xvec && has2) {
-      *reinterpret_cast<double2*>(xp) = v;
+      QMC_XST2(xp, v);
     } else {
-      xp[0] = v.x;
-      if (has2) xp[1] = v.y;
+      QMC_XST(xp, v.x);
+      if (has2) QMC_XST(xp + 1, v.y);
     }
   }
   if (EP == EPK_LIN) {
@@ -284,6 +301,45 @@ __device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, boo
   } else {
     rsum = ok ? v.x + v.y : 0.0;
   }
+}
+
+// Fast path (every pair of the tile present, t even, X 16-byte aligned with
+// even ldx, every output row real): no predicates
+template <int EP>
+__device__ __forceinline__ void emit_fast(const EpiArgs& E, double2 v, int n, double* xk, double2& acc,
+                                          double& rsum) {
+  if (EP == EPK_LIN) {
+    v.x += E.fparam;
+    v.y += E.fparam;
+  }
+  if (xk) QMC_XST2(xk + int64_t(n) * E.ldx, v);
+  if (EP == EPK_LIN) {
+    acc.x += v.x;
+    acc.y += v.y;
+  } else if (EP == EPK_EXP) {
+    acc.x += exp(v.x);
+    acc.y += exp(v.y);
+  } else {
+    rsum = v.x + v.y;
+  }
+}
+
+// ROWSUM, 16 rows × 16 lanes (PG = 16): butterfly reduce-scatter over the
+// half-warp (xor 8, 4, 2, 1; fixed order) — on return r[0] of lane l is the
+// sum over the 16 lanes of row (l & 15).
+__device__ __forceinline__ double rowsum_butterfly16(double (&r)[16]) {
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int h = 8; h > 0; h >>= 1) {
+    const bool up = lane & h;
+#pragma unroll
+    for (int k = 0; k < h; ++k) {
+      const double send = up ? r[k] : r[k + h];
+      const double keep = up ? r[k + h] : r[k];
+      r[k] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+    }
+  }
+  return r[0];
 }
 
 // ROWSUM: the NR row values of every lane of the warp → per (lane group of
@@ -317,7 +373,7 @@ __device__ __forceinline__ double2 omegaL(int64_t x, int lg2L2, int L2, const do
   return cmul(__ldg(&tw1[x >> lg2L2]), __ldg(&twL[x & (L2 - 1)]));
 }
 
-template <int R, int M, int EP>
+template <int R, int M, int EP, bool FAST>
 __global__ void __launch_bounds__(kColThreads, 2)
     k_cols_x(const double2* __restrict__ U, int64_t L, int L2, int lg2L2, int64_t m, int np, int PG,
              const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
@@ -369,8 +425,14 @@ __global__ void __launch_bounds__(kColThreads, 2)
     double2 v[L1];
     const double2* ub = Up + int64_t(e2 >> 2) * (L1 * kUB) + (e2 & 3);
     if (okp && okc) {
+#ifdef QMC_U_HINTS
+      const uint64_t pol = policy_evict_first();
+#pragma unroll
+      for (int f1 = 0; f1 < L1; ++f1) v[f1] = ld_hint(&ub[f1 * kUB], pol);
+#else
 #pragma unroll
       for (int f1 = 0; f1 < L1; ++f1) v[f1] = __ldg(&ub[f1 * kUB]);
+#endif
     } else {
 #pragma unroll
       for (int f1 = 0; f1 < L1; ++f1) v[f1] = make_double2(0.0, 0.0);
@@ -391,11 +453,44 @@ __global__ void __launch_bounds__(kColThreads, 2)
         v[f1] = cmulc(v[f1], tw);
       }
     }
+    // this CTA's U blocks (PG pairs × CB/kUB column blocks of L1·kUB complex,
+    // read only here) are dead: drop them from L2 without write-back
+#ifndef QMC_NO_DISCARD
+    if (CB % kUB == 0) {
+      __syncthreads();
+      const int lines = L1 * kUB * 16 / 128;  // per block (L1·kUB·16 bytes)
+      const int nb = CB / kUB;
+      for (int i = tid; i < PG * nb * lines; i += kColThreads) {
+        const int pp = i / (nb * lines), rest = i % (nb * lines);
+        const int b = rest / lines, l = rest % lines;
+        if (pg0 + pp < np && (blockIdx.x * CB) / kUB + b < L2 / kUB && (L1 * kUB * 16) % 128 == 0)
+          discard_l2(reinterpret_cast<const char*>(U + int64_t(pg0 + pp) * L +
+                                                   int64_t((blockIdx.x * CB) / kUB + b) * (L1 * kUB)) + 128 * l);
+      }
+    }
+#endif
     reg_dft<L1, +1>(v, tw1);
     double r[L1];
+    if constexpr (FAST) {
 #pragma unroll
-    for (int e1 = 0; e1 < L1; ++e1) emit<EP>(E, v[e1], nrow[e1], okp && nrow[e1] >= 0, has2, xk, acc, r[e1]);
-    if (EP == EPK_ROWSUM) rowsum_flush<L1>(r, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
+      for (int e1 = 0; e1 < L1; ++e1) emit_fast<EP>(E, v[e1], nrow[e1], xk, acc, r[e1]);
+      if constexpr (EP == EPK_ROWSUM && L1 == 16) {
+        if (PG == 16) {
+          const double sum = rowsum_butterfly16(r);
+          const int e1 = tid & 15;
+          const int64_t i = int64_t(L2) * e1 + e2;
+          rowpart[__ldg(&P[i == 0 ? 0 : m - i])] = sum;
+        } else {
+          rowsum_flush<L1>(r, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
+        }
+      } else if constexpr (EP == EPK_ROWSUM) {
+        rowsum_flush<L1>(r, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
+      }
+    } else {
+#pragma unroll
+      for (int e1 = 0; e1 < L1; ++e1) emit<EP>(E, v[e1], nrow[e1], okp && nrow[e1] >= 0, has2, xk, acc, r[e1]);
+      if (EP == EPK_ROWSUM) rowsum_flush<L1>(r, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
+    }
   } else {
     double2* T = sm;  // [(p + PG·c)·LP + r·M + k2]
     const int nA = 32 * R;  // = PG·CB·R items
@@ -472,6 +567,137 @@ __global__ void __launch_bounds__(kColThreads, 2)
       dst[1] = sacc.y;
     }
   }
+}
+
+// Persistent, software-pipelined K2 for the fast path (R = 1, PG = 16): tile =
+// (16 columns e2, 16 pairs), its U blocks (16 pairs × 4 blocks × L1·kUB
+// complex, contiguous per pair) and its output row indices staged in shared
+// memory by cp.async one tile ahead, so the DRAM/L2 reads of the next tile
+// overlap the DFTs and X stores of this one.  Same arithmetic and output as
+// k_cols_x<1, L1, EP, true>.
+#ifndef QMC_K2_STAGES
+#define QMC_K2_STAGES 3
+#endif
+constexpr int kPipeStages = QMC_K2_STAGES;
+template <int L1>
+__host__ __device__ constexpr int pipe_pair_stride() { return (kColThreads / 16 / kUB) * L1 * kUB + 1; }
+template <int L1>
+__host__ __device__ constexpr size_t cols_pipe_smem() {
+  return size_t(kPipeStages) * 16 * pipe_pair_stride<L1>() * 16 + size_t(kPipeStages) * L1 * 16 * 4;
+}
+
+template <int L1, int EP>
+__global__ void __launch_bounds__(kColThreads, 1)
+    k_cols_pipe(const double2* __restrict__ U, int64_t L, int L2, int64_t m, int ntx, int ngroups,
+                const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
+                const double2* __restrict__ tw1, const double2* __restrict__ twL, int64_t pair0, EpiArgs E,
+                double* __restrict__ part, int part_stride) {
+  constexpr int PG = 16, CB = kColThreads / PG, NB = CB / kUB, BLK = L1 * kUB;
+  constexpr int PSTR = pipe_pair_stride<L1>();  // odd (16-B units): conflict-free column reads
+  constexpr int STAGE = PG * PSTR;
+  extern __shared__ double2 sm[];
+  int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
+  __shared__ double2 red[kColThreads / 32][16];
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int p = tid % PG, c = tid / PG;
+  const int ntiles = ntx * ngroups;
+  auto issue = [&](int tile, int st) {
+    const int bx = tile % ntx, g = tile / ntx;
+    double2* dst = sm + st * STAGE;
+    for (int i = tid; i < PG * NB * BLK; i += kColThreads) {
+      const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
+      cp_async16(dst + pp * PSTR + o, U + int64_t(g * PG + pp) * L + int64_t(bx) * (NB * BLK) + o);
+    }
+    int* nd = nS + st * (L1 * CB);
+    for (int i = tid; i < L1 * CB; i += kColThreads) {
+      const int e1 = i / CB, cc = i - e1 * CB;
+      const int64_t ii = int64_t(L2) * e1 + bx * CB + cc;
+      cp_async4(nd + i, &P[ii == 0 ? 0 : m - ii]);
+    }
+  };
+#pragma unroll
+  for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
+    if (blockIdx.x + s0 * gridDim.x < ntiles) issue(blockIdx.x + s0 * gridDim.x, s0);
+    cp_async_commit();
+  }
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kPipeStages;
+    const int ahead = tile + (kPipeStages - 1) * gridDim.x;
+    if (ahead < ntiles) issue(ahead, (it + kPipeStages - 1) % kPipeStages);
+    cp_async_commit();
+    asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
+    __syncthreads();
+    const int bx = tile % ntx, g = tile / ntx;
+    const int pair = g * PG + p;
+    const int64_t k = 2 * (pair0 + pair);
+    double* xk = E.X ? E.X + k : nullptr;
+    double* rowpart = EP == EPK_ROWSUM ? E.rowpart + (pair0 / PG + g) * E.N : nullptr;
+    double2 acc = make_double2(0.0, 0.0);
+    if (bx == 0 && warp == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
+      const bool okrow = tid < PG;
+      const double phi0 = __ldg(scal);
+      const double2 v0 = make_double2(phi0 * colsum[k], phi0 * colsum[k + 1]);
+      double r0[1];
+      int n0[1] = {okrow ? 0 : -1};
+      emit<EP>(E, v0, 0, okrow, true, xk, acc, r0[0]);
+      if (EP == EPK_ROWSUM) {
+        double s0 = r0[0];
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        if (tid == 0) rowpart[0] = s0;
+      }
+      (void)n0;
+    }
+    const int e2 = bx * CB + c;
+    const double2* src = sm + st * STAGE + p * PSTR + (c / kUB) * BLK + (c % kUB);
+    double2 v[L1];
+#pragma unroll
+    for (int f1 = 0; f1 < L1; ++f1) v[f1] = src[f1 * kUB];
+    if (L1 > 1) {
+      const double2 w1 = __ldg(&twL[e2]);
+      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+      const double2 w4 = cmul(w2, w2);
+      double2 hi = w4;
+#pragma unroll
+      for (int f1 = 1; f1 < L1; ++f1) {
+        const int b = f1 & 3;
+        if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
+        const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
+        const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
+        v[f1] = cmulc(v[f1], tw);
+      }
+    }
+    reg_dft<L1, +1>(v, tw1);
+    const int* nr = nS + st * (L1 * CB) + c;
+    double r[L1];
+#pragma unroll
+    for (int e1 = 0; e1 < L1; ++e1) emit_fast<EP>(E, v[e1], nr[e1 * CB], xk, acc, r[e1]);
+    if constexpr (EP == EPK_ROWSUM) {
+      static_assert(EP != EPK_ROWSUM || L1 == 16, "row sums of the pipelined K2 need L1 = 16");
+      const double sum = rowsum_butterfly16(r);
+      rowpart[nr[(tid & 15) * CB]] = sum;
+    } else {
+      if (part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
+#pragma unroll
+        for (int o = PG; o < 32; o <<= 1) {
+          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+        }
+        if ((tid & 31) < PG) red[warp][tid & 31] = acc;
+        __syncthreads();
+        if (tid < PG) {
+          double2 sacc = red[0][tid];
+          for (int ww = 1; ww < kColThreads / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
+          double* dst = part + int64_t(bx) * part_stride + 2 * pair;
+          dst[0] = sacc.x;
+          dst[1] = sacc.y;
+        }
+      }
+    }
+    __syncthreads();  // stage st and red are reused
+  }
+  cp_async_wait_all();
 }
 
 // out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
@@ -612,7 +838,32 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
                           const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
   constexpr int L1 = R * M;
   const size_t smem = R == 1 ? 0 : size_t(32) * (L1 | 1) * sizeof(double2);
-  auto kern = k_cols_x<R, M, EP>;
+  // fast path: whole pair groups, whole pairs, vector X stores, no padded rows
+  const bool fast = R == 1 && np % cl.PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L == pl->m &&
+                    (pl->sp.L2 % ((R == 1 ? kColThreads : 32) / cl.PG)) == 0;
+  if constexpr (R == 1 && (EP != EPK_ROWSUM || L1 == 16)) {
+    if (fast && cl.PG == 16 && !getenv("QMC_K2_NOPIPE")) {
+      constexpr size_t psm = cols_pipe_smem<L1>();
+      auto pk = k_cols_pipe<L1, EP>;
+      set_smem_attr(pk, psm);
+      static int nsm = 0;
+      if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      }
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kColThreads, psm);
+      const int ntx = int(pl->sp.L2 / 16), ng = (np + 15) / 16;
+      const int64_t ntiles = int64_t(ntx) * ng;
+      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
+      pk<<<grid, kColThreads, psm, st>>>(U, pl->sp.L, int(pl->sp.L2), pl->m, ntx, ng, pl->d_P, colsum, pl->d_scal,
+                                         pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
+      QMC_LAUNCHED();
+      return QMC_OK;
+    }
+  }
+  auto kern = fast ? k_cols_x<R, M, EP, (R == 1)> : k_cols_x<R, M, EP, false>;
   set_smem_attr(kern, smem);
   dim3 g((unsigned)cl.nbx, (unsigned)((np + cl.PG - 1) / cl.PG));
   kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
@@ -679,6 +930,25 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
       return QMC_ECUDA;
     }
   }
+#ifdef QMC_L2_PERSIST
+  {  // keep the batch scratch U resident in L2 (access-policy window)
+    int dev = 0, maxwin = 0, maxpers = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev);
+    const size_t ubytes = size_t(nsets) * pairs_b * pl->sp.L * 16;
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(ubytes, size_t(maxpers)));
+    cudaStreamAttrValue av = {};
+    av.accessPolicyWindow.base_ptr = ws + cl.off_U;
+    av.accessPolicyWindow.num_bytes = std::min<size_t>(ubytes, size_t(maxwin));
+    av.accessPolicyWindow.hitRatio = 1.0f;
+    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    for (int k = 0; k < (nsets == 2 ? 2 : 1); ++k)
+      cudaStreamSetAttribute(nsets == 2 ? pl->ist[k] : st, cudaStreamAttributeAccessPolicyWindow, &av);
+    cudaGetLastError();
+  }
+#endif
   int64_t bidx = 0;
   for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs, ++bidx) {
     const int np = int(std::min<int64_t>(pl->batch_pairs, npairs_total - pair0));
@@ -698,6 +968,9 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     prof_end(KC_ROWS, bs);
     prof_begin(KC_COLS, bs);
     rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs);
+#ifdef QMC_K2_TWICE
+    if (!rc) rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs);
+#endif
     if (rc) return rc;
     prof_end(KC_COLS, bs);
     if (colmean) {

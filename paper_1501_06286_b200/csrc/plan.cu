@@ -459,12 +459,13 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->ws = (char*)plan_ws;
   pl->ws_bytes = plan_ws_bytes;
   {
-    // U of one batch (16·L bytes per pair) ~64 MB per scratch set (measured
-    // best for config 2: fewer, longer K1 launches keep more items per
-    // persistent CTA); at least two waves of K1 CTAs; a multiple of the K2
-    // pair group (16, 8 or 4 pairs)
+    // U of one batch (16·L bytes per pair) ~128 MB per scratch set (measured
+    // best for config 2: fewer, longer launches keep more items per
+    // persistent CTA; U does not stay in L2 between K1 and K2 on B200 anyway,
+    // DESIGN.md §5); at least two waves of K1 CTAs; a multiple of the K2 pair
+    // group (16, 8 or 4 pairs)
     const int64_t per_pair = 16 * sp.L;
-    int64_t bp = std::max<int64_t>(1, (int64_t(64) << 20) / per_pair);
+    int64_t bp = std::max<int64_t>(1, (int64_t(128) << 20) / per_pair);
     const int64_t want = (296 + sp.L1 - 1) / sp.L1;  // >= 2 waves of K1 CTAs
     if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(64) << 20) / per_pair));
     bp = std::min<int64_t>(bp, 256);

@@ -12,6 +12,8 @@ def main():
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--steps", type=int, default=2)
     ap.add_argument("--t", type=int, default=0, help="override t (columns)")
+    ap.add_argument("--nox", action="store_true", help="means only: X is not written")
+    ap.add_argument("--matmul", action="store_true", help="qmc_matmul instead of the config's f")
     a = ap.parse_args()
     import torch
     import paper_1501_06286_b200 as q
@@ -21,10 +23,10 @@ def main():
     A = q.to_device_colmajor(w.A, "cuda")
     X = q.x_empty(plan.N, w.t, "cuda")
     for _ in range(a.steps):
-        if w.f is None:
+        if w.f is None or a.matmul:
             plan.matmul(A, X)
         else:
-            out = plan.mean(A, w.f, w.f_param, X=X)
+            out = plan.mean(A, w.f, w.f_param, X=None if a.nox else X)
             if w.f == W.F_ROWMEAN_RELU:
                 plan.finalize(w.f, out, w.t)
     torch.cuda.synchronize()
