@@ -444,6 +444,50 @@ __device__ __forceinline__ void fftE(double2 (&v)[E], double2* S, const double2*
   fftE_rec<N, E, DIR, 1, 0, 0>(v, S, tws, tid);
 }
 
+// Forward FFT fused with the pointwise product by the spectrum row Wr
+// (natural order, Wr[tid + q·NT] for v[q]): the first E/2 spectrum values are
+// loaded while the last exchange is in flight, the rest after the last
+// butterflies; dc receives the unmultiplied v[0] (the DC term for tid 0).
+template <int N, int E, int NS, int I, int OFF>
+__device__ __forceinline__ void fftE_fwd_w_rec(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid,
+                                               const double2* __restrict__ Wr, double2& dc) {
+  if constexpr (I < RPlan<N, E>::count) {
+    constexpr int R = RPlan<N, E>::get(I);
+    constexpr bool LAST = I + 1 == RPlan<N, E>::count;
+    constexpr int NT = N / E, H = E / 2;
+    double2 wv[LAST ? H : 1];
+    if constexpr (I > 0) {
+      constexpr int RP = RPlan<N, E>::get(I - 1);
+      __syncthreads();
+      store_stage<RP, N, E, NS / RP>(v, S);
+      if constexpr (LAST) {
+#pragma unroll
+        for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wr[tid_fresh() + q * NT]);
+      }
+      __syncthreads();
+      load_strided<N, E>(v, S);
+    } else if constexpr (LAST) {
+#pragma unroll
+      for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wr[tid_fresh() + q * NT]);
+    }
+    reg_stage<R, N, E, NS, -1>(v, tws + OFF, tid);
+    if constexpr (LAST) {
+      dc = v[0];
+#pragma unroll
+      for (int q = 0; q < H; ++q) v[q] = cmul(v[q], wv[q]);
+#pragma unroll
+      for (int q = H; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid_fresh() + q * NT]));
+    }
+    fftE_fwd_w_rec<N, E, NS * R, I + 1, (I > 0 ? OFF + NS * (R - 1) : OFF)>(v, S, tws, tid, Wr, dc);
+  }
+}
+
+template <int N, int E>
+__device__ __forceinline__ void fftE_fwd_w(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid,
+                                           const double2* __restrict__ Wr, double2& dc) {
+  fftE_fwd_w_rec<N, E, 1, 0, 0>(v, S, tws, tid, Wr, dc);
+}
+
 // ----------------------------------------------------------------- register column DFT
 // Length-N DFT entirely in one thread's registers, N = R·M with R, M in
 // {1,2,3,4,5,8,16}: M-point DFTs over stride-R subsequences, twiddles

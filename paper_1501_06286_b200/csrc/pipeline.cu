@@ -206,6 +206,18 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
       const int e2 = tid_fresh() + q * NT;
       v[q] = (__ldg(&occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
     }
+    const double2* Wr = W + int64_t(f1) * L2;
+#ifndef QMC_NO_WPREFETCH
+    double2 dc;
+    fftE_fwd_w<L2, E>(v, S, tws, tid, Wr, dc);
+    QMC_TS(2);
+    if (f1 == 0 && tid == 0) {
+      const int64_t k1 = 2 * (pair0 + p);
+      colsum[k1] = dc.x;
+      if (k1 + 1 < t) colsum[k1 + 1] = dc.y;
+    }
+    QMC_TS(3);
+#else
     fftE<L2, E, -1>(v, S, tws, tid);
     QMC_TS(2);
     if (f1 == 0 && tid == 0) {
@@ -213,10 +225,10 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
       colsum[k1] = v[0].x;
       if (k1 + 1 < t) colsum[k1 + 1] = v[0].y;
     }
-    const double2* Wr = W + int64_t(f1) * L2;
 #pragma unroll
     for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid + q * NT]));
     QMC_TS(3);
+#endif
     fftE<L2, E, +1>(v, S, tws, tid);
     QMC_TS(4);
     // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
@@ -576,40 +588,43 @@ __global__ void __launch_bounds__(kColThreads, 2)
 // overlap the DFTs and X stores of this one.  Same arithmetic and output as
 // k_cols_x<1, L1, EP, true>.
 #ifndef QMC_K2_STAGES
-#define QMC_K2_STAGES 3
+#define QMC_K2_STAGES 2
 #endif
 constexpr int kPipeStages = QMC_K2_STAGES;
-template <int L1>
-__host__ __device__ constexpr int pipe_pair_stride() { return (kColThreads / 16 / kUB) * L1 * kUB + 1; }
-template <int L1>
+#ifndef QMC_K2_CB
+#define QMC_K2_CB 8
+#endif
+template <int L1, int CB>
+__host__ __device__ constexpr int pipe_pair_stride() { return (CB / kUB) * L1 * kUB + 1; }
+template <int L1, int CB>
 __host__ __device__ constexpr size_t cols_pipe_smem() {
-  return size_t(kPipeStages) * 16 * pipe_pair_stride<L1>() * 16 + size_t(kPipeStages) * L1 * 16 * 4;
+  return size_t(kPipeStages) * 16 * pipe_pair_stride<L1, CB>() * 16 + size_t(kPipeStages) * L1 * CB * 4;
 }
 
-template <int L1, int EP>
-__global__ void __launch_bounds__(kColThreads, 1)
+template <int L1, int EP, int CB>
+__global__ void __launch_bounds__(16 * CB, 1)
     k_cols_pipe(const double2* __restrict__ U, int64_t L, int L2, int64_t m, int ntx, int ngroups,
                 const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
                 const double2* __restrict__ tw1, const double2* __restrict__ twL, int64_t pair0, EpiArgs E,
                 double* __restrict__ part, int part_stride) {
-  constexpr int PG = 16, CB = kColThreads / PG, NB = CB / kUB, BLK = L1 * kUB;
-  constexpr int PSTR = pipe_pair_stride<L1>();  // odd (16-B units): conflict-free column reads
+  constexpr int PG = 16, NT = PG * CB, NB = CB / kUB, BLK = L1 * kUB;
+  constexpr int PSTR = pipe_pair_stride<L1, CB>();  // odd (16-B units): conflict-free column reads
   constexpr int STAGE = PG * PSTR;
   extern __shared__ double2 sm[];
   int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
-  __shared__ double2 red[kColThreads / 32][16];
+  __shared__ double2 red[NT / 32][16];
   const int tid = threadIdx.x, warp = tid >> 5;
   const int p = tid % PG, c = tid / PG;
   const int ntiles = ntx * ngroups;
   auto issue = [&](int tile, int st) {
     const int bx = tile % ntx, g = tile / ntx;
     double2* dst = sm + st * STAGE;
-    for (int i = tid; i < PG * NB * BLK; i += kColThreads) {
+    for (int i = tid; i < PG * NB * BLK; i += NT) {
       const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
       cp_async16(dst + pp * PSTR + o, U + int64_t(g * PG + pp) * L + int64_t(bx) * (NB * BLK) + o);
     }
     int* nd = nS + st * (L1 * CB);
-    for (int i = tid; i < L1 * CB; i += kColThreads) {
+    for (int i = tid; i < L1 * CB; i += NT) {
       const int e1 = i / CB, cc = i - e1 * CB;
       const int64_t ii = int64_t(L2) * e1 + bx * CB + cc;
       cp_async4(nd + i, &P[ii == 0 ? 0 : m - ii]);
@@ -688,7 +703,7 @@ __global__ void __launch_bounds__(kColThreads, 1)
         __syncthreads();
         if (tid < PG) {
           double2 sacc = red[0][tid];
-          for (int ww = 1; ww < kColThreads / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
+          for (int ww = 1; ww < NT / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
           double* dst = part + int64_t(bx) * part_stride + 2 * pair;
           dst[0] = sacc.x;
           dst[1] = sacc.y;
@@ -843,8 +858,9 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
                     (pl->sp.L2 % ((R == 1 ? kColThreads : 32) / cl.PG)) == 0;
   if constexpr (R == 1 && (EP != EPK_ROWSUM || L1 == 16)) {
     if (fast && cl.PG == 16 && !getenv("QMC_K2_NOPIPE")) {
-      constexpr size_t psm = cols_pipe_smem<L1>();
-      auto pk = k_cols_pipe<L1, EP>;
+      constexpr int CBP = QMC_K2_CB;
+      constexpr size_t psm = cols_pipe_smem<L1, CBP>();
+      auto pk = k_cols_pipe<L1, EP, CBP>;
       set_smem_attr(pk, psm);
       static int nsm = 0;
       if (!nsm) {
@@ -853,11 +869,12 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
       }
       int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kColThreads, psm);
-      const int ntx = int(pl->sp.L2 / 16), ng = (np + 15) / 16;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, 16 * CBP, psm);
+      if (pl->k2_per_sm > 0) per_sm = std::min(per_sm, pl->k2_per_sm);
+      const int ntx = int(pl->sp.L2 / CBP), ng = (np + 15) / 16;
       const int64_t ntiles = int64_t(ntx) * ng;
       const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
-      pk<<<grid, kColThreads, psm, st>>>(U, pl->sp.L, int(pl->sp.L2), pl->m, ntx, ng, pl->d_P, colsum, pl->d_scal,
+      pk<<<grid, 16 * CBP, psm, st>>>(U, pl->sp.L, int(pl->sp.L2), pl->m, ntx, ng, pl->d_P, colsum, pl->d_scal,
                                          pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
       QMC_LAUNCHED();
       return QMC_OK;

@@ -472,6 +472,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
     pl->batch_pairs = bp;
     if (const char* ev = getenv("QMC_K1_PER_SM")) pl->k1_per_sm = int(strtol(ev, nullptr, 10));  // tuning
+    if (const char* ev = getenv("QMC_K2_PER_SM")) pl->k2_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
       if (v > 0) pl->batch_pairs = v;

@@ -85,6 +85,7 @@ struct qmc_plan {
   qmc::Split sp;
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
+  int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
   // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3
