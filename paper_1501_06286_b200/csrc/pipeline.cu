@@ -779,7 +779,9 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   c.nsets = (pl->nstreams == 2 && nbatch > 1) ? 2 : 1;
   c.PG = pair_group(pairs);
   c.ngroups = int((pairs + c.PG - 1) / c.PG);
-  const int CB = cols_cb(pl, c.PG);
+  // column-partial slots: the larger of the two K2 tilings (k_cols_x: CB
+  // columns per CTA; k_cols_pipe: QMC_K2_CB columns per tile)
+  const int CB = std::min(cols_cb(pl, c.PG), int(QMC_K2_CB));
   c.nbx = int((pl->sp.L2 + CB - 1) / CB);
   c.part_stride = int(2 * c.ngroups * c.PG);
   c.off_U = take(size_t(c.nsets) * pairs * pl->sp.L * 16);
@@ -850,7 +852,7 @@ static int ilog2(int64_t x) {
 
 template <int R, int M, int EP>
 static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0,
-                          const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+                          const EpiArgs& E, double* part, double* colsum, cudaStream_t st, int* nbx_used) {
   constexpr int L1 = R * M;
   const size_t smem = R == 1 ? 0 : size_t(32) * (L1 | 1) * sizeof(double2);
   // fast path: whole pair groups, whole pairs, vector X stores, no padded rows
@@ -877,12 +879,15 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       pk<<<grid, 16 * CBP, psm, st>>>(U, pl->sp.L, int(pl->sp.L2), pl->m, ntx, ng, pl->d_P, colsum, pl->d_scal,
                                          pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
       QMC_LAUNCHED();
+      *nbx_used = ntx;
       return QMC_OK;
     }
   }
   auto kern = fast ? k_cols_x<R, M, EP, (R == 1)> : k_cols_x<R, M, EP, false>;
   set_smem_attr(kern, smem);
-  dim3 g((unsigned)cl.nbx, (unsigned)((np + cl.PG - 1) / cl.PG));
+  const int CBx = cols_cb(pl, cl.PG);
+  dim3 g((unsigned)((pl->sp.L2 + CBx - 1) / CBx), (unsigned)((np + cl.PG - 1) / cl.PG));
+  *nbx_used = int(g.x);
   kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
                                      colsum, pl->d_scal, pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
   QMC_LAUNCHED();
@@ -891,19 +896,20 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
 
 template <int R, int M>
 static int launch_cols(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0, int ep,
-                       const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+                       const EpiArgs& E, double* part, double* colsum, cudaStream_t st, int* nbx_used) {
   switch (ep) {
-    case EPK_EXP: return launch_cols_ep<R, M, EPK_EXP>(pl, cl, U, np, pair0, E, part, colsum, st);
-    case EPK_ROWSUM: return launch_cols_ep<R, M, EPK_ROWSUM>(pl, cl, U, np, pair0, E, part, colsum, st);
-    default: return launch_cols_ep<R, M, EPK_LIN>(pl, cl, U, np, pair0, E, part, colsum, st);
+    case EPK_EXP: return launch_cols_ep<R, M, EPK_EXP>(pl, cl, U, np, pair0, E, part, colsum, st, nbx_used);
+    case EPK_ROWSUM: return launch_cols_ep<R, M, EPK_ROWSUM>(pl, cl, U, np, pair0, E, part, colsum, st, nbx_used);
+    default: return launch_cols_ep<R, M, EPK_LIN>(pl, cl, U, np, pair0, E, part, colsum, st, nbx_used);
   }
 }
 
+// launches K2 for the batch; *nbx_used = column-partial slots it wrote
 static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2* U, int np, int64_t pair0, int ep,
-                         const EpiArgs& E, double* part, double* colsum, cudaStream_t st) {
+                         const EpiArgs& E, double* part, double* colsum, cudaStream_t st, int* nbx_used) {
   const int R = k2_split_R(pl->sp.L1), M = int(pl->sp.L1) / std::max(R, 1);
 #define QMC_COLS_CASE(RR, MM) \
-  if (R == RR && M == MM) return launch_cols<RR, MM>(pl, cl, U, np, pair0, ep, E, part, colsum, st);
+  if (R == RR && M == MM) return launch_cols<RR, MM>(pl, cl, U, np, pair0, ep, E, part, colsum, st, nbx_used);
   QMC_K2_SPLITS(QMC_COLS_CASE)
 #undef QMC_COLS_CASE
   return QMC_EINVAL_N;
@@ -984,15 +990,14 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     if (rc) return rc;
     prof_end(KC_ROWS, bs);
     prof_begin(KC_COLS, bs);
-    rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs);
-#ifdef QMC_K2_TWICE
-    if (!rc) rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs);
-#endif
+    int nbx_used = cl.nbx;
+    rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs, &nbx_used);
+
     if (rc) return rc;
     prof_end(KC_COLS, bs);
     if (colmean) {
       prof_begin(KC_REDUCE, bs);
-      k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, cl.nbx, cl.part_stride, 2 * np, 2 * pair0, t,
+      k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, nbx_used, cl.part_stride, 2 * np, 2 * pair0, t,
                                                          pl->N, out);
       QMC_LAUNCHED();
       prof_end(KC_REDUCE, bs);
