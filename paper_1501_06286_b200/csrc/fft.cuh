@@ -61,27 +61,6 @@ __device__ __forceinline__ void stcs(double* p, double v) { asm volatile("st.glo
 __device__ __forceinline__ void stcs2(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
-// L2 eviction-priority policies (createpolicy) and hinted accesses: the
-// batch scratch U is written by K1 with evict_last and read by K2 with
-// evict_first, so streamed data (X, A) cannot push it out of L2 in between
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void st_hint(double2* p, double2 v, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
-}
-__device__ __forceinline__ double2 ld_hint(const double2* p, uint64_t pol) {
-  double2 r;
-  asm("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(r.x), "=d"(r.y) : "l"(p), "l"(pol));
-  return r;
-}
 // Drop a dead 128-byte line from L2 without writing it back (scratch data
 // that is never read again); p must be 128-byte aligned.
 __device__ __forceinline__ void discard_l2(const void* p) {

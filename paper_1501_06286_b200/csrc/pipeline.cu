@@ -132,122 +132,132 @@ __host__ __device__ constexpr size_t rows_smem(int CH) {
   return size_t(PadE<L2, QMC_ROW_E>::size) * 16 + size_t(CH) * (16 + 16 + 4);
 }
 
+struct K1Args {
+  const double2* __restrict__ asort;   // [np][s] a in bucket order (K0)
+  const int32_t* __restrict__ e2q;     // [s]
+  const uint32_t* __restrict__ occ;    // nonempty buckets
+  int64_t s;
+  int CH;                              // staging entries per chunk
+  const double2* __restrict__ twj;     // [L1][s]
+  const double2* __restrict__ tws;     // row-FFT stage twiddles
+  const double2* __restrict__ W;       // [L1][L2] spectrum
+  double2* __restrict__ U;             // [np][L] blocked
+  int64_t L;
+  int L1, np;
+  int64_t pair0, t;
+  double* __restrict__ colsum;
+};
+
 template <int L2>
-__global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_ROWS_MINB512 : QMC_ROWS_MINB))
-    k_rows16(const double2* __restrict__ asort, const int32_t* __restrict__ e2q, const uint32_t* __restrict__ occ,
-             int64_t s, int CH,
-             const double2* __restrict__ twj, const double2* __restrict__ tws, const double2* __restrict__ W,
-             double2* __restrict__ U, int64_t L, int L1, int np, int64_t pair0, int64_t t,
-             double* __restrict__ colsum) {
-  extern __shared__ double2 smem[];
+struct K1Smem {
+  double2* S;    // padded row
+  double2* stA;  // staging: a
+  double2* stW;  // staging: twiddles
+  int32_t* stE;  // staging: e2q
+  __device__ K1Smem(double2* base, int CH)
+      : S(base), stA(base + PadE<L2, QMC_ROW_E>::size), stW(stA + CH), stE(reinterpret_cast<int32_t*>(stW + CH)) {}
+};
+
+// stage chunk c of item it (all threads issue, one commit group)
+template <int L2>
+__device__ __forceinline__ void k1_issue(const K1Args& a, const K1Smem<L2>& sm, int it, int c) {
+  constexpr int NT = L2 / QMC_ROW_E;
+  const int f1 = it % a.L1, p = it / a.L1;
+  const int64_t q0 = int64_t(c) * a.CH;
+  const int n = int(a.CH < a.s - q0 ? a.CH : a.s - q0);
+  const double2* ga = a.asort + int64_t(p) * a.s + q0;
+  const double2* gw = a.twj + int64_t(f1) * a.s + q0;
+  for (int i = threadIdx.x; i < n; i += NT) {
+    cp_async16(sm.stA + i, ga + i);
+    cp_async16(sm.stW + i, gw + i);
+    cp_async4(sm.stE + i, a.e2q + q0 + i);
+  }
+  cp_async_commit();
+}
+
+// One K1 item (f1, pair); its chunk 0 must have been issued.  next >= 0: the
+// item whose chunk 0 is issued once this item's staging is consumed (it then
+// overlaps this item's FFTs).
+template <int L2>
+__device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, int item, int next) {
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
-  double2* S = smem;
-  double2* stA = smem + PadE<L2, E>::size;
-  double2* stW = stA + CH;
-  int32_t* stE = reinterpret_cast<int32_t*>(stW + CH);
+  double2* S = sm.S;
   const int tid = threadIdx.x;
-  const int nitems = L1 * np;
-  const int nch = int((s + CH - 1) / CH);
-  // stage chunk c of item it (all threads issue, one commit group)
-  auto issue = [&](int it, int c) {
-    const int f1 = it % L1, p = it / L1;
-    const int64_t q0 = int64_t(c) * CH;
-    const int n = int((CH < s - q0 ? CH : s - q0));
-    const double2* ga = asort + int64_t(p) * s + q0;
-    const double2* gw = twj + int64_t(f1) * s + q0;
+  const int L1 = a.L1;
+  const int f1 = item % L1, p = item / L1;
+  const int nch = int((a.s + a.CH - 1) / a.CH);
+  QMC_TS(0);
+  for (int c = 0; c < nch; ++c) {
+    cp_async_wait_all();
+    __syncthreads();  // staging complete; every use of S by the previous item is done
+    // scatter a' = P a fused with the first DFT dimension:
+    //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
+    // The first entry of a bucket (size in e2q >> 13) sums it in j order and
+    // stores T (S holds the previous item's data elsewhere: only nonempty
+    // buckets are read back, by the occupancy mask); a bucket continued from
+    // the previous chunk is added to by this chunk's entry 0.
+    const int n = int(a.CH < a.s - int64_t(c) * a.CH ? a.CH : a.s - int64_t(c) * a.CH);
     for (int i = tid; i < n; i += NT) {
-      cp_async16(stA + i, ga + i);
-      cp_async16(stW + i, gw + i);
-      cp_async4(stE + i, e2q + q0 + i);
-    }
-    cp_async_commit();
-  };
-  int item = blockIdx.x;
-  if (item < nitems) issue(item, 0);
-  for (; item < nitems; item += gridDim.x) {
-    const int f1 = item % L1, p = item / L1;
-    QMC_TS(0);
-    for (int c = 0; c < nch; ++c) {
-      cp_async_wait_all();
-      __syncthreads();  // staging complete; every use of S by the previous item is done
-      // scatter a' = P a fused with the first DFT dimension:
-      //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
-      // The first entry of a bucket (size in e2q >> 13) sums it in j order and
-      // stores T (S holds the previous item's data elsewhere: only nonempty
-      // buckets are read back, by the occupancy mask); a bucket continued from
-      // the previous chunk is added to by this chunk's entry 0.
-      const int n = int(CH < s - int64_t(c) * CH ? CH : s - int64_t(c) * CH);
-      for (int i = tid; i < n; i += NT) {
-        const int pk = stE[i];
-        const int len = pk >> 13, e2 = pk & 8191;
-        if (len > 0) {
-          double2 acc = cmul(stA[i], stW[i]);
-          const int end = min(n, i + len);
-          for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(stA[k], stW[k]));
-          S[padE<E>(e2)] = acc;
-        } else if (i == 0) {  // continuation of a bucket from the previous chunk
-          double2 acc = cmul(stA[0], stW[0]);
-          for (int k = 1; k < n && stE[k] == pk; ++k) acc = cadd(acc, cmul(stA[k], stW[k]));
-          S[padE<E>(e2)] = cadd(S[padE<E>(e2)], acc);
-        }
-      }
-      __syncthreads();  // staging consumed
-      if (c + 1 < nch) {
-        issue(item, c + 1);
-      } else if (item + gridDim.x < nitems) {
-        issue(item + gridDim.x, 0);  // overlaps this item's FFTs
+      const int pk = sm.stE[i];
+      const int len = pk >> 13, e2 = pk & 8191;
+      if (len > 0) {
+        double2 acc = cmul(sm.stA[i], sm.stW[i]);
+        const int end = min(n, i + len);
+        for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
+        S[padE<E>(e2)] = acc;
+      } else if (i == 0) {  // continuation of a bucket from the previous chunk
+        double2 acc = cmul(sm.stA[0], sm.stW[0]);
+        for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
+        S[padE<E>(e2)] = cadd(S[padE<E>(e2)], acc);
       }
     }
-    QMC_TS(1);
-    double2 v[E];
-#pragma unroll
-    for (int q = 0; q < E; ++q) {  // nonempty buckets only (the rest of S is stale)
-      const int e2 = tid_fresh() + q * NT;
-      v[q] = (__ldg(&occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
+    __syncthreads();  // staging consumed
+    if (c + 1 < nch) {
+      k1_issue<L2>(a, sm, item, c + 1);
+    } else if (next >= 0) {
+      k1_issue<L2>(a, sm, next, 0);  // overlaps this item's FFTs
     }
-    const double2* Wr = W + int64_t(f1) * L2;
-#ifndef QMC_NO_WPREFETCH
-    double2 dc;
-    fftE_fwd_w<L2, E>(v, S, tws, tid, Wr, dc);
-    QMC_TS(2);
-    if (f1 == 0 && tid == 0) {
-      const int64_t k1 = 2 * (pair0 + p);
-      colsum[k1] = dc.x;
-      if (k1 + 1 < t) colsum[k1 + 1] = dc.y;
-    }
-    QMC_TS(3);
-#else
-    fftE<L2, E, -1>(v, S, tws, tid);
-    QMC_TS(2);
-    if (f1 == 0 && tid == 0) {
-      const int64_t k1 = 2 * (pair0 + p);
-      colsum[k1] = v[0].x;
-      if (k1 + 1 < t) colsum[k1 + 1] = v[0].y;
-    }
-#pragma unroll
-    for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid + q * NT]));
-    QMC_TS(3);
-#endif
-    fftE<L2, E, +1>(v, S, tws, tid);
-    QMC_TS(4);
-    // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
-    // whole sectors of kUB·16 bytes per f1
-    double2* Up = U + int64_t(p) * L + int64_t(f1) * kUB;
-#ifdef QMC_U_HINTS
-    const uint64_t pol = policy_evict_last();
-#endif
-#pragma unroll
-    for (int q = 0; q < E; ++q) {
-      const int e2 = tid + q * NT;
-#ifdef QMC_U_HINTS
-      st_hint(&Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)], v[q], pol);
-#else
-      Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
-#endif
-    }
-    QMC_TS(5);
   }
+  QMC_TS(1);
+  double2 v[E];
+#pragma unroll
+  for (int q = 0; q < E; ++q) {  // nonempty buckets only (the rest of S is stale)
+    const int e2 = tid_fresh() + q * NT;
+    v[q] = (__ldg(&a.occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
+  }
+  const double2* Wr = a.W + int64_t(f1) * L2;
+  double2 dc;
+  fftE_fwd_w<L2, E>(v, S, a.tws, tid, Wr, dc);
+  QMC_TS(2);
+  if (f1 == 0 && tid == 0) {
+    const int64_t k1 = 2 * (a.pair0 + p);
+    a.colsum[k1] = dc.x;
+    if (k1 + 1 < a.t) a.colsum[k1 + 1] = dc.y;
+  }
+  QMC_TS(3);
+  fftE<L2, E, +1>(v, S, a.tws, tid);
+  QMC_TS(4);
+  // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
+  // whole sectors of kUB·16 bytes per f1
+  double2* Up = a.U + int64_t(p) * a.L + int64_t(f1) * kUB;
+#pragma unroll
+  for (int q = 0; q < E; ++q) {
+    const int e2 = tid + q * NT;
+    Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+  }
+  QMC_TS(5);
+}
+
+template <int L2>
+__global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_ROWS_MINB512 : QMC_ROWS_MINB))
+    k_rows16(K1Args a) {
+  extern __shared__ double2 smem[];
+  const K1Smem<L2> sm(smem, a.CH);
+  const int nitems = a.L1 * a.np;
+  if (int(blockIdx.x) < nitems) k1_issue<L2>(a, sm, blockIdx.x, 0);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x)
+    k1_item<L2>(a, sm, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1);
   cp_async_wait_all();
 }
 
@@ -437,14 +447,8 @@ __global__ void __launch_bounds__(kColThreads, 2)
     double2 v[L1];
     const double2* ub = Up + int64_t(e2 >> 2) * (L1 * kUB) + (e2 & 3);
     if (okp && okc) {
-#ifdef QMC_U_HINTS
-      const uint64_t pol = policy_evict_first();
-#pragma unroll
-      for (int f1 = 0; f1 < L1; ++f1) v[f1] = ld_hint(&ub[f1 * kUB], pol);
-#else
 #pragma unroll
       for (int f1 = 0; f1 < L1; ++f1) v[f1] = __ldg(&ub[f1 * kUB]);
-#endif
     } else {
 #pragma unroll
       for (int f1 = 0; f1 < L1; ++f1) v[f1] = make_double2(0.0, 0.0);
@@ -467,7 +471,6 @@ __global__ void __launch_bounds__(kColThreads, 2)
     }
     // this CTA's U blocks (PG pairs × CB/kUB column blocks of L1·kUB complex,
     // read only here) are dead: drop them from L2 without write-back
-#ifndef QMC_NO_DISCARD
     if (CB % kUB == 0) {
       __syncthreads();
       const int lines = L1 * kUB * 16 / 128;  // per block (L1·kUB·16 bytes)
@@ -480,7 +483,6 @@ __global__ void __launch_bounds__(kColThreads, 2)
                                                    int64_t((blockIdx.x * CB) / kUB + b) * (L1 * kUB)) + 128 * l);
       }
     }
-#endif
     reg_dft<L1, +1>(v, tw1);
     double r[L1];
     if constexpr (FAST) {
@@ -601,115 +603,143 @@ __host__ __device__ constexpr size_t cols_pipe_smem() {
   return size_t(kPipeStages) * 16 * pipe_pair_stride<L1, CB>() * 16 + size_t(kPipeStages) * L1 * CB * 4;
 }
 
-template <int L1, int EP, int CB>
-__global__ void __launch_bounds__(16 * CB, 1)
-    k_cols_pipe(const double2* __restrict__ U, int64_t L, int L2, int64_t m, int ntx, int ngroups,
-                const int32_t* __restrict__ P, const double* __restrict__ colsum, const double* __restrict__ scal,
-                const double2* __restrict__ tw1, const double2* __restrict__ twL, int64_t pair0, EpiArgs E,
-                double* __restrict__ part, int part_stride) {
+struct K2Args {
+  const double2* __restrict__ U;
+  int64_t L;
+  int L2;
+  int64_t m;
+  int ntx, ngroups;                    // tiles: ntx column groups × ngroups pair groups
+  const int32_t* __restrict__ P;
+  const double* __restrict__ colsum;
+  const double* __restrict__ scal;
+  const double2* __restrict__ tw1;
+  const double2* __restrict__ twL;
+  int64_t pair0;
+  EpiArgs E;
+  double* __restrict__ part;
+  int part_stride;
+};
+
+// stage tile (16 pairs × CB columns): U blocks into dst (pair pitch PSTR),
+// output row indices into nd[e1][c]; all 16·CB threads issue (no commit)
+template <int L1, int CB>
+__device__ __forceinline__ void k2_issue(const K2Args& a, int tile, double2* dst, int* nd) {
   constexpr int PG = 16, NT = PG * CB, NB = CB / kUB, BLK = L1 * kUB;
+  constexpr int PSTR = pipe_pair_stride<L1, CB>();
+  const int bx = tile % a.ntx, g = tile / a.ntx;
+  for (int i = threadIdx.x; i < PG * NB * BLK; i += NT) {
+    const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
+    cp_async16(dst + pp * PSTR + o, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * (NB * BLK) + o);
+  }
+  for (int i = threadIdx.x; i < L1 * CB; i += NT) {
+    const int e1 = i / CB, cc = i - e1 * CB;
+    const int64_t ii = int64_t(a.L2) * e1 + bx * CB + cc;
+    cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
+  }
+}
+
+// column pass + epilogue of one staged tile (16·CB threads, one column each)
+template <int L1, int EP, int CB>
+__device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2* tileS, const int* nS,
+                                        double2 (*red)[16]) {
+  constexpr int PG = 16, NT = PG * CB, BLK = L1 * kUB;
   constexpr int PSTR = pipe_pair_stride<L1, CB>();  // odd (16-B units): conflict-free column reads
-  constexpr int STAGE = PG * PSTR;
+  const EpiArgs& E = a.E;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int p = tid % PG, c = tid / PG;
+  const int bx = tile % a.ntx, g = tile / a.ntx;
+  const int pair = g * PG + p;
+  const int64_t k = 2 * (a.pair0 + pair);
+  double* xk = E.X ? E.X + k : nullptr;
+  double* rowpart = EP == EPK_ROWSUM ? E.rowpart + (a.pair0 / PG + g) * E.N : nullptr;
+  double2 acc = make_double2(0.0, 0.0);
+  if (bx == 0 && warp == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
+    const bool okrow = tid < PG;
+    const double phi0 = __ldg(a.scal);
+    const double2 v0 = make_double2(phi0 * a.colsum[k], phi0 * a.colsum[k + 1]);
+    double r0 = 0.0;
+    emit<EP>(E, v0, 0, okrow, true, xk, acc, r0);
+    if (EP == EPK_ROWSUM) {
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) r0 += __shfl_xor_sync(0xffffffffu, r0, o);
+      if (tid == 0) rowpart[0] = r0;
+    }
+  }
+  const int e2 = bx * CB + c;
+  const double2* src = tileS + p * PSTR + (c / kUB) * BLK + (c % kUB);
+  double2 v[L1];
+#pragma unroll
+  for (int f1 = 0; f1 < L1; ++f1) v[f1] = src[f1 * kUB];
+  if (L1 > 1) {
+    // conj(ω_L^{e2 f1}) = conj(w^f1), w = ω_L^{e2}, as w^{4a}·w^b (f1 = 4a + b)
+    const double2 w1 = __ldg(&a.twL[e2]);
+    const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+    const double2 w4 = cmul(w2, w2);
+    double2 hi = w4;
+#pragma unroll
+    for (int f1 = 1; f1 < L1; ++f1) {
+      const int b = f1 & 3;
+      if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
+      const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
+      const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
+      v[f1] = cmulc(v[f1], tw);
+    }
+  }
+  reg_dft<L1, +1>(v, a.tw1);
+  const int* nr = nS + c;
+  double r[L1];
+#pragma unroll
+  for (int e1 = 0; e1 < L1; ++e1) emit_fast<EP>(E, v[e1], nr[e1 * CB], xk, acc, r[e1]);
+  if constexpr (EP == EPK_ROWSUM) {
+    static_assert(EP != EPK_ROWSUM || L1 == 16, "row sums of the pipelined K2 need L1 = 16");
+    const double sum = rowsum_butterfly16(r);
+    rowpart[nr[(tid & 15) * CB]] = sum;
+  } else {
+    if (a.part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
+#pragma unroll
+      for (int o = PG; o < 32; o <<= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if ((tid & 31) < PG) red[warp][tid & 31] = acc;
+      __syncthreads();
+      if (tid < PG) {
+        double2 sacc = red[0][tid];
+        for (int ww = 1; ww < NT / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
+        double* dst = a.part + int64_t(bx) * a.part_stride + 2 * pair;
+        dst[0] = sacc.x;
+        dst[1] = sacc.y;
+      }
+    }
+  }
+}
+
+template <int L1, int EP, int CB>
+__global__ void __launch_bounds__(16 * CB, 1) k_cols_pipe(K2Args a) {
+  constexpr int NT = 16 * CB;
+  constexpr int STAGE = 16 * pipe_pair_stride<L1, CB>();
   extern __shared__ double2 sm[];
   int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
   __shared__ double2 red[NT / 32][16];
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int p = tid % PG, c = tid / PG;
-  const int ntiles = ntx * ngroups;
-  auto issue = [&](int tile, int st) {
-    const int bx = tile % ntx, g = tile / ntx;
-    double2* dst = sm + st * STAGE;
-    for (int i = tid; i < PG * NB * BLK; i += NT) {
-      const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
-      cp_async16(dst + pp * PSTR + o, U + int64_t(g * PG + pp) * L + int64_t(bx) * (NB * BLK) + o);
-    }
-    int* nd = nS + st * (L1 * CB);
-    for (int i = tid; i < L1 * CB; i += NT) {
-      const int e1 = i / CB, cc = i - e1 * CB;
-      const int64_t ii = int64_t(L2) * e1 + bx * CB + cc;
-      cp_async4(nd + i, &P[ii == 0 ? 0 : m - ii]);
-    }
-  };
+  const int ntiles = a.ntx * a.ngroups;
 #pragma unroll
   for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
-    if (blockIdx.x + s0 * gridDim.x < ntiles) issue(blockIdx.x + s0 * gridDim.x, s0);
+    const int tl = blockIdx.x + s0 * gridDim.x;
+    if (tl < ntiles) k2_issue<L1, CB>(a, tl, sm + s0 * STAGE, nS + s0 * (L1 * CB));
     cp_async_commit();
   }
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % kPipeStages;
     const int ahead = tile + (kPipeStages - 1) * gridDim.x;
-    if (ahead < ntiles) issue(ahead, (it + kPipeStages - 1) % kPipeStages);
+    if (ahead < ntiles) {
+      const int sa = (it + kPipeStages - 1) % kPipeStages;
+      k2_issue<L1, CB>(a, ahead, sm + sa * STAGE, nS + sa * (L1 * CB));
+    }
     cp_async_commit();
     asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
     __syncthreads();
-    const int bx = tile % ntx, g = tile / ntx;
-    const int pair = g * PG + p;
-    const int64_t k = 2 * (pair0 + pair);
-    double* xk = E.X ? E.X + k : nullptr;
-    double* rowpart = EP == EPK_ROWSUM ? E.rowpart + (pair0 / PG + g) * E.N : nullptr;
-    double2 acc = make_double2(0.0, 0.0);
-    if (bx == 0 && warp == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
-      const bool okrow = tid < PG;
-      const double phi0 = __ldg(scal);
-      const double2 v0 = make_double2(phi0 * colsum[k], phi0 * colsum[k + 1]);
-      double r0[1];
-      int n0[1] = {okrow ? 0 : -1};
-      emit<EP>(E, v0, 0, okrow, true, xk, acc, r0[0]);
-      if (EP == EPK_ROWSUM) {
-        double s0 = r0[0];
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-        if (tid == 0) rowpart[0] = s0;
-      }
-      (void)n0;
-    }
-    const int e2 = bx * CB + c;
-    const double2* src = sm + st * STAGE + p * PSTR + (c / kUB) * BLK + (c % kUB);
-    double2 v[L1];
-#pragma unroll
-    for (int f1 = 0; f1 < L1; ++f1) v[f1] = src[f1 * kUB];
-    if (L1 > 1) {
-      const double2 w1 = __ldg(&twL[e2]);
-      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
-      const double2 w4 = cmul(w2, w2);
-      double2 hi = w4;
-#pragma unroll
-      for (int f1 = 1; f1 < L1; ++f1) {
-        const int b = f1 & 3;
-        if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
-        const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
-        const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
-        v[f1] = cmulc(v[f1], tw);
-      }
-    }
-    reg_dft<L1, +1>(v, tw1);
-    const int* nr = nS + st * (L1 * CB) + c;
-    double r[L1];
-#pragma unroll
-    for (int e1 = 0; e1 < L1; ++e1) emit_fast<EP>(E, v[e1], nr[e1 * CB], xk, acc, r[e1]);
-    if constexpr (EP == EPK_ROWSUM) {
-      static_assert(EP != EPK_ROWSUM || L1 == 16, "row sums of the pipelined K2 need L1 = 16");
-      const double sum = rowsum_butterfly16(r);
-      rowpart[nr[(tid & 15) * CB]] = sum;
-    } else {
-      if (part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
-#pragma unroll
-        for (int o = PG; o < 32; o <<= 1) {
-          acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-          acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-        }
-        if ((tid & 31) < PG) red[warp][tid & 31] = acc;
-        __syncthreads();
-        if (tid < PG) {
-          double2 sacc = red[0][tid];
-          for (int ww = 1; ww < NT / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
-          double* dst = part + int64_t(bx) * part_stride + 2 * pair;
-          dst[0] = sacc.x;
-          dst[1] = sacc.y;
-        }
-      }
-    }
+    k2_tile<L1, EP, CB>(a, tile, sm + st * STAGE, nS + st * (L1 * CB), red);
     __syncthreads();  // stage st and red are reused
   }
   cp_async_wait_all();
@@ -808,6 +838,27 @@ static int rows_chunk(int64_t L2, int64_t s) {
   return int(std::min<int64_t>(cap, (s + 31) / 32 * 32));
 }
 
+static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
+                      double* colsum) {
+  K1Args a;
+  a.asort = asort;
+  a.e2q = pl->d_e2q;
+  a.occ = pl->d_occ;
+  a.s = pl->s;
+  a.CH = rows_chunk(pl->sp.L2, pl->s);
+  a.twj = pl->d_twj;
+  a.tws = pl->d_tws;
+  a.W = pl->d_W;
+  a.U = U;
+  a.L = pl->sp.L;
+  a.L1 = int(pl->sp.L1);
+  a.np = np;
+  a.pair0 = pair0;
+  a.t = t;
+  a.colsum = colsum;
+  return a;
+}
+
 template <int L2>
 static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                        double* colsum, cudaStream_t st) {
@@ -826,8 +877,7 @@ static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int6
   if (pl->k1_per_sm > 0) per_sm = std::min(per_sm, pl->k1_per_sm);
   const int64_t items = pl->sp.L1 * int64_t(np);
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, int64_t(nsm) * std::max(per_sm, 1))));
-  kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(asort, pl->d_e2q, pl->d_occ, pl->s, CH, pl->d_twj, pl->d_tws, pl->d_W, U, pl->sp.L,
-                                           int(pl->sp.L1), np, pair0, t, colsum);
+  kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(k1_args(pl, asort, t, pair0, U, np, colsum));
   QMC_LAUNCHED();
   return QMC_OK;
 }
@@ -848,6 +898,27 @@ static int ilog2(int64_t x) {
   int r = 0;
   while ((int64_t(1) << r) < x) ++r;
   return r;
+}
+
+static K2Args k2_args(const qmc_plan* pl, const CallLayout& cl, const double2* U, int ntx, int ng, int64_t pair0,
+                      const EpiArgs& E, double* part, double* colsum) {
+  K2Args a;
+  a.U = U;
+  a.L = pl->sp.L;
+  a.L2 = int(pl->sp.L2);
+  a.m = pl->m;
+  a.ntx = ntx;
+  a.ngroups = ng;
+  a.P = pl->d_P;
+  a.colsum = colsum;
+  a.scal = pl->d_scal;
+  a.tw1 = pl->d_tw1;
+  a.twL = pl->d_twL;
+  a.pair0 = pair0;
+  a.E = E;
+  a.part = part;
+  a.part_stride = cl.part_stride;
+  return a;
 }
 
 template <int R, int M, int EP>
@@ -876,8 +947,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       const int ntx = int(pl->sp.L2 / CBP), ng = (np + 15) / 16;
       const int64_t ntiles = int64_t(ntx) * ng;
       const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
-      pk<<<grid, 16 * CBP, psm, st>>>(U, pl->sp.L, int(pl->sp.L2), pl->m, ntx, ng, pl->d_P, colsum, pl->d_scal,
-                                         pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
+      pk<<<grid, 16 * CBP, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum));
       QMC_LAUNCHED();
       *nbx_used = ntx;
       return QMC_OK;
@@ -943,8 +1013,10 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   E.xvec = X && (ldx % 2 == 0) && (uintptr_t(X) % 16 == 0);
   E.t = t;
   E.N = pl->N;
+  E.rowpart = (double*)(ws + cl.off_rowsum);
   std::unique_lock<std::mutex> lock;
-  if (nsets == 2) {  // fork: both internal streams start after the caller's prior work
+  const bool two = nsets == 2 && pl->nstreams == 2;
+  if (two) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
     if (cudaEventRecord(pl->ev_fork, st) != cudaSuccess ||
         cudaStreamWaitEvent(pl->ist[0], pl->ev_fork, 0) != cudaSuccess ||
@@ -953,30 +1025,11 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
       return QMC_ECUDA;
     }
   }
-#ifdef QMC_L2_PERSIST
-  {  // keep the batch scratch U resident in L2 (access-policy window)
-    int dev = 0, maxwin = 0, maxpers = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-    cudaDeviceGetAttribute(&maxpers, cudaDevAttrMaxPersistingL2CacheSize, dev);
-    const size_t ubytes = size_t(nsets) * pairs_b * pl->sp.L * 16;
-    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min<size_t>(ubytes, size_t(maxpers)));
-    cudaStreamAttrValue av = {};
-    av.accessPolicyWindow.base_ptr = ws + cl.off_U;
-    av.accessPolicyWindow.num_bytes = std::min<size_t>(ubytes, size_t(maxwin));
-    av.accessPolicyWindow.hitRatio = 1.0f;
-    av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    for (int k = 0; k < (nsets == 2 ? 2 : 1); ++k)
-      cudaStreamSetAttribute(nsets == 2 ? pl->ist[k] : st, cudaStreamAttributeAccessPolicyWindow, &av);
-    cudaGetLastError();
-  }
-#endif
   int64_t bidx = 0;
   for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs, ++bidx) {
     const int np = int(std::min<int64_t>(pl->batch_pairs, npairs_total - pair0));
     const int set = nsets == 2 ? int(bidx & 1) : 0;
-    const cudaStream_t bs = nsets == 2 ? pl->ist[set] : st;
+    const cudaStream_t bs = two ? pl->ist[set] : st;
     double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
     double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
     E.rowpart = (double*)(ws + cl.off_rowsum);
@@ -1003,7 +1056,7 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
       prof_end(KC_REDUCE, bs);
     }
   }
-  if (nsets == 2) {  // join
+  if (two) {  // join
     if (cudaEventRecord(pl->ev_join[0], pl->ist[0]) != cudaSuccess ||
         cudaEventRecord(pl->ev_join[1], pl->ist[1]) != cudaSuccess ||
         cudaStreamWaitEvent(st, pl->ev_join[0], 0) != cudaSuccess ||
