@@ -419,8 +419,12 @@ __global__ void __launch_bounds__(kColThreads, 2)
   double* xk = E.X ? E.X + k : nullptr;
   double* rowpart = EP == EPK_ROWSUM ? E.rowpart + (pair0 / PG + blockIdx.y) * E.N : nullptr;
   double2 acc = make_double2(0.0, 0.0);
+  // column groups bx = blockIdx.x, + gridDim.x, ... (the CTA's column sums
+  // accumulate over all of them: one partial slot per CTA)
+  const int nbxT = (L2 + CB - 1) / CB;
+  for (int bx = blockIdx.x; bx < nbxT; bx += gridDim.x) {
   // row 0: X[0, k] = φ(0) Σ_j A[j, k]
-  if (blockIdx.x == 0 && warp == 0) {
+  if (bx == 0 && warp == 0) {
     const bool okrow = tid < PG;
     double2 v0 = make_double2(0.0, 0.0);
     if (okp && okrow) {
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(kColThreads, 2)
   }
   if constexpr (R == 1) {
     const int c = tid / PG;
-    const int e2 = blockIdx.x * CB + c;
+    const int e2 = bx * CB + c;
     const bool okc = e2 < L2;
     // rows first: every load of the tile is issued before the first store
     int nrow[L1];
@@ -478,9 +482,9 @@ __global__ void __launch_bounds__(kColThreads, 2)
       for (int i = tid; i < PG * nb * lines; i += kColThreads) {
         const int pp = i / (nb * lines), rest = i % (nb * lines);
         const int b = rest / lines, l = rest % lines;
-        if (pg0 + pp < np && (blockIdx.x * CB) / kUB + b < L2 / kUB && (L1 * kUB * 16) % 128 == 0)
+        if (pg0 + pp < np && (bx * CB) / kUB + b < L2 / kUB && (L1 * kUB * 16) % 128 == 0)
           discard_l2(reinterpret_cast<const char*>(U + int64_t(pg0 + pp) * L +
-                                                   int64_t((blockIdx.x * CB) / kUB + b) * (L1 * kUB)) + 128 * l);
+                                                   int64_t((bx * CB) / kUB + b) * (L1 * kUB)) + 128 * l);
       }
     }
     reg_dft<L1, +1>(v, tw1);
@@ -511,7 +515,7 @@ __global__ void __launch_bounds__(kColThreads, 2)
     for (int it = tid; it < nA; it += kColThreads) {
       const int rest = it / PG;
       const int r = rest % R, c = rest / R;
-      const int e2 = blockIdx.x * CB + c;
+      const int e2 = bx * CB + c;
       const bool ok = okp && e2 < L2;
       double2 x[M];
       if (ok) {
@@ -544,7 +548,7 @@ __global__ void __launch_bounds__(kColThreads, 2)
     for (int it = tid; it < nB; it += kColThreads) {
       const int rest = it / PG;
       const int k2 = rest % M, c = rest / M;
-      const int e2 = blockIdx.x * CB + c;
+      const int e2 = bx * CB + c;
       const bool okc = e2 < L2;
       int nrow[R];
 #pragma unroll
@@ -562,6 +566,8 @@ __global__ void __launch_bounds__(kColThreads, 2)
       for (int k1 = 0; k1 < R; ++k1) emit<EP>(E, z[k1], nrow[k1], okp && nrow[k1] >= 0, has2, xk, acc, rr[k1]);
       if (EP == EPK_ROWSUM) rowsum_flush<R>(rr, nrow, PG, &rsT[warp][0], &rsN[warp][0], rowpart);
     }
+  }
+  __syncthreads();  // shared tiles are reused by the next column group
   }
   // per-column partial sums of this CTA: lanes with equal p, then warps in order
   if (EP != EPK_ROWSUM) {
@@ -900,6 +906,16 @@ static int ilog2(int64_t x) {
   return r;
 }
 
+static int sm_count_cols() {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return nsm;
+}
+
 static K2Args k2_args(const qmc_plan* pl, const CallLayout& cl, const double2* U, int ntx, int ng, int64_t pair0,
                       const EpiArgs& E, double* part, double* colsum) {
   K2Args a;
@@ -956,8 +972,12 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   auto kern = fast ? k_cols_x<R, M, EP, (R == 1)> : k_cols_x<R, M, EP, false>;
   set_smem_attr(kern, smem);
   const int CBx = cols_cb(pl, cl.PG);
-  dim3 g((unsigned)((pl->sp.L2 + CBx - 1) / CBx), (unsigned)((np + cl.PG - 1) / cl.PG));
-  *nbx_used = int(g.x);
+  const int nbxT = int((pl->sp.L2 + CBx - 1) / CBx), ngr = (np + cl.PG - 1) / cl.PG;
+  // enough CTAs for ~8 per SM; each loops over several column groups, so the
+  // column means need only gridDim.x partial slots per pair
+  const int gx = std::max(1, std::min(nbxT, (sm_count_cols() * 8 + ngr - 1) / ngr));
+  dim3 g((unsigned)gx, (unsigned)ngr);
+  *nbx_used = gx;
   kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
                                      colsum, pl->d_scal, pl->d_tw1, pl->d_twL, pair0, E, part, cl.part_stride);
   QMC_LAUNCHED();
