@@ -265,3 +265,64 @@ def test_config5_sampled(qmc):
     # Δ mean(exp X) <= tol · max exp(X) + 1e-14 · mean  (reading R16)
     tol = col_tolerance(w, cols=cols) * np.exp(Xoc).max(axis=0) + 1e-14 * np.abs(m_o)
     assert np.all(np.abs(m_g - m_o) <= tol)
+
+
+# ------------------------------------------------------------------ fused epilogues on every K2 path
+# (N, s, t, batch pairs or None): L1 = 16 pipelined K2 (t a multiple of 32),
+# partial pair groups (t = 30, 6: k_cols_x), L1 = 10 (N = 40961), the
+# two-stage column pass L1 = 96 (N = 786433), and several batches on two
+# internal streams (batch 16 of 32 pairs).
+MEAN_CASES = [(65537, 64, 32, None), (65537, 64, 30, None), (40961, 50, 32, None), (65537, 40, 64, 16),
+              (786433, 16, 6, None)]
+
+
+@pytest.mark.parametrize("N,s,t,bp", MEAN_CASES)
+@pytest.mark.parametrize("f", [W.F_IDENTITY, W.F_AFFINE, W.F_EXP, W.F_ROWMEAN_RELU])
+def test_means_every_k2_path(qmc, monkeypatch, N, s, t, bp, f):
+    import torch
+    if bp:
+        monkeypatch.setenv("QMC_BATCH_PAIRS", str(bp))
+    phi = W.PHI_INVNORM_MID if f == W.F_EXP else W.PHI_SHIFT_HALF
+    w = W.custom_lattice(N, s, t, phi, seed=N + s + t + f)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = qmc.x_empty(plan.N, t, "cuda")
+    c = 0.75
+    out = plan.mean(A, f, c, X=X)
+    torch.cuda.synchronize()
+    Xo = X_full(w)
+    tol = col_tolerance(w)
+    if f == W.F_AFFINE:
+        check_X(w, X.cpu().numpy() - c, Xo)
+    else:
+        check_X(w, X.cpu().numpy(), Xo)
+    if f == W.F_ROWMEAN_RELU:
+        Q = float(plan.finalize(f, out, t).item())
+        Qo = O.rowmean_relu(Xo)
+        assert abs(Q - Qo) <= tol.sum() / t + 1e-14 * abs(Qo)
+        np.testing.assert_allclose(out.cpu().numpy(), O.row_sums(Xo), rtol=0, atol=tol.sum())
+    else:
+        mo = O.column_means(Xo, f, c)
+        mg = out.cpu().numpy()
+        # reading R16: |Δmean| <= tol·max|f'| + 1e-14·mean|f|
+        fprime = np.exp(Xo).max(axis=0) if f == W.F_EXP else 1.0
+        assert np.all(np.abs(mg - mo) <= tol * fprime + 1e-14 * np.abs(mo) + 1e-15)
+
+
+def test_mean_host_entry(qmc):
+    """qmc_mean_host: host A in, device X, host result (the e2e path bench.py times)."""
+    import torch
+    from paper_1501_06286_b200 import _abi as abi
+    w = W.custom_lattice(65537, 48, 32, W.PHI_SHIFT_HALF, seed=11)
+    plan = qmc.Plan.from_workload(w)
+    A_host = torch.from_numpy(np.ascontiguousarray(w.A.T)).pin_memory()   # col-major s×t, lda = s
+    A_dev = torch.empty_like(A_host, device="cuda")
+    X = qmc.x_empty(plan.N, w.t, "cuda")
+    out_host = torch.empty(w.t, dtype=torch.float64).pin_memory()
+    out_dev = torch.empty(max(plan.N, w.t), dtype=torch.float64, device="cuda")
+    ws = plan.call_workspace(w.t, W.F_AFFINE)
+    abi.qmc_mean_host(plan.handle, A_host, w.s, w.t, W.F_AFFINE, 1.0, out_host, A_dev, X, w.t, out_dev, ws,
+                      ws.numel(), torch.cuda.current_stream().cuda_stream)
+    Xo = X_full(w)
+    check_X(w, X.cpu().numpy() - 1.0, Xo)
+    np.testing.assert_allclose(out_host.numpy(), O.column_means(Xo, O.F_AFFINE, 1.0), rtol=0, atol=1e-13)
