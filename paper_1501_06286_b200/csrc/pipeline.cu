@@ -165,12 +165,16 @@ __device__ __forceinline__ void k1_issue(const K1Args& a, const K1Smem<L2>& sm, 
   const int f1 = it % a.L1, p = it / a.L1;
   const int64_t q0 = int64_t(c) * a.CH;
   const int n = int(a.CH < a.s - q0 ? a.CH : a.s - q0);
-  const double2* ga = a.asort + int64_t(p) * a.s + q0;
-  const double2* gw = a.twj + int64_t(f1) * a.s + q0;
-  for (int i = threadIdx.x; i < n; i += NT) {
-    cp_async16(sm.stA + i, ga + i);
-    cp_async16(sm.stW + i, gw + i);
-    cp_async4(sm.stE + i, a.e2q + q0 + i);
+  const double2* ga = a.asort + int64_t(p) * a.s + q0 + threadIdx.x;
+  const double2* gw = a.twj + int64_t(f1) * a.s + q0 + threadIdx.x;
+  const int32_t* ge = a.e2q + q0 + threadIdx.x;
+  double2* sa = sm.stA + threadIdx.x;
+  double2* sw = sm.stW + threadIdx.x;
+  int32_t* se = sm.stE + threadIdx.x;
+  for (int i = threadIdx.x; i < n; i += NT, ga += NT, gw += NT, ge += NT, sa += NT, sw += NT, se += NT) {
+    cp_async16(sa, ga);
+    cp_async16(sw, gw);
+    cp_async4(se, ge);
   }
   cp_async_commit();
 }
@@ -201,16 +205,19 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, i
     for (int i = tid; i < n; i += NT) {
       const int pk = sm.stE[i];
       const int len = pk >> 13, e2 = pk & 8191;
-      if (len > 0) {
-        double2 acc = cmul(sm.stA[i], sm.stW[i]);
-        const int end = min(n, i + len);
-        for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
-        S[padE<E>(e2)] = acc;
-      } else if (i == 0) {  // continuation of a bucket from the previous chunk
-        double2 acc = cmul(sm.stA[0], sm.stW[0]);
-        for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
-        S[padE<E>(e2)] = cadd(S[padE<E>(e2)], acc);
-      }
+      double2 acc = cmul(sm.stA[i], sm.stW[i]);
+      const int end = min(n, i + len);
+      for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));  // collisions (rare)
+      if (len > 0) S[padE<E>(e2)] = acc;
+    }
+    if (c > 0 && tid == 0 && (sm.stE[0] >> 13) == 0) {
+      // a bucket continued from the previous chunk: its remaining entries
+      // are added by one thread after the heads (S[e2] is not touched by
+      // this chunk's heads, whose buckets all start in this chunk)
+      const int pk = sm.stE[0];
+      double2 acc = cmul(sm.stA[0], sm.stW[0]);
+      for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
+      S[padE<E>(pk & 8191)] = cadd(S[padE<E>(pk & 8191)], acc);
     }
     __syncthreads();  // staging consumed
     if (c + 1 < nch) {
