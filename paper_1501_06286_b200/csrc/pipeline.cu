@@ -808,9 +808,21 @@ struct CallLayout {
   int PG, ngroups, ngroups_all, nbx, nsets, part_stride;
 };
 
+// pairs per batch of a call on t columns: the plan's batch, capped at half
+// the call's pairs (rounded up to the pair group) so that two batches overlap
+static int64_t call_batch(const qmc_plan* pl, int64_t t) {
+  const int64_t npairs = std::max<int64_t>(1, (t + 1) / 2);
+  int64_t b = pl->batch_pairs;
+  if (npairs >= 32 && !getenv("QMC_BATCH_PAIRS")) {
+    const int64_t half = ((npairs + 1) / 2 + 15) / 16 * 16;
+    b = std::min(b, half);
+  }
+  return std::max<int64_t>(1, std::min(b, npairs));
+}
+
 static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   CallLayout c;
-  const int64_t pairs = std::max<int64_t>(1, std::min<int64_t>(pl->batch_pairs, (t + 1) / 2));
+  const int64_t pairs = call_batch(pl, t);
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t r = o;
@@ -818,7 +830,7 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
     return r;
   };
   // one scratch set (U, partial sums) per internal stream in use
-  const int64_t nbatch = ((t + 1) / 2 + pl->batch_pairs - 1) / pl->batch_pairs;
+  const int64_t nbatch = ((t + 1) / 2 + pairs - 1) / pairs;
   c.nsets = (pl->nstreams == 2 && nbatch > 1) ? 2 : 1;
   c.PG = pair_group(pairs);
   c.ngroups = int((pairs + c.PG - 1) / c.PG);
@@ -1027,7 +1039,7 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   const CallLayout cl = call_layout(pl, t, f);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
-  const int64_t pairs_b = std::max<int64_t>(1, std::min<int64_t>(pl->batch_pairs, (t + 1) / 2));
+  const int64_t pairs_b = call_batch(pl, t);
   double* colsum = (double*)(ws + cl.off_colsum);
   const int64_t npairs_total = (t + 1) / 2;
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
@@ -1053,8 +1065,8 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     }
   }
   int64_t bidx = 0;
-  for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pl->batch_pairs, ++bidx) {
-    const int np = int(std::min<int64_t>(pl->batch_pairs, npairs_total - pair0));
+  for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pairs_b, ++bidx) {
+    const int np = int(std::min<int64_t>(pairs_b, npairs_total - pair0));
     const int set = nsets == 2 ? int(bidx & 1) : 0;
     const cudaStream_t bs = two ? pl->ist[set] : st;
     double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;

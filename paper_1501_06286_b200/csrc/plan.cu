@@ -459,16 +459,17 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->ws = (char*)plan_ws;
   pl->ws_bytes = plan_ws_bytes;
   {
-    // U of one batch (16·L bytes per pair) ~128 MB per scratch set (measured
-    // best for config 2: fewer, longer launches keep more items per
-    // persistent CTA; U does not stay in L2 between K1 and K2 on B200 anyway,
-    // DESIGN.md §5); at least two waves of K1 CTAs; a multiple of the K2 pair
-    // group (16, 8 or 4 pairs)
+    // Batch of column pairs (measured on B200): enough K1 items
+    // (L1 per pair) for ~8192 per launch — persistent CTAs then keep several
+    // items each and the long launches amortise their tails — with U (16·L
+    // bytes per pair) at least ~128 MB and at most ~768 MB per scratch set;
+    // a multiple of the K2 pair group (16, 8 or 4 pairs).  Per call the
+    // batch is further capped at half the call's pairs (run() / call_layout),
+    // so that two batches can overlap on the two internal streams.
     const int64_t per_pair = 16 * sp.L;
-    int64_t bp = std::max<int64_t>(1, (int64_t(128) << 20) / per_pair);
-    const int64_t want = (296 + sp.L1 - 1) / sp.L1;  // >= 2 waves of K1 CTAs
-    if (bp < want) bp = std::max<int64_t>(bp, std::min<int64_t>(want, (int64_t(64) << 20) / per_pair));
-    bp = std::min<int64_t>(bp, 256);
+    int64_t bp = std::max<int64_t>((int64_t(128) << 20) / per_pair, (8192 + sp.L1 - 1) / sp.L1);
+    bp = std::max<int64_t>(1, std::min<int64_t>(bp, (int64_t(768) << 20) / per_pair));
+    bp = std::min<int64_t>(bp, 4096);
     bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
     pl->batch_pairs = bp;
     if (const char* ev = getenv("QMC_K1_PER_SM")) pl->k1_per_sm = int(strtol(ev, nullptr, 10));  // tuning
