@@ -813,7 +813,7 @@ struct CallLayout {
 static int64_t call_batch(const qmc_plan* pl, int64_t t) {
   const int64_t npairs = std::max<int64_t>(1, (t + 1) / 2);
   int64_t b = pl->batch_pairs;
-  if (npairs >= 32 && !getenv("QMC_BATCH_PAIRS")) {
+  if (npairs >= 128 && !getenv("QMC_BATCH_PAIRS")) {  // small calls: one batch (launch-bound)
     const int64_t half = ((npairs + 1) / 2 + 15) / 16 * 16;
     b = std::min(b, half);
   }
