@@ -580,8 +580,12 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
 #undef QMC_PLAN_LAUNCHED
   pl->nstreams = 1;
   pl->mu = new (std::nothrow) std::mutex();
+  // two internal streams overlap consecutive batches; with rows of 8192 (one
+  // K1 CTA per SM) that overlap measured slower on B200 (config 5: 119 vs
+  // 111 ms/step), so those plans run their batches on the caller's stream
   const char* one = getenv("QMC_ONE_STREAM");
-  if (!(one && one[0] == '1') && pl->mu &&
+  const bool want2 = one ? one[0] != '1' : sp.L2 < 8192;
+  if (want2 && pl->mu &&
       cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
       cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
       cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
