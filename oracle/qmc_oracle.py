@@ -37,6 +37,7 @@ __all__ = [
     "point_matrix_rows", "reordered_lattice_point", "circulant_Z", "selection_P",
     "oracle_X_rows", "oracle_X_rows_fsum", "oracle_X_full", "column_means",
     "rowmean_relu", "row_sums",
+    "pset_index_matrix", "pset_c", "pset_reordered_point",
 ]
 
 # φ enumeration (PAPER.md:295-302 names Φ^{-1}, the tent transform and the
@@ -374,3 +375,36 @@ def rowmean_relu(X: np.ndarray, t_total: int | None = None) -> float:
     t = t if t_total is None else t_total
     r = row_sums(X)
     return math.fsum(max(0.0, rn / t) for rn in r) / N
+
+
+# ---------------------------------------------------------------- Korobov p-set
+def pset_index_matrix(K: int, s: int, rows) -> np.ndarray:
+    """The union of all Korobov lattice point sets (Hua–Wang):
+    N = (K-1)^2 points x_{n,g} = ({n g^0/K}, {n g^1/K}, ..., {n g^{s-1}/K}),
+    n, g = 1..K-1, K prime.  Conventional order (reading R24): row
+    r = (g-1)(K-1) + (n-1).  Returns idx[r, j] = (n · g^j) mod K, so that
+    x_{r,j} = idx / K."""
+    rows = np.asarray(rows, dtype=np.int64)
+    g = rows // (K - 1) + 1
+    n = rows % (K - 1) + 1
+    gj = np.ones((len(rows), s), dtype=np.int64)
+    for j in range(1, s):                       # g^j mod K by repeated multiplication
+        gj[:, j] = (gj[:, j - 1] * g) % K
+    return (n[:, None] * gj) % K
+
+
+def pset_c(K: int, s: int, g: int) -> np.ndarray:
+    """c_{g,j} = (j-1)(g-1) + 1 mod (K-1), j = 1..s: the
+    column map of block g in the paper's reordered indexing, with the residue
+    0 read as K-1 (reading R5)."""
+    j = np.arange(1, s + 1, dtype=np.int64)
+    c = ((j - 1) * (g - 1) + 1) % (K - 1)
+    c[c == 0] = K - 1
+    return c
+
+
+def pset_reordered_point(K: int, beta: int, s: int, n: int, g: int) -> np.ndarray:
+    """The paper's reordered point x_{n,g} = ({β^{c_{g,j} - n} / K})_j
+    (PAPER.md:510-521), as integer numerators over K; n, g = 1..K-1."""
+    c = pset_c(K, s, g)
+    return np.array([pow(beta, int((cj - n) % (K - 1)), K) for cj in c], dtype=np.int64)

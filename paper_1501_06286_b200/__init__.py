@@ -13,10 +13,10 @@ from . import _abi
 from ._abi import (QMC_F_AFFINE, QMC_F_EXP, QMC_F_IDENTITY, QMC_F_NONE, QMC_F_ROWMEAN_RELU,
                    QMC_FAMILY_LATTICE, QMC_FAMILY_POLY, QMC_PHI_IDENTITY, QMC_PHI_INVNORM_MID,
                    QMC_PHI_SHIFT_HALF, QMC_PHI_TENT, QMCError)
-from .api import Plan, colmajor_empty, to_device_colmajor, x_empty
+from .api import KorobovPSet, Plan, colmajor_empty, to_device_colmajor, x_empty
 
 __all__ = [
-    "Plan", "QMCError", "colmajor_empty", "to_device_colmajor", "x_empty", "_abi",
+    "KorobovPSet", "Plan", "QMCError", "colmajor_empty", "to_device_colmajor", "x_empty", "_abi",
     "QMC_FAMILY_LATTICE", "QMC_FAMILY_POLY", "QMC_PHI_IDENTITY", "QMC_PHI_SHIFT_HALF",
     "QMC_PHI_TENT", "QMC_PHI_INVNORM_MID", "QMC_F_NONE", "QMC_F_IDENTITY", "QMC_F_AFFINE",
     "QMC_F_EXP", "QMC_F_ROWMEAN_RELU",

@@ -326,3 +326,23 @@ def test_mean_host_entry(qmc):
     Xo = X_full(w)
     check_X(w, X.cpu().numpy() - 1.0, Xo)
     np.testing.assert_allclose(out_host.numpy(), O.column_means(Xo, O.F_AFFINE, 1.0), rtol=0, atol=1e-13)
+
+
+# ------------------------------------------------------------------ Korobov p-set (NEXT #1)
+@pytest.mark.parametrize("K,s,t", [(5, 3, 1), (7, 9, 6), (31, 40, 33), (61, 20, 8), (257, 64, 16)])
+@pytest.mark.parametrize("phi", [W.PHI_SHIFT_HALF, W.PHI_INVNORM_MID])
+def test_korobov_pset(qmc, K, s, t, phi):
+    """X = Y·A for the union of all Korobov lattices, N = (K-1)^2 rows in the
+    conventional (g, n) order, against the oracle's plain definition."""
+    import torch
+    rng = np.random.default_rng(K * 100 + s + t)
+    A = rng.standard_normal((s, t))
+    ps = qmc.KorobovPSet(K, s, phi)
+    X = ps.matmul(qmc.to_device_colmajor(A, "cuda"))
+    torch.cuda.synchronize()
+    tab = O.phi_table(phi, K)
+    Xo = O.point_matrix_rows(tab, O.pset_index_matrix(K, s, np.arange((K - 1) ** 2))) @ A
+    tol = 1e-11 * np.abs(A).sum(axis=0) * np.abs(tab).max()
+    err = np.abs(X.cpu().numpy() - Xo).max(axis=0)
+    assert X.shape == ((K - 1) ** 2, t)
+    assert np.all(err <= tol), (err / tol).max()

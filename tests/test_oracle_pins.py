@@ -367,3 +367,62 @@ def test_config3_means_closed_form():
     means = O.column_means(X, O.F_AFFINE, 1.0)
     want = 1.0 - A.sum(axis=0) / (2 * N)
     np.testing.assert_allclose(means, want, rtol=0, atol=1e-13)
+
+
+# ---------------------------------------------------------------- Korobov p-set
+@pytest.mark.parametrize("K", [5, 7, 11, 13, 31])
+def test_pset_columns_are_uniform_multisets(K):
+    """Every column of the p-set hits each nonzero residue exactly K-1 times:
+    for fixed g, n -> n·g^j is a bijection of Z_K^* (PAPER.md:478-489), so the
+    column sums of Y are (K-1)·Σ_{i=1}^{K-1} φ(i/K) (closed form)."""
+    s = 6
+    idx = O.pset_index_matrix(K, s, np.arange((K - 1) ** 2))
+    for j in range(s):
+        counts = np.bincount(idx[:, j], minlength=K)
+        assert counts[0] == 0 and np.all(counts[1:] == K - 1)
+    tab = O.phi_table(O.PHI_SHIFT_HALF, K)
+    Y = O.point_matrix_rows(tab, idx)
+    S = math.fsum(tab[1:])
+    np.testing.assert_allclose(Y.sum(axis=0), (K - 1) * S, rtol=0, atol=1e-12 * K * K)
+
+
+@pytest.mark.parametrize("K", [5, 7, 11, 13, 31, 61])
+def test_pset_paper_reordering(K):
+    """The paper's substitution n -> β^{-(n-1)}, g -> β^{(g-1)} turns x_{n,g}
+    into ({β^{c_{g,j} - n}/K})_j with c_{g,j} = (j-1)(g-1)+1 mod (K-1)
+    (PAPER.md:510-524): checked point by point against the conventional
+    definition, exhaustively over n, g."""
+    s = 5
+    beta = O.primitive_root(K)
+    binv = pow(beta, K - 2, K)
+    for g in range(1, K):
+        for n in range(1, K):
+            nc = pow(binv, n - 1, K)            # conventional n
+            gc = pow(beta, g - 1, K)            # conventional g
+            r = (gc - 1) * (K - 1) + (nc - 1)
+            conv = O.pset_index_matrix(K, s, [r])[0]
+            assert np.array_equal(conv, O.pset_reordered_point(K, beta, s, n, g))
+
+
+@pytest.mark.parametrize("K", [7, 11, 13])
+def test_pset_blocks_are_circulant_with_one_Z(K):
+    """Y'_g = Z·P_g for every block with the same circulant Z:
+    all K-1 blocks share one spectrum, only the column map c_{g,·} changes."""
+    s = K + 2                                    # repeats in c_{g,·} (reading R18)
+    beta = O.primitive_root(K)
+    tab = O.phi_table(O.PHI_TENT, K)
+    Z = O.circulant_Z(tab[O.power_table(K, beta)])
+    for g in range(1, K):
+        Yp = np.array([tab[O.pset_reordered_point(K, beta, s, n, g)] for n in range(1, K)])
+        np.testing.assert_array_equal(Yp, Z @ O.selection_P(O.pset_c(K, s, g), K - 1))
+
+
+def test_pset_block_is_korobov_lattice():
+    """Block g (rows (g-1)(K-1) .. g(K-1)-1) is the Korobov rank-1 lattice with
+    z = (1, g, g^2, ...) mod K without its row n = 0."""
+    K, s = 31, 8
+    idx = O.pset_index_matrix(K, s, np.arange((K - 1) ** 2))
+    for g in (1, 2, 3, 17, 30):
+        z = [pow(g, j, K) for j in range(s)]
+        blk = idx[(g - 1) * (K - 1): g * (K - 1)]
+        np.testing.assert_array_equal(blk, O.lattice_index_matrix(K, z, np.arange(1, K)))
