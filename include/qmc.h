@@ -148,6 +148,22 @@ int qmc_mean_host(qmc_plan_t plan, const double* A_host, int64_t lda, int64_t t,
                   double f_param, double* out_host, double* A_dev, double* X_dev, int64_t ldx,
                   double* out_dev, void* call_ws, size_t call_ws_bytes, void* stream);
 
+/* Experiment 2 of the paper: the
+ * uniform 1-D ODE -(a u')' = g with a(x,y) = 2 + Σ_j y_j j^{-3/2} sin(2πjx),
+ * K = M-1 hat functions.  Its stiffness matrices B(y_n) = A_0 + Σ_j y_{n,j}A_j
+ * are tridiagonal; X (device, row-major N × ldx, ldx >=
+ * 2K-1) holds, per QMC point n, the perturbations Σ_j y_{n,j} A_j as computed
+ * by qmc_matmul: K diagonal entries then the K-1 entries (k, k+1) (B is
+ * symmetric).  d0, e0: the diagonal and off-diagonal entries of A_0.
+ * Solves B(y_n) û^(n) = ĝ for every n IN PLACE (X row n: û^(n) in its first
+ * K slots afterwards; the other slots are scratch) by the Thomas algorithm,
+ * one thread per sample, and writes mean_out[k] = (1/N) Σ_n û_k^(n)
+ * (PAPER.md:665-668), summed in increasing n.  rhs: device ĝ (K doubles) or
+ * NULL for ĝ = (1, ..., 1).  B must be positive definite
+ * (true for this ODE: a >= 2 - ζ(3/2)/2 > 0).  Asynchronous on `stream`. */
+int qmc_tridiag_solve_mean(int64_t N, int64_t K, double d0, double e0, const double* rhs, double* X,
+                           int64_t ldx, double* mean_out, void* stream);
+
 /* Plan facts: info[0..11] = family, N, m, s, phi, generator (β or the
  * encoding of x = 2), L (FFT length; L = m or padded L >= 2m-1), L1, L2,
  * pairs per batch, D, p.  Host pointer, >= 12 int64. */

@@ -38,6 +38,7 @@ __all__ = [
     "oracle_X_rows", "oracle_X_rows_fsum", "oracle_X_full", "column_means",
     "rowmean_relu", "row_sums",
     "pset_index_matrix", "pset_c", "pset_reordered_point",
+    "pde1d_fe_mean",
 ]
 
 # φ enumeration (PAPER.md:295-302 names Φ^{-1}, the tent transform and the
@@ -408,3 +409,27 @@ def pset_reordered_point(K: int, beta: int, s: int, n: int, g: int) -> np.ndarra
     (PAPER.md:510-521), as integer numerators over K; n, g = 1..K-1."""
     c = pset_c(K, s, g)
     return np.array([pow(beta, int((cj - n) % (K - 1)), K) for cj in c], dtype=np.int64)
+
+
+# ---------------------------------------------------------------- Experiment 2 (SURVEY §8(f) NEXT #2)
+def pde1d_fe_mean(X: np.ndarray, d0: float, e0: float, rhs: np.ndarray | None = None) -> np.ndarray:
+    """Mean FE coefficients ū = (1/N) Σ_n û^{(n)} where
+    û^{(n)} solves B(y_n) û = ĝ, B(y_n) = A_0 + Σ_j y_{n,j} A_j tridiagonal
+    (PAPER.md:672-690), given X = Y·A (row n: K diagonal then K-1
+    off-diagonal perturbations, qmc_workloads.pde1d_uniform_matrix) and
+    ĝ = (1, ..., 1) by default.  Each system is solved by
+    LAPACK's banded solver (scipy.linalg.solve_banded); the mean per k is
+    math.fsum over n."""
+    from scipy.linalg import solve_banded
+    N, t = X.shape
+    K = (t + 1) // 2
+    g = np.ones(K) if rhs is None else np.asarray(rhs, dtype=np.float64)
+    U = np.empty((N, K))
+    ab = np.zeros((3, K))
+    for n in range(N):
+        off = e0 + X[n, K:]
+        ab[0, 1:] = off
+        ab[1, :] = d0 + X[n, :K]
+        ab[2, :-1] = off
+        U[n] = solve_banded((1, 1), ab, g)
+    return np.array([math.fsum(U[:, k]) / N for k in range(K)])

@@ -23,7 +23,7 @@ EXPORTS = [
     "qmc_plan_workspace_size", "qmc_call_workspace_size", "qmc_plan_create",
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
-    "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name",
+    "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
 ]
 
 
@@ -56,6 +56,7 @@ _sig = {
     "qmc_mean_finalize": (_i32, [_vp, _i32, _vp, _i64, _vp, _vp]),
     "qmc_mean_host": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "qmc_plan_info": (_i32, [_vp, _P64]),
+    "qmc_tridiag_solve_mean": (_i32, [_i64, _i64, _d, _d, _vp, _vp, _i64, _vp, _vp]),
     "qmc_plan_tables": (_i32, [_vp, _P64, _P32, _P32, _P32, _PD]),
     "qmc_launch_count": (_i64, []),
     "qmc_plan_destroy": (None, [_vp]),
@@ -149,6 +150,11 @@ def qmc_mean_host(plan, A_host, lda: int, t: int, f: int, f_param: float, out_ho
     _check(_lib.qmc_mean_host(plan, ptr(A_host), lda, t, f, f_param, ptr(out_host), ptr(A_dev),
                               ptr(X_dev), ldx, ptr(out_dev), ptr(call_ws), call_ws_bytes, stream),
            "qmc_mean_host")
+
+
+def qmc_tridiag_solve_mean(N: int, K: int, d0: float, e0: float, rhs, X, ldx: int, mean_out, stream=None):
+    _check(_lib.qmc_tridiag_solve_mean(N, K, d0, e0, ptr(rhs), ptr(X), ldx, ptr(mean_out), stream),
+           "qmc_tridiag_solve_mean")
 
 
 def qmc_plan_info(plan) -> dict:

@@ -146,3 +146,33 @@ def custom_poly(D: int, p: int, s: int, t: int, phi: int, seed: int,
     A = np.asfortranarray(rng.standard_normal((s, t)))
     return Workload(f"poly_D{D}_p{p}_s{s}_t{t}_phi{phi}", FAMILY_POLY, 1 << D, m, s, t, phi,
                     q, A, D=D, p=p, f=f, f_param=f_param, seed=seed)
+
+
+# ---------------------------------------------------------------- Experiment 2
+def pde1d_uniform_matrix(M: int, s: int) -> tuple[np.ndarray, float, float]:
+    """Stiffness coefficients of the paper's uniform 1-D ODE:
+    -(a u')' = g on (0,1), a(x, y) = 2 + Σ_j y_j j^{-3/2} sin(2π j x), hat
+    functions on x_k = k/M, K = M-1 unknowns.  Returns (A, d0, e0): A is the
+    s × (2K-1) matrix (Fortran order) whose column c holds a_{j,k,l} for
+    j = 1..s at the tridiagonal position c — c < K: (k, k), k = c+1; c >= K:
+    (k, k+1), k = c-K+1 — and d0 = a_{0,k,k} = 4M, e0 = a_{0,k,k+1} = -2M.
+    The closed forms are the paper's, restated."""
+    K = M - 1
+    j = np.arange(1, s + 1, dtype=np.float64)[:, None]
+    amp = M * M / (np.pi * j ** 2.5)
+    k = np.arange(1, K + 1, dtype=np.float64)[None, :]
+    diag = amp * np.sin(2 * np.pi * j / M) * np.sin(2 * np.pi * j * k / M)
+    ko = np.arange(1, K, dtype=np.float64)[None, :]
+    off = -amp * np.sin(np.pi * j / M) * np.sin(np.pi * j * (2 * ko + 1) / M)
+    A = np.asfortranarray(np.concatenate([diag, off], axis=1))
+    return A, 4.0 * M, -2.0 * M
+
+
+def pde1d_uniform(N: int, M: int, s: int, seed: int = 2) -> Workload:
+    """Experiment 2 workload: lattice rule N (prime), random z (reading R19),
+    φ(u) = u - 1/2, A from pde1d_uniform_matrix."""
+    rng = np.random.default_rng(seed)
+    z = _z(rng, N - 1, s)
+    A, d0, e0 = pde1d_uniform_matrix(M, s)
+    return Workload(f"exp2_pde1d_N{N}_M{M}_s{s}", FAMILY_LATTICE, N, N - 1, s, A.shape[1],
+                    PHI_SHIFT_HALF, z, A, seed=seed, extra={"M": M, "K": M - 1, "d0": d0, "e0": e0})

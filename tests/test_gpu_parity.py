@@ -346,3 +346,21 @@ def test_korobov_pset(qmc, K, s, t, phi):
     err = np.abs(X.cpu().numpy() - Xo).max(axis=0)
     assert X.shape == ((K - 1) ** 2, t)
     assert np.all(err <= tol), (err / tol).max()
+
+
+# ------------------------------------------------------------------ Experiment 2 (NEXT #2)
+@pytest.mark.parametrize("N,M,s", [(67, 134, 134), (127, 254, 254), (257, 514, 514), (1021, 32, 32)])
+def test_pde1d_uniform_mean(qmc, N, M, s):
+    """Mean FE coefficients of the paper's uniform ODE:
+    fast X = Y·A, N Thomas solves and the mean on the GPU, against the oracle
+    (direct product, LAPACK banded solves, fsum).  Tolerance: the R16 bound on
+    X propagates through B^{-1} (condition number ≈ (M/π)^2); rtol 1e-8 is
+    far above the observed error and far below any meaningful difference."""
+    import torch
+    w = W.pde1d_uniform(N, M, s, seed=N)
+    pde = qmc.UniformPDE1D(w.N, w.z, w.A, w.extra["d0"], w.extra["e0"])
+    ubar = pde.solve_mean().cpu().numpy()
+    torch.cuda.synchronize()
+    Xo = X_full(w)
+    uo = O.pde1d_fe_mean(Xo, w.extra["d0"], w.extra["e0"])
+    np.testing.assert_allclose(ubar, uo, rtol=1e-8, atol=0)

@@ -426,3 +426,49 @@ def test_pset_block_is_korobov_lattice():
         z = [pow(g, j, K) for j in range(s)]
         blk = idx[(g - 1) * (K - 1): g * (K - 1)]
         np.testing.assert_array_equal(blk, O.lattice_index_matrix(K, z, np.arange(1, K)))
+
+
+# ---------------------------------------------------------------- Experiment 2 (NEXT #2)
+def test_pde1d_stiffness_closed_forms_by_quadrature():
+    """The paper's closed forms of a_{j,k,l} = ∫ j^{-3/2} sin(2πjx) φ'_k φ'_l dx
+    (PAPER.md:862-868), as restated by qmc_workloads.pde1d_uniform_matrix,
+    against adaptive quadrature of the integral itself (φ'_k = ±M on the two
+    elements of node k)."""
+    from scipy.integrate import quad
+    M, s = 9, 5
+    A, d0, e0 = W.pde1d_uniform_matrix(M, s)
+    K = M - 1
+    assert d0 == 4 * M and e0 == -2 * M          # ∫ 2 φ'_k φ'_l: 2·2M, 2·(-M)
+    for j in range(1, s + 1):
+        psi = lambda x, j=j: j ** -1.5 * np.sin(2 * np.pi * j * x)  # noqa: E731
+        for k in range(1, K + 1):                 # (k, k): M^2 ∫ over [x_{k-1}, x_{k+1}]
+            v = M * M * quad(psi, (k - 1) / M, (k + 1) / M, epsabs=1e-13)[0]
+            assert abs(A[j - 1, k - 1] - v) <= 1e-9 * max(1.0, abs(v))
+        for k in range(1, K):                     # (k, k+1): -M^2 ∫ over [x_k, x_{k+1}]
+            v = -M * M * quad(psi, k / M, (k + 1) / M, epsabs=1e-13)[0]
+            assert abs(A[j - 1, K + k - 1] - v) <= 1e-9 * max(1.0, abs(v))
+
+
+def test_pde1d_solve_closed_form_constant_coefficient():
+    """y = 0 (no perturbation): B = 2M·tridiag(-1, 2, -1) and ĝ = 1, whose
+    solution is û_k = k(K+1-k) / (4M) (discrete Poisson, closed form)."""
+    M = 12
+    K = M - 1
+    X = np.zeros((3, 2 * K - 1))
+    ubar = O.pde1d_fe_mean(X, 4.0 * M, -2.0 * M)
+    k = np.arange(1, K + 1)
+    np.testing.assert_allclose(ubar, k * (K + 1 - k) / (4.0 * M), rtol=1e-13)
+
+
+def test_pde1d_solve_matches_dense():
+    """The banded solves of the oracle against dense np.linalg.solve."""
+    rng = np.random.default_rng(7)
+    M, N = 10, 4
+    K = M - 1
+    X = 0.3 * rng.standard_normal((N, 2 * K - 1)) * M
+    d0, e0 = 4.0 * M, -2.0 * M
+    U = []
+    for n in range(N):
+        B = np.diag(d0 + X[n, :K]) + np.diag(e0 + X[n, K:], 1) + np.diag(e0 + X[n, K:], -1)
+        U.append(np.linalg.solve(B, np.ones(K)))
+    np.testing.assert_allclose(O.pde1d_fe_mean(X, d0, e0), np.mean(U, axis=0), rtol=1e-12)
