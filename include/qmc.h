@@ -164,6 +164,20 @@ int qmc_mean_host(qmc_plan_t plan, const double* A_host, int64_t lda, int64_t t,
 int qmc_tridiag_solve_mean(int64_t N, int64_t K, double d0, double e0, const double* rhs, double* X,
                            int64_t ldx, double* mean_out, void* stream);
 
+/* Experiment 3 of the paper (SURVEY §8(f) NEXT
+ * #3): the log-normal 1-D ODE, a(x,y) = exp(ψ_0 + Σ_j y_j ψ_j(x)), M hat
+ * elements, equal-weight quadrature at the M element midpoints (reading
+ * R25).  X (device, row-major N × ldx, ldx >= 2M-2) holds in its first M
+ * slots θ_{n,i} = Σ_j y_{n,j} ψ_j(x_i) as computed by qmc_matmul (Θ = Y·Ψ,
+ * Eq. fastB).  Forms B̂(y_n) on the fly — a_i = exp(ψ_0 + θ_i), diagonal
+ * M (a_{k-1} + a_k), off-diagonal -M a_k (Eq. def:b nkl) — and solves
+ * B̂ û = ĝ in place (û^(n) in the first M-1 slots of row n afterwards; slots
+ * up to 2M-3 are scratch), one warp per 32 samples; mean_out[k] =
+ * (1/N) Σ_n û_k^(n), summed in increasing n.  rhs: device ĝ (M-1 doubles) or
+ * NULL for ĝ = 1.  Asynchronous on `stream`. */
+int qmc_fe1d_lognormal_solve_mean(int64_t N, int64_t M, double psi0, const double* rhs, double* X,
+                                  int64_t ldx, double* mean_out, void* stream);
+
 /* Plan facts: info[0..11] = family, N, m, s, phi, generator (β or the
  * encoding of x = 2), L (FFT length; L = m or padded L >= 2m-1), L1, L2,
  * pairs per batch, D, p.  Host pointer, >= 12 int64. */

@@ -38,7 +38,7 @@ __all__ = [
     "oracle_X_rows", "oracle_X_rows_fsum", "oracle_X_full", "column_means",
     "rowmean_relu", "row_sums",
     "pset_index_matrix", "pset_c", "pset_reordered_point",
-    "pde1d_fe_mean",
+    "pde1d_fe_mean", "pde1d_lognormal_fe_mean",
 ]
 
 # φ enumeration (PAPER.md:295-302 names Φ^{-1}, the tent transform and the
@@ -430,6 +430,30 @@ def pde1d_fe_mean(X: np.ndarray, d0: float, e0: float, rhs: np.ndarray | None = 
         off = e0 + X[n, K:]
         ab[0, 1:] = off
         ab[1, :] = d0 + X[n, :K]
+        ab[2, :-1] = off
+        U[n] = solve_banded((1, 1), ab, g)
+    return np.array([math.fsum(U[:, k]) / N for k in range(K)])
+
+
+def pde1d_lognormal_fe_mean(Theta: np.ndarray, psi0: float, rhs: np.ndarray | None = None) -> np.ndarray:
+    """Experiment 3: Θ = Y·Ψ at the M element
+    midpoints (N × M), a_i = exp(ψ_0 + Θ[n, i]); the equal-weight quadrature
+    (weight 1/M, reading R25) of b_{n,k,l} = ∫ a φ'_k φ'_l (Eq. def:b nkl)
+    gives the tridiagonal B̂(y_n): diagonal M (a_{k-1} + a_k) for node k =
+    1..M-1 (elements k-1 and k, 0-based), off-diagonal -M a_k between nodes
+    k and k+1.  Solves B̂ û = ĝ (ĝ = 1) with LAPACK's banded solver; returns
+    ū = (1/N) Σ_n û^{(n)} (fsum)."""
+    from scipy.linalg import solve_banded
+    N, M = Theta.shape
+    K = M - 1
+    g = np.ones(K) if rhs is None else np.asarray(rhs, dtype=np.float64)
+    U = np.empty((N, K))
+    ab = np.zeros((3, K))
+    for n in range(N):
+        a = np.exp(psi0 + Theta[n])
+        off = -M * a[1:K]
+        ab[0, 1:] = off
+        ab[1, :] = M * (a[:K] + a[1:])
         ab[2, :-1] = off
         U[n] = solve_banded((1, 1), ab, g)
     return np.array([math.fsum(U[:, k]) / N for k in range(K)])

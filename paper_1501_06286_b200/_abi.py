@@ -24,6 +24,7 @@ EXPORTS = [
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
+    "qmc_fe1d_lognormal_solve_mean",
 ]
 
 
@@ -57,6 +58,7 @@ _sig = {
     "qmc_mean_host": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
     "qmc_plan_info": (_i32, [_vp, _P64]),
     "qmc_tridiag_solve_mean": (_i32, [_i64, _i64, _d, _d, _vp, _vp, _i64, _vp, _vp]),
+    "qmc_fe1d_lognormal_solve_mean": (_i32, [_i64, _i64, _d, _vp, _vp, _i64, _vp, _vp]),
     "qmc_plan_tables": (_i32, [_vp, _P64, _P32, _P32, _P32, _PD]),
     "qmc_launch_count": (_i64, []),
     "qmc_plan_destroy": (None, [_vp]),
@@ -155,6 +157,11 @@ def qmc_mean_host(plan, A_host, lda: int, t: int, f: int, f_param: float, out_ho
 def qmc_tridiag_solve_mean(N: int, K: int, d0: float, e0: float, rhs, X, ldx: int, mean_out, stream=None):
     _check(_lib.qmc_tridiag_solve_mean(N, K, d0, e0, ptr(rhs), ptr(X), ldx, ptr(mean_out), stream),
            "qmc_tridiag_solve_mean")
+
+
+def qmc_fe1d_lognormal_solve_mean(N: int, M: int, psi0: float, rhs, X, ldx: int, mean_out, stream=None):
+    _check(_lib.qmc_fe1d_lognormal_solve_mean(N, M, psi0, ptr(rhs), ptr(X), ldx, ptr(mean_out), stream),
+           "qmc_fe1d_lognormal_solve_mean")
 
 
 def qmc_plan_info(plan) -> dict:

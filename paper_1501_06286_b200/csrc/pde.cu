@@ -30,39 +30,48 @@ __device__ __forceinline__ void cpa8(double* smem, const double* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(gmem) : "memory");
 }
 
-// stage tile [k0, k0+kTT) of the diagonal and off-diagonal slots of the
-// warp's 32 rows (rows >= N and k >= K are skipped)
-__device__ __forceinline__ void thomas_stage(const double* X, int64_t ldx, int64_t N, int64_t K, int64_t n0, int64_t k0,
-                                             double* sd, double* se) {
+// Matrix source of the tiled solver.
+//   TD_PERTURB  : row n = K diagonal then K-1 off-diagonal perturbations of
+//                 A_0 (Experiment 2): d_k = d0 + X[k], e_k = e0 + X[K + k];
+//                 c'_k is kept in slot K + k.
+//   TD_LOGNORMAL: row n = θ at the M = K+1 element midpoints (Experiment 3):
+//                 a_i = exp(ψ_0 + θ_i), d_k = h (a_k + a_{k+1}),
+//                 e_k = -h a_{k+1} (h = d0 = M, ψ_0 = e0); c'_k in slot K+1+k.
+enum { TD_PERTURB = 0, TD_LOGNORMAL = 1 };
+
+// stage tile [k0, k0+kTT) of the warp's 32 rows: sd ← slots k0.. (for the
+// log-normal forward pass one more, the lookahead θ_{k0+kTT}, into the pad
+// column), se ← slots ob + k0.. (off-diagonal or c'); rows >= N skipped
+__device__ __forceinline__ void thomas_stage(const double* X, int64_t ldx, int64_t N, int64_t nd, int64_t ne,
+                                             int64_t ob, int64_t n0, int64_t k0, double* sd, double* se,
+                                             bool look) {
   const int lane = threadIdx.x;
   for (int r = 0; r < 32; ++r) {
     const int64_t n = n0 + r;
     if (n >= N) break;
     const double* row = X + n * ldx;
-    for (int c = lane; c < kTT; c += 32) {
-      const int64_t k = k0 + c;
-      if (k < K) cpa8(&sd[r * kTP + c], row + k);
-      if (k + 1 < K) cpa8(&se[r * kTP + c], row + K + k);
-    }
+    const int64_t k = k0 + lane;
+    if (k < nd) cpa8(&sd[r * kTP + lane], row + k);
+    if (k < ne) cpa8(&se[r * kTP + lane], row + ob + k);
+    if (look && lane == 0 && k0 + kTT < nd) cpa8(&sd[r * kTP + kTT], row + k0 + kTT);
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
 
-__device__ __forceinline__ void thomas_store(double* X, int64_t ldx, int64_t N, int64_t K, int64_t n0, int64_t k0,
-                                             const double* sd, const double* se, bool off) {
+__device__ __forceinline__ void thomas_store(double* X, int64_t ldx, int64_t N, int64_t K, int64_t ob, int64_t n0,
+                                             int64_t k0, const double* sd, const double* se, bool off) {
   const int lane = threadIdx.x;
   for (int r = 0; r < 32; ++r) {
     const int64_t n = n0 + r;
     if (n >= N) break;
     double* row = X + n * ldx;
-    for (int c = lane; c < kTT; c += 32) {
-      const int64_t k = k0 + c;
-      if (k < K) row[k] = sd[r * kTP + c];
-      if (off && k + 1 < K) row[K + k] = se[r * kTP + c];
-    }
+    const int64_t k = k0 + lane;
+    if (k < K) row[k] = sd[r * kTP + lane];
+    if (off && k + 1 < K) row[ob + k] = se[r * kTP + lane];
   }
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(32) k_thomas_tiled(int64_t N, int64_t K, double d0, double e0,
                                                       const double* __restrict__ rhs, double* __restrict__ X,
                                                       int64_t ldx) {
@@ -70,13 +79,17 @@ __global__ void __launch_bounds__(32) k_thomas_tiled(int64_t N, int64_t K, doubl
   const int lane = threadIdx.x;
   const int64_t n0 = int64_t(blockIdx.x) * 32;
   const int64_t ntile = (K + kTT - 1) / kTT;
-  // forward sweep: slots become g'_k (diagonal) and c'_k (off-diagonal)
-  double cprev = 0.0, gprev = 0.0, eprev = 0.0;
-  thomas_stage(X, ldx, N, K, n0, 0, sd[0], se[0]);
+  const bool LN = MODE == TD_LOGNORMAL;
+  const int64_t ob = LN ? K + 1 : K;        // slot of c'_0
+  const int64_t ndf = LN ? K + 1 : K;       // forward pass: matrix slots on the diagonal side
+  const int64_t nef = LN ? 0 : K - 1;       // forward pass: off-diagonal slots read
+  // forward sweep: slots become g'_k (diagonal side) and c'_k (slot ob + k)
+  double cprev = 0.0, gprev = 0.0, eprev = 0.0, aprev = 0.0;
+  thomas_stage(X, ldx, N, ndf, nef, ob, n0, 0, sd[0], se[0], LN);
   for (int64_t tI = 0; tI < ntile; ++tI) {
     const int b = int(tI & 1);
     if (tI + 1 < ntile) {
-      thomas_stage(X, ldx, N, K, n0, (tI + 1) * kTT, sd[b ^ 1], se[b ^ 1]);
+      thomas_stage(X, ldx, N, ndf, nef, ob, n0, (tI + 1) * kTT, sd[b ^ 1], se[b ^ 1], LN);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -86,14 +99,24 @@ __global__ void __launch_bounds__(32) k_thomas_tiled(int64_t N, int64_t K, doubl
     double* d = &sd[b][lane * kTP];
     double* e = &se[b][lane * kTP];
     const int cnt = int(K - k0 < kTT ? K - k0 : kTT);
+    if (LN && tI == 0) aprev = exp(e0 + d[0]);
     for (int c = 0; c < cnt; ++c) {
       const int64_t k = k0 + c;
       const double g = rhs ? __ldg(&rhs[k]) : 1.0;
-      const double inv = 1.0 / ((d0 + d[c]) - eprev * cprev);
+      double dk, ek = 0.0;
+      if (LN) {
+        const double anext = exp(e0 + d[c + 1]);   // θ_{k+1} (the pad column at c = kTT - 1)
+        dk = d0 * (aprev + anext);
+        ek = -d0 * anext;
+        aprev = anext;
+      } else {
+        dk = d0 + d[c];
+        if (k + 1 < K) ek = e0 + e[c];
+      }
+      const double inv = 1.0 / (dk - eprev * cprev);
       const double gk = (g - eprev * gprev) * inv;
       double ck = 0.0;
       if (k + 1 < K) {
-        const double ek = e0 + e[c];
         ck = ek * inv;
         e[c] = ck;
         eprev = ek;
@@ -103,16 +126,16 @@ __global__ void __launch_bounds__(32) k_thomas_tiled(int64_t N, int64_t K, doubl
       gprev = gk;
     }
     __syncwarp();
-    thomas_store(X, ldx, N, K, n0, k0, sd[b], se[b], true);
+    thomas_store(X, ldx, N, K, ob, n0, k0, sd[b], se[b], true);
     __syncwarp();
   }
   // back substitution, tiles in decreasing k: u_k = g'_k - c'_k u_{k+1}
   double u = 0.0;
-  thomas_stage(X, ldx, N, K, n0, (ntile - 1) * kTT, sd[0], se[0]);
+  thomas_stage(X, ldx, N, K, K - 1, ob, n0, (ntile - 1) * kTT, sd[0], se[0], false);
   for (int64_t tI = ntile - 1, it = 0; tI >= 0; --tI, ++it) {
     const int b = int(it & 1);
     if (tI > 0) {
-      thomas_stage(X, ldx, N, K, n0, (tI - 1) * kTT, sd[b ^ 1], se[b ^ 1]);
+      thomas_stage(X, ldx, N, K, K - 1, ob, n0, (tI - 1) * kTT, sd[b ^ 1], se[b ^ 1], false);
       asm volatile("cp.async.wait_group 1;" ::: "memory");
     } else {
       asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -128,7 +151,7 @@ __global__ void __launch_bounds__(32) k_thomas_tiled(int64_t N, int64_t K, doubl
       d[c] = u;
     }
     __syncwarp();
-    thomas_store(X, ldx, N, K, n0, k0, sd[b], se[b], false);
+    thomas_store(X, ldx, N, K, ob, n0, k0, sd[b], se[b], false);
     __syncwarp();
   }
 }
@@ -188,8 +211,21 @@ extern "C" int qmc_tridiag_solve_mean(int64_t N, int64_t K, double d0, double e0
   if (getenv("QMC_THOMAS_SIMPLE")) {
     k_thomas<<<unsigned((N + 127) / 128), 128, 0, st>>>(N, K, d0, e0, rhs, X, ldx);
   } else {
-    k_thomas_tiled<<<unsigned((N + 31) / 32), 32, 0, st>>>(N, K, d0, e0, rhs, X, ldx);
+    k_thomas_tiled<TD_PERTURB><<<unsigned((N + 31) / 32), 32, 0, st>>>(N, K, d0, e0, rhs, X, ldx);
   }
+  QMC_LAUNCHED();
+  k_col_mean<<<unsigned((K + 255) / 256), 256, 0, st>>>(N, K, X, ldx, mean_out);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
+extern "C" int qmc_fe1d_lognormal_solve_mean(int64_t N, int64_t M, double psi0, const double* rhs, double* X,
+                                             int64_t ldx, double* mean_out, void* stream) {
+  if (!X || !mean_out) return QMC_ENULL;
+  const int64_t K = M - 1;
+  if (N < 1 || K < 1 || ldx < 2 * K) return QMC_EINVAL_DIM;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_thomas_tiled<TD_LOGNORMAL><<<unsigned((N + 31) / 32), 32, 0, st>>>(N, K, double(M), psi0, rhs, X, ldx);
   QMC_LAUNCHED();
   k_col_mean<<<unsigned((K + 255) / 256), 256, 0, st>>>(N, K, X, ldx, mean_out);
   QMC_LAUNCHED();

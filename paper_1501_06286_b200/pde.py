@@ -43,3 +43,30 @@ class UniformPDE1D:
         abi.qmc_tridiag_solve_mean(self.N, self.K, self.d0, self.e0, None, self.X, self.t, self.mean,
                                    _stream(self.device))
         return self.mean
+
+
+class LognormalPDE1D:
+    """Fast-QMC mean FE coefficients of the log-normal ODE of Experiment 3
+    (PAPER.md:716-767, 924-940): Θ = Y·Ψ by the fast path (Ψ: s × M values of
+    ψ_j at the element midpoints, qmc_workloads.pde1d_lognormal_matrix), then
+    the on-the-fly exp / midpoint-rule assembly, the N tridiagonal solves and
+    the mean in qmc_fe1d_lognormal_solve_mean.  φ defaults to Φ^{-1}(u +
+    1/(2N)) (y_j ~ N(0,1), reading R26)."""
+
+    def __init__(self, N: int, z, Psi: np.ndarray, psi0: float, phi: int = abi.QMC_PHI_INVNORM_MID,
+                 device=None):
+        self.device = torch.device(device if device is not None else "cuda")
+        self.plan = Plan.lattice(N, z, phi, device=self.device)
+        self.N = N
+        self.M = Psi.shape[1]
+        self.psi0 = float(psi0)
+        self.Psi = to_device_colmajor(Psi, self.device)
+        self.ldx = 2 * self.M - 2
+        self.buf = torch.empty((N, self.ldx), dtype=torch.float64, device=self.device)
+        self.mean = torch.empty(self.M - 1, dtype=torch.float64, device=self.device)
+
+    def solve_mean(self) -> torch.Tensor:
+        self.plan.matmul(self.Psi, self.buf[:, :self.M])      # Θ in the first M slots of each row
+        abi.qmc_fe1d_lognormal_solve_mean(self.N, self.M, self.psi0, None, self.buf, self.ldx, self.mean,
+                                          _stream(self.device))
+        return self.mean

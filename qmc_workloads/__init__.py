@@ -176,3 +176,26 @@ def pde1d_uniform(N: int, M: int, s: int, seed: int = 2) -> Workload:
     A, d0, e0 = pde1d_uniform_matrix(M, s)
     return Workload(f"exp2_pde1d_N{N}_M{M}_s{s}", FAMILY_LATTICE, N, N - 1, s, A.shape[1],
                     PHI_SHIFT_HALF, z, A, seed=seed, extra={"M": M, "K": M - 1, "d0": d0, "e0": e0})
+
+
+# ---------------------------------------------------------------- Experiment 3
+def pde1d_lognormal_matrix(M: int, s: int) -> tuple[np.ndarray, float]:
+    """Log-normal ODE of Experiment 3: a(x, y) =
+    exp(ψ_0 + Σ_j y_j ψ_j(x)), ψ_0 = 2, ψ_j(x) = j^{-3/2} sin(2π j x), with
+    an equal-weight quadrature of I = M points (reading R25: the midpoint of
+    each of the M elements, weight 1/M).  Returns (Ψ, ψ_0): Ψ is s × M
+    (Fortran order), Ψ[j-1, i] = ψ_j((i + 1/2)/M), so that Θ = ψ_0 + Y·Ψ
+    (PAPER.md:757-767, Eq. fastB)."""
+    j = np.arange(1, s + 1, dtype=np.float64)[:, None]
+    x = (np.arange(M, dtype=np.float64)[None, :] + 0.5) / M
+    return np.asfortranarray(j ** -1.5 * np.sin(2 * np.pi * j * x)), 2.0
+
+
+def pde1d_lognormal(N: int, M: int, s: int, seed: int = 3) -> Workload:
+    """Experiment 3 workload: lattice rule N, random z (R19), y_j ~ N(0,1) via
+    φ(u) = Φ^{-1}(u + 1/(2N)) (reading R26), Ψ from pde1d_lognormal_matrix."""
+    rng = np.random.default_rng(seed)
+    z = _z(rng, N - 1, s)
+    Psi, psi0 = pde1d_lognormal_matrix(M, s)
+    return Workload(f"exp3_pde1d_lognormal_N{N}_M{M}_s{s}", FAMILY_LATTICE, N, N - 1, s, M,
+                    PHI_INVNORM_MID, z, Psi, seed=seed, extra={"M": M, "K": M - 1, "psi0": psi0})

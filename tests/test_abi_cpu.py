@@ -24,7 +24,7 @@ def abi():
 def declared_functions():
     txt = open(os.path.join(ROOT, "include", "qmc.h")).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(qmc_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(qmc_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_exports_every_declared_symbol(abi):

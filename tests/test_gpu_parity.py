@@ -364,3 +364,20 @@ def test_pde1d_uniform_mean(qmc, N, M, s):
     Xo = X_full(w)
     uo = O.pde1d_fe_mean(Xo, w.extra["d0"], w.extra["e0"])
     np.testing.assert_allclose(ubar, uo, rtol=1e-8, atol=0)
+
+
+# ------------------------------------------------------------------ Experiment 3 (NEXT #3)
+@pytest.mark.parametrize("N,M,s", [(67, 134, 134), (257, 514, 514), (1021, 33, 33), (127, 40, 254)])
+def test_pde1d_lognormal_mean(qmc, N, M, s):
+    """Mean FE coefficients of the paper's log-normal ODE:
+    fast Θ = Y·Ψ, on-the-fly exp / midpoint assembly, N Thomas solves and the
+    mean on the GPU, against the oracle (direct product, LAPACK banded
+    solves).  rtol 1e-8 as for Experiment 2 (the exp adds a factor max a)."""
+    import torch
+    w = W.pde1d_lognormal(N, M, s, seed=N)
+    pde = qmc.LognormalPDE1D(w.N, w.z, w.A, w.extra["psi0"])
+    ubar = pde.solve_mean().cpu().numpy()
+    torch.cuda.synchronize()
+    Theta = X_full(w)
+    uo = O.pde1d_lognormal_fe_mean(Theta, w.extra["psi0"])
+    np.testing.assert_allclose(ubar, uo, rtol=1e-8, atol=0)

@@ -472,3 +472,41 @@ def test_pde1d_solve_matches_dense():
         B = np.diag(d0 + X[n, :K]) + np.diag(e0 + X[n, K:], 1) + np.diag(e0 + X[n, K:], -1)
         U.append(np.linalg.solve(B, np.ones(K)))
     np.testing.assert_allclose(O.pde1d_fe_mean(X, d0, e0), np.mean(U, axis=0), rtol=1e-12)
+
+
+# ---------------------------------------------------------------- Experiment 3 (NEXT #3)
+def test_pde1d_lognormal_constant_coefficient_closed_form():
+    """Θ = 0: a = e^{ψ0} everywhere, B̂ = e^{ψ0}·M·tridiag(-1, 2, -1), whose
+    solution with ĝ = 1 is û_k = k(K+1-k) / (2 e^{ψ0} M)."""
+    M = 10
+    K = M - 1
+    ubar = O.pde1d_lognormal_fe_mean(np.zeros((2, M)), 2.0)
+    k = np.arange(1, K + 1)
+    np.testing.assert_allclose(ubar, k * (K + 1 - k) / (2 * np.exp(2.0) * M), rtol=1e-13)
+
+
+def test_pde1d_lognormal_midpoint_assembly_exact_for_affine_coefficient():
+    """When a(x) is affine on every element the one-point midpoint rule of
+    reading R25 is exact, so the oracle's assembled B̂ must equal the exact
+    stiffness ∫ a φ'_k φ'_l dx (adaptive quadrature): checked through the
+    solution ū for a(x) = 1 + x (log a at the midpoints supplied as Θ)."""
+    from scipy.integrate import quad
+    M = 8
+    K = M - 1
+    mids = (np.arange(M) + 0.5) / M
+    Theta = np.log(1.0 + mids)[None, :] - 2.0          # exp(2 + Θ) = 1 + x at the midpoints
+    ubar = O.pde1d_lognormal_fe_mean(Theta, 2.0)
+    a = lambda x: 1.0 + x  # noqa: E731
+    B = np.zeros((K, K))
+    for k in range(1, K + 1):
+        B[k - 1, k - 1] = M * M * quad(a, (k - 1) / M, (k + 1) / M)[0]
+        if k < K:
+            B[k - 1, k] = B[k, k - 1] = -M * M * quad(a, k / M, (k + 1) / M)[0]
+    np.testing.assert_allclose(ubar, np.linalg.solve(B, np.ones(K)), rtol=1e-12)
+
+
+def test_pde1d_lognormal_psi_matrix():
+    """Ψ[j-1, i] = j^{-3/2} sin(2π j (i + 1/2)/M) (R25)."""
+    Psi, psi0 = W.pde1d_lognormal_matrix(6, 4)
+    assert psi0 == 2.0 and Psi.shape == (4, 6)
+    assert abs(Psi[2, 1] - 3 ** -1.5 * math.sin(2 * math.pi * 3 * 1.5 / 6)) < 1e-15
