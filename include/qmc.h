@@ -111,6 +111,18 @@ int qmc_call_workspace_size(qmc_plan_t plan, int64_t t, int f, size_t* call_byte
 int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
                     void* plan_ws, size_t plan_ws_bytes, void* stream);
 
+/* Randomly shifted rank-1 lattice (the paper's equal shift, PAPER.md:466-468;
+ * SURVEY §8(f) NEXT #4): as qmc_plan_create with every point shifted by the
+ * same Δ in [0, 1) in every coordinate, x_{n,j} = frac(n z_j / N + Δ); for
+ * INVNORM_MID the midpoint shift 1/(2N) is composed with Δ:
+ * φ = Φ^{-1}(frac(n z_j/N + 1/(2N) + Δ)).  Only ζ (the circulant base) and
+ * φ(x_0) change, so independent shifts Δ_r give cheap randomised replicates
+ * and error bars.  Δ outside [0, 1) -> QMC_EINVAL_PHI.  With INVNORM_MID a Δ
+ * that puts a point exactly on 0 (Δ ≡ -(2i+1)/(2N) mod 1) makes that φ
+ * infinite; such Δ have measure zero and are not rejected. */
+int qmc_plan_create_shifted(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
+                            double delta, void* plan_ws, size_t plan_ws_bytes, void* stream);
+
 /* Polynomial lattice over F_2 (PAPER.md:456-459 Remark; reading R2/R3):
  * p has bit D set, 2 <= D <= 24, and must be primitive (checked on the
  * device: x has order 2^D-1); q_host: s values in [1, 2^D-1] (integer

@@ -22,6 +22,7 @@ with f=EXP: parity unpinned (no closed form).
 from __future__ import annotations
 
 import math
+from fractions import Fraction
 import statistics
 
 import numpy as np
@@ -38,7 +39,7 @@ __all__ = [
     "oracle_X_rows", "oracle_X_rows_fsum", "oracle_X_full", "column_means",
     "rowmean_relu", "row_sums",
     "pset_index_matrix", "pset_c", "pset_reordered_point",
-    "pde1d_fe_mean", "pde1d_lognormal_fe_mean",
+    "pde1d_fe_mean", "pde1d_lognormal_fe_mean", "phi_value_shifted", "phi_table_shifted",
 ]
 
 # φ enumeration (PAPER.md:295-302 names Φ^{-1}, the tent transform and the
@@ -245,6 +246,30 @@ def phi_value(phi: int, i: int, N: int) -> float:
     if phi == PHI_INVNORM_MID:
         return _ND.inv_cdf((2 * i + 1) / (2 * N))
     raise ValueError("unknown phi")
+
+
+def phi_value_shifted(phi: int, i: int, N: int, delta: float) -> float:
+    """φ at the point i/N of a rule shifted by the equal shift Δ
+    (PAPER.md:466-468): u = frac(i/N + Δ) (INVNORM_MID: frac(i/N + 1/(2N) +
+    Δ), its own midpoint shift composed with Δ); Δ = 0 is phi_value."""
+    if delta == 0.0:
+        return phi_value(phi, i, N)
+    u = Fraction(i, N) + (Fraction(1, 2 * N) if phi == PHI_INVNORM_MID else 0) + Fraction(delta)
+    u = float(u - math.floor(u))
+    if phi == PHI_IDENTITY:
+        return u
+    if phi == PHI_SHIFT_HALF:
+        return u - 0.5
+    if phi == PHI_TENT:
+        return 1.0 - abs(2.0 * u - 1.0)
+    if phi == PHI_INVNORM_MID:
+        return _ND.inv_cdf(u)
+    raise ValueError("unknown phi")
+
+
+def phi_table_shifted(phi: int, N: int, delta: float) -> np.ndarray:
+    """tab[i] = φ(frac(i/N + Δ)) (see phi_value_shifted)."""
+    return np.array([phi_value_shifted(phi, i, N, delta) for i in range(N)], dtype=np.float64)
 
 
 def phi_table(phi: int, N: int) -> np.ndarray:

@@ -24,7 +24,7 @@ EXPORTS = [
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
-    "qmc_fe1d_lognormal_solve_mean",
+    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted",
 ]
 
 
@@ -52,6 +52,7 @@ _sig = {
     "qmc_call_workspace_size": (_i32, [_vp, _i64, _i32, _PSZ]),
     "qmc_plan_create": (_i32, [C.POINTER(_vp), _i64, _i64, _P64, _i32, _vp, _sz, _vp]),
     "qmc_plan_create_poly": (_i32, [C.POINTER(_vp), _i32, C.c_uint64, _i64, _P64, _i32, _vp, _sz, _vp]),
+    "qmc_plan_create_shifted": (_i32, [C.POINTER(_vp), _i64, _i64, _P64, _i32, _d, _vp, _sz, _vp]),
     "qmc_matmul": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp]),
     "qmc_mean": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _i64, _vp, _sz, _vp]),
     "qmc_mean_finalize": (_i32, [_vp, _i32, _vp, _i64, _vp, _vp]),
@@ -120,6 +121,16 @@ def qmc_plan_create(N: int, s: int, z, phi: int, plan_ws, plan_ws_bytes: int, st
     assert len(arr) == s
     _check(_lib.qmc_plan_create(C.byref(h), N, s, p, phi, ptr(plan_ws), plan_ws_bytes, stream),
            "qmc_plan_create")
+    return h
+
+
+def qmc_plan_create_shifted(N: int, s: int, z, phi: int, delta: float, plan_ws, plan_ws_bytes: int,
+                            stream=None):
+    h = _vp()
+    arr, p = _i64arr(z)
+    assert len(arr) == s
+    _check(_lib.qmc_plan_create_shifted(C.byref(h), N, s, p, phi, delta, ptr(plan_ws), plan_ws_bytes, stream),
+           "qmc_plan_create_shifted")
     return h
 
 

@@ -60,7 +60,7 @@ def _stream(device) -> int:
 class Plan:
     """Fast QMC point-matrix operator Y (N × s) for one device."""
 
-    def __init__(self, family: int, N_or_D: int, z, phi: int, p: int = 0, device=None):
+    def __init__(self, family: int, N_or_D: int, z, phi: int, p: int = 0, device=None, delta: float = 0.0):
         if not torch.cuda.is_available():
             raise RuntimeError("libqmc needs a CUDA device (no CPU fallback)")
         self.device = torch.device(device if device is not None else "cuda")
@@ -70,7 +70,10 @@ class Plan:
         self.plan_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
         with torch.cuda.device(self.device):
             st = _stream(self.device)
-            if family == abi.QMC_FAMILY_LATTICE:
+            if family == abi.QMC_FAMILY_LATTICE and delta:
+                self.handle = abi.qmc_plan_create_shifted(N_or_D, self.s, z, phi, float(delta), self.plan_ws,
+                                                          nbytes, st)
+            elif family == abi.QMC_FAMILY_LATTICE:
                 self.handle = abi.qmc_plan_create(N_or_D, self.s, z, phi, self.plan_ws, nbytes, st)
             else:
                 self.handle = abi.qmc_plan_create_poly(N_or_D, p, self.s, z, phi, self.plan_ws, nbytes, st)
@@ -79,8 +82,9 @@ class Plan:
         self._ws = None
 
     @classmethod
-    def lattice(cls, N: int, z, phi: int, device=None) -> "Plan":
-        return cls(abi.QMC_FAMILY_LATTICE, N, z, phi, device=device)
+    def lattice(cls, N: int, z, phi: int, device=None, delta: float = 0.0) -> "Plan":
+        """Rank-1 lattice plan; delta != 0: every point shifted by the equal shift Δ."""
+        return cls(abi.QMC_FAMILY_LATTICE, N, z, phi, device=device, delta=delta)
 
     @classmethod
     def poly(cls, D: int, p: int, q, phi: int, device=None) -> "Plan":
@@ -180,3 +184,18 @@ class KorobovPSet:
                 Xg = buf[(g - 1) * (self.K - 1):]          # rows n = 0..K-1 of block g
                 abi.qmc_matmul(self.plans[g - 1].handle, A, lda, t, Xg, ldx, self._ws, self._ws.numel(), st)
         return buf[1:]
+
+
+def shifted_means(N: int, z, phi: int, A: torch.Tensor, f: int, f_param: float, deltas,
+                  device=None) -> tuple[torch.Tensor, torch.Tensor]:
+    """Randomised QMC: the fused means of f(X) over R
+    equally shifted copies of the rule (Δ_r in `deltas`).
+    Returns (per-replicate means R × t, their average over r).  The spread
+    over replicates is the usual error estimate; each replicate is one plan
+    (only ζ changes) and one fused qmc_mean call."""
+    outs = []
+    for d in deltas:
+        plan = Plan.lattice(N, z, phi, device=device, delta=float(d))
+        outs.append(plan.mean(A, f, f_param))
+    R = torch.stack(outs)
+    return R, R.mean(dim=0)

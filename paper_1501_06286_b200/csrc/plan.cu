@@ -199,13 +199,26 @@ __device__ __forceinline__ int64_t gf2_vd_index(uint64_t r, uint64_t p, int D) {
 }
 
 // φ(i/N) (INVNORM_MID per reading R6)
-__device__ __forceinline__ double phi_eval(int phi, int64_t i, int64_t N) {
-  const double u = double(i) / double(N);
+// φ at the grid point i/N, shifted by the equal shift Δ (
+// Δ = 0: the unshifted rule).  INVNORM_MID composes its own midpoint shift
+// 1/(2N) with Δ: Φ^{-1}(frac(i/N + 1/(2N) + Δ)).
+__device__ __forceinline__ double phi_eval(int phi, int64_t i, int64_t N, double delta) {
+  if (delta == 0.0) {
+    const double u = double(i) / double(N);
+    switch (phi) {
+      case QMC_PHI_IDENTITY: return u;
+      case QMC_PHI_SHIFT_HALF: return u - 0.5;
+      case QMC_PHI_TENT: return 1.0 - fabs(2.0 * u - 1.0);
+      default: return normcdfinv(double(2 * i + 1) / double(2 * N));
+    }
+  }
+  double u = double(i) / double(N) + (phi == QMC_PHI_INVNORM_MID ? 0.5 / double(N) : 0.0) + delta;
+  u -= floor(u);
   switch (phi) {
     case QMC_PHI_IDENTITY: return u;
     case QMC_PHI_SHIFT_HALF: return u - 0.5;
     case QMC_PHI_TENT: return 1.0 - fabs(2.0 * u - 1.0);
-    default: return normcdfinv(double(2 * i + 1) / double(2 * N));
+    default: return normcdfinv(u);
   }
 }
 
@@ -289,14 +302,14 @@ __global__ void k_rtable(const int32_t* __restrict__ L, int64_t N, int64_t m, in
   R[n] = n == 0 ? -1 : int32_t((m - L[n]) % m);
 }
 
-__global__ void k_zeta(int family, int phi, int64_t N, uint64_t p, int D, int64_t m,
+__global__ void k_zeta(int family, int phi, double delta, int64_t N, uint64_t p, int D, int64_t m,
                        const int32_t* __restrict__ P, double* __restrict__ zeta, double* __restrict__ scal) {
   const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (k == 0) scal[0] = phi_eval(phi, 0, N);
+  if (k == 0) scal[0] = phi_eval(phi, 0, N, delta);
   if (k >= m) return;
   const int64_t r = P[k];
   const int64_t idx = family == QMC_FAMILY_LATTICE ? r : gf2_vd_index(uint64_t(r), p, D);
-  zeta[k] = phi_eval(phi, idx, N);
+  zeta[k] = phi_eval(phi, idx, N, delta);
 }
 
 // tw[k] = ω_n^k = exp(-2πi k/n), k < count
@@ -424,7 +437,7 @@ static int validate_family(int family, int64_t N_or_D, int64_t s, int64_t* N, in
   return QMC_OK;
 }
 
-static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p, int64_t s,
+static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p, double delta, int64_t s,
                          const int64_t* z_host, int phi, void* plan_ws, size_t plan_ws_bytes,
                          void* stream) {
   if (!out) return QMC_ENULL;
@@ -449,6 +462,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   if (!pl) return QMC_ECUDA;
   pl->family = family;
   pl->phi = phi;
+  pl->delta = delta;
   pl->N = N;
   pl->m = m;
   pl->s = s;
@@ -562,7 +576,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   k_rtable<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, m, pl->d_R);
   QMC_PLAN_LAUNCHED();
   // a4
-  k_zeta<<<blocks(m, 256), 256, 0, st>>>(family, phi, N, p, pl->D, m, pl->d_P, pl->d_zeta, pl->d_scal);
+  k_zeta<<<blocks(m, 256), 256, 0, st>>>(family, phi, delta, N, p, pl->D, m, pl->d_P, pl->d_zeta, pl->d_scal);
   QMC_PLAN_LAUNCHED();
   k_twiddles<<<blocks(sp.L1, 256), 256, 0, st>>>(pl->d_tw1, sp.L1, sp.L1);
   QMC_PLAN_LAUNCHED();
@@ -616,12 +630,18 @@ int qmc_plan_workspace_size(int family, int64_t N_or_D, int64_t s, size_t* plan_
 
 int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
                     void* plan_ws, size_t plan_ws_bytes, void* stream) {
-  return create_common(out, QMC_FAMILY_LATTICE, N, 0, s, z_host, phi, plan_ws, plan_ws_bytes, stream);
+  return create_common(out, QMC_FAMILY_LATTICE, N, 0, 0.0, s, z_host, phi, plan_ws, plan_ws_bytes, stream);
+}
+
+int qmc_plan_create_shifted(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi, double delta,
+                            void* plan_ws, size_t plan_ws_bytes, void* stream) {
+  if (!(delta >= 0.0 && delta < 1.0)) return QMC_EINVAL_PHI;
+  return create_common(out, QMC_FAMILY_LATTICE, N, 0, delta, s, z_host, phi, plan_ws, plan_ws_bytes, stream);
 }
 
 int qmc_plan_create_poly(qmc_plan_t* out, int D, uint64_t p, int64_t s, const int64_t* q_host,
                          int phi, void* plan_ws, size_t plan_ws_bytes, void* stream) {
-  return create_common(out, QMC_FAMILY_POLY, D, p, s, q_host, phi, plan_ws, plan_ws_bytes, stream);
+  return create_common(out, QMC_FAMILY_POLY, D, p, 0.0, s, q_host, phi, plan_ws, plan_ws_bytes, stream);
 }
 
 int qmc_plan_info(qmc_plan_t pl, int64_t* info) {

@@ -78,6 +78,7 @@ inline int k2_split_R(int64_t L1) {
 struct qmc_plan {
   int family;
   int phi;
+  double delta;         // equal shift Δ of the rule (0: unshifted)
   int64_t N, m, s;
   int D;
   uint64_t p;

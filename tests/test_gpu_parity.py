@@ -381,3 +381,35 @@ def test_pde1d_lognormal_mean(qmc, N, M, s):
     Theta = X_full(w)
     uo = O.pde1d_lognormal_fe_mean(Theta, w.extra["psi0"])
     np.testing.assert_allclose(ubar, uo, rtol=1e-8, atol=0)
+
+
+# ------------------------------------------------------------------ equal shift (NEXT #4)
+@pytest.mark.parametrize("N,s,t,delta", [(13, 7, 3, 0.37), (257, 300, 64, 0.25), (65537, 64, 32, 0.0123456789),
+                                         (4001, 100, 9, 0.999)])
+@pytest.mark.parametrize("phi", [W.PHI_SHIFT_HALF, W.PHI_INVNORM_MID, W.PHI_TENT])
+def test_shifted_lattice(qmc, N, s, t, delta, phi):
+    import torch
+    w = W.custom_lattice(N, s, t, phi, seed=N + t)
+    plan = qmc.Plan.lattice(N, w.z, phi, delta=delta)
+    X = plan.matmul(qmc.to_device_colmajor(w.A, "cuda")).cpu().numpy()
+    torch.cuda.synchronize()
+    tab = O.phi_table_shifted(phi, N, delta)
+    Xo = O.oracle_X_full(index_fn(w), tab, N, w.A)
+    tol = 1e-11 * np.abs(w.A).sum(axis=0) * np.abs(tab).max()
+    assert np.all(np.abs(X - Xo).max(axis=0) <= tol)
+
+
+def test_shifted_replicate_means(qmc):
+    """R = 4 equally shifted replicates of config 3's affine mean (c + X): each
+    replicate's fused column means against the oracle's."""
+    import torch
+    N, s, t = 4001, 64, 8
+    w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=9)
+    deltas = [0.1, 0.35, 0.6, 0.85]
+    R, avg = qmc.shifted_means(N, w.z, W.PHI_SHIFT_HALF, qmc.to_device_colmajor(w.A, "cuda"),
+                               W.F_AFFINE, 1.0, deltas)
+    torch.cuda.synchronize()
+    for r, d in enumerate(deltas):
+        Xo = O.oracle_X_full(index_fn(w), O.phi_table_shifted(W.PHI_SHIFT_HALF, N, d), N, w.A)
+        np.testing.assert_allclose(R[r].cpu().numpy(), O.column_means(Xo, O.F_AFFINE, 1.0), rtol=0, atol=1e-12)
+    np.testing.assert_allclose(avg.cpu().numpy(), R.cpu().numpy().mean(axis=0), rtol=1e-15)

@@ -510,3 +510,41 @@ def test_pde1d_lognormal_psi_matrix():
     Psi, psi0 = W.pde1d_lognormal_matrix(6, 4)
     assert psi0 == 2.0 and Psi.shape == (4, 6)
     assert abs(Psi[2, 1] - 3 ** -1.5 * math.sin(2 * math.pi * 3 * 1.5 / 6)) < 1e-15
+
+
+# ---------------------------------------------------------------- equal shift (NEXT #4)
+@pytest.mark.parametrize("N,delta", [(7, 0.3), (13, 0.9), (101, 0.123456789), (257, 1e-3)])
+def test_shifted_column_sums_closed_form(N, delta):
+    """u - 1/2 on a rule shifted by Δ: every column is a permutation of the
+    shifted grid, so its sum is Σ_i (i/N + Δ) - #wraps - N/2 with
+    #wraps = #{i : i/N + Δ >= 1} = N - ceil(N(1 - Δ)) (closed form)."""
+    rng = np.random.default_rng(N)
+    z = rng.integers(1, N, size=5)
+    tab = O.phi_table_shifted(O.PHI_SHIFT_HALF, N, delta)
+    Y = O.point_matrix_rows(tab, O.lattice_index_matrix(N, z, np.arange(N)))
+    wraps = N - math.ceil(N * (1 - delta))
+    closed = (N - 1) / 2 + N * delta - wraps - N / 2
+    np.testing.assert_allclose(Y.sum(axis=0), closed, rtol=0, atol=1e-12 * N)
+
+
+def test_shift_half_cell_is_the_midpoint_rule():
+    """Δ = 1/(2N) with φ = identity gives the midpoints (2i+1)/(2N)."""
+    N = 31
+    tab = O.phi_table_shifted(O.PHI_IDENTITY, N, 1.0 / (2 * N))
+    np.testing.assert_allclose(tab, (2 * np.arange(N) + 1) / (2 * N), rtol=0, atol=1e-16)
+
+
+@pytest.mark.parametrize("N", [11, 61])
+def test_shift_by_grid_step_permutes_rows(N):
+    """Δ = k/N: column j of the shifted Y is column j of the unshifted Y with
+    row n moved to n - k·z_j^{-1} mod N ({(n z_j + k)/N} = {(n + k z_j^{-1}) z_j / N})."""
+    rng = np.random.default_rng(N + 5)
+    z = rng.integers(1, N, size=4)
+    k = 3
+    Ys = O.point_matrix_rows(O.phi_table_shifted(O.PHI_TENT, N, k / N),
+                             O.lattice_index_matrix(N, z, np.arange(N)))
+    Y = O.point_matrix_rows(O.phi_table(O.PHI_TENT, N), O.lattice_index_matrix(N, z, np.arange(N)))
+    for j, zj in enumerate(z):
+        zinv = pow(int(zj), N - 2, N)
+        perm = (np.arange(N) + k * zinv) % N
+        np.testing.assert_allclose(Ys[:, j], Y[perm, j], rtol=0, atol=1e-15)
