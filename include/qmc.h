@@ -67,7 +67,9 @@ enum { QMC_FAMILY_LATTICE = 0, QMC_FAMILY_POLY = 1 };
  * INVNORM_MID φ(u)=Φ^{-1}(u + 1/(2N)) — the paper's Φ^{-1} with the equal
  * shift Δ=1/(2N) it allows, finite at u=0 (reading R6).
  * Plain Φ^{-1} is not offered: Φ^{-1}(0) = -inf at row 0. */
-enum { QMC_PHI_IDENTITY = 0, QMC_PHI_SHIFT_HALF = 1, QMC_PHI_TENT = 2, QMC_PHI_INVNORM_MID = 3 };
+enum { QMC_PHI_IDENTITY = 0, QMC_PHI_SHIFT_HALF = 1, QMC_PHI_TENT = 2, QMC_PHI_INVNORM_MID = 3,
+       QMC_PHI_BERNOULLI2 = 4 /* B_2(u) = u^2 - u + 1/6: the kernel of the shift-averaged
+                                 worst-case error used by the CBC search (qmc_cbc_step) */ };
 
 /* fused downstream functional for qmc_mean (PAPER.md:60-62 eq_qmc) */
 enum {
@@ -189,6 +191,21 @@ int qmc_tridiag_solve_mean(int64_t N, int64_t K, double d0, double e0, const dou
  * NULL for ĝ = 1.  Asynchronous on `stream`. */
 int qmc_fe1d_lognormal_solve_mean(int64_t N, int64_t M, double psi0, const double* rhs, double* X,
                                   int64_t ldx, double* mean_out, void* stream);
+
+/* One step of the component-by-component construction of z (SURVEY §8(f)
+ * NEXT #4; fast CBC, cited but not restated by the paper):
+ * criterion e² = -1 + (1/N) Σ_n Π_j (1 + γ_j 2π² B_2({n z_j/N})) (weighted
+ * Korobov space, product weights, shift-averaged worst case).  crit (device,
+ * N doubles): crit[z] = Σ_{n>=1} B_2({n z/N}) p_n, i.e. X of qmc_matmul for
+ * the plan with generating vector (1, 2, ..., N-1), φ = QMC_PHI_BERNOULLI2 and
+ * A = p_1..p_{N-1} (the fast product of this library; the n = 0 term is the
+ * same for every z).  Picks z_d = argmin_{1 <= z <= zmax} crit[z] (smallest z
+ * among equal values), stores it to z_out[d] (device int64) and updates p
+ * (device, N doubles) to p_n (1 + γ 2π² B_2({n z_d/N})).  Start with p = 1;
+ * zmax = 1 fixes z_1 = 1; zmax = (N-1)/2 uses the symmetry crit[z] =
+ * crit[N-z].  Asynchronous on `stream`. */
+int qmc_cbc_step(int64_t N, const double* crit, int64_t zmax, double gamma, double* p, int64_t* z_out,
+                 int64_t d, void* stream);
 
 /* Plan facts: info[0..11] = family, N, m, s, phi, generator (β or the
  * encoding of x = 2), L (FFT length; L = m or padded L >= 2m-1), L1, L2,

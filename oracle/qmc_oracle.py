@@ -28,7 +28,7 @@ import statistics
 import numpy as np
 
 __all__ = [
-    "PHI_IDENTITY", "PHI_SHIFT_HALF", "PHI_TENT", "PHI_INVNORM_MID",
+    "PHI_IDENTITY", "PHI_SHIFT_HALF", "PHI_TENT", "PHI_INVNORM_MID", "PHI_BERNOULLI2",
     "F_IDENTITY", "F_AFFINE", "F_EXP",
     "is_prime", "prime_factors", "primitive_root", "power_table", "log_table",
     "column_exponents",
@@ -40,6 +40,7 @@ __all__ = [
     "rowmean_relu", "row_sums",
     "pset_index_matrix", "pset_c", "pset_reordered_point",
     "pde1d_fe_mean", "pde1d_lognormal_fe_mean", "phi_value_shifted", "phi_table_shifted",
+    "cbc_criterion_table", "cbc_lattice", "cbc_error",
 ]
 
 # φ enumeration (PAPER.md:295-302 names Φ^{-1}, the tent transform and the
@@ -51,6 +52,7 @@ PHI_IDENTITY = 0
 PHI_SHIFT_HALF = 1
 PHI_TENT = 2
 PHI_INVNORM_MID = 3
+PHI_BERNOULLI2 = 4   # B_2(u) = u^2 - u + 1/6 (CBC worst-case error kernel)
 
 # downstream f for the QMC mean (1/N) Σ_n f(b_n)
 F_IDENTITY = 0
@@ -245,6 +247,9 @@ def phi_value(phi: int, i: int, N: int) -> float:
         return 1.0 - abs(2.0 * (i / N) - 1.0)
     if phi == PHI_INVNORM_MID:
         return _ND.inv_cdf((2 * i + 1) / (2 * N))
+    if phi == PHI_BERNOULLI2:
+        u = Fraction(i, N)
+        return float(u * u - u + Fraction(1, 6))
     raise ValueError("unknown phi")
 
 
@@ -264,6 +269,8 @@ def phi_value_shifted(phi: int, i: int, N: int, delta: float) -> float:
         return 1.0 - abs(2.0 * u - 1.0)
     if phi == PHI_INVNORM_MID:
         return _ND.inv_cdf(u)
+    if phi == PHI_BERNOULLI2:
+        return u * u - u + 1.0 / 6.0
     raise ValueError("unknown phi")
 
 
@@ -482,3 +489,44 @@ def pde1d_lognormal_fe_mean(Theta: np.ndarray, psi0: float, rhs: np.ndarray | No
         ab[2, :-1] = off
         U[n] = solve_banded((1, 1), ab, g)
     return np.array([math.fsum(U[:, k]) / N for k in range(K)])
+
+
+# ---------------------------------------------------------------- CBC
+def cbc_criterion_table(N: int) -> np.ndarray:
+    """B_2(i/N) = (i/N)^2 - i/N + 1/6, i = 0..N-1 (exact rationals, rounded once)."""
+    return np.array([float(Fraction(i, N) ** 2 - Fraction(i, N) + Fraction(1, 6)) for i in range(N)])
+
+
+def cbc_lattice(N: int, s: int, gamma) -> np.ndarray:
+    """Component-by-component construction, plain form (no FFT): z_1 = 1; for
+    d >= 2, z_d = argmin over z = 1..(N-1)/2 (first minimum) of
+    Σ_{n>=1} B_2({n z/N}) p_n, with p_n = Π_{j<d} (1 + γ_j 2π² B_2({n z_j/N}))
+    (shift-averaged worst-case error, weighted Korobov space, product
+    weights; see libqmc's qmc_cbc_step)."""
+    gam = np.broadcast_to(np.asarray(gamma, dtype=np.float64), (s,))
+    B = cbc_criterion_table(N)
+    n = np.arange(N, dtype=np.int64)
+    p = np.ones(N)
+    cand = np.arange(1, (N - 1) // 2 + 1, dtype=np.int64)
+    z = np.zeros(s, dtype=np.int64)
+    for d in range(s):
+        if d == 0:
+            zd = 1
+        else:
+            crit = B[(n[1:, None] * cand[None, :]) % N].T @ p[1:]
+            zd = int(cand[np.argmin(crit)])
+        z[d] = zd
+        p = p * (1.0 + gam[d] * 2 * math.pi ** 2 * B[(n * zd) % N])
+    return z
+
+
+def cbc_error(N: int, z, gamma) -> float:
+    """e²(z) = -1 + (1/N) Σ_n Π_j (1 + γ_j 2π² B_2({n z_j/N})) (fsum)."""
+    z = np.asarray(z, dtype=np.int64)
+    gam = np.broadcast_to(np.asarray(gamma, dtype=np.float64), (len(z),))
+    B = cbc_criterion_table(N)
+    n = np.arange(N, dtype=np.int64)
+    p = np.ones(N)
+    for j, zj in enumerate(z):
+        p = p * (1.0 + gam[j] * 2 * math.pi ** 2 * B[(n * int(zj)) % N])
+    return math.fsum(p) / N - 1.0

@@ -15,7 +15,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libqmc.so")
 
 QMC_FAMILY_LATTICE, QMC_FAMILY_POLY = 0, 1
-QMC_PHI_IDENTITY, QMC_PHI_SHIFT_HALF, QMC_PHI_TENT, QMC_PHI_INVNORM_MID = 0, 1, 2, 3
+QMC_PHI_IDENTITY, QMC_PHI_SHIFT_HALF, QMC_PHI_TENT, QMC_PHI_INVNORM_MID, QMC_PHI_BERNOULLI2 = 0, 1, 2, 3, 4
 QMC_F_IDENTITY, QMC_F_AFFINE, QMC_F_EXP, QMC_F_ROWMEAN_RELU = 0, 1, 2, 3
 QMC_F_NONE = -1  # workspace query for qmc_matmul
 
@@ -24,7 +24,7 @@ EXPORTS = [
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
-    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted",
+    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step",
 ]
 
 
@@ -60,6 +60,7 @@ _sig = {
     "qmc_plan_info": (_i32, [_vp, _P64]),
     "qmc_tridiag_solve_mean": (_i32, [_i64, _i64, _d, _d, _vp, _vp, _i64, _vp, _vp]),
     "qmc_fe1d_lognormal_solve_mean": (_i32, [_i64, _i64, _d, _vp, _vp, _i64, _vp, _vp]),
+    "qmc_cbc_step": (_i32, [_i64, _vp, _i64, _d, _vp, _vp, _i64, _vp]),
     "qmc_plan_tables": (_i32, [_vp, _P64, _P32, _P32, _P32, _PD]),
     "qmc_launch_count": (_i64, []),
     "qmc_plan_destroy": (None, [_vp]),
@@ -173,6 +174,10 @@ def qmc_tridiag_solve_mean(N: int, K: int, d0: float, e0: float, rhs, X, ldx: in
 def qmc_fe1d_lognormal_solve_mean(N: int, M: int, psi0: float, rhs, X, ldx: int, mean_out, stream=None):
     _check(_lib.qmc_fe1d_lognormal_solve_mean(N, M, psi0, ptr(rhs), ptr(X), ldx, ptr(mean_out), stream),
            "qmc_fe1d_lognormal_solve_mean")
+
+
+def qmc_cbc_step(N: int, crit, zmax: int, gamma: float, p, z_out, d: int, stream=None):
+    _check(_lib.qmc_cbc_step(N, ptr(crit), zmax, gamma, ptr(p), ptr(z_out), d, stream), "qmc_cbc_step")
 
 
 def qmc_plan_info(plan) -> dict:

@@ -14,7 +14,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libqmc.so")
-SOURCES = ["plan.cu", "pipeline.cu", "pde.cu"]
+SOURCES = ["plan.cu", "pipeline.cu", "pde.cu", "cbc.cu"]
 HEADERS = ["fft.cuh", "qmc_internal.cuh", "rowcfg.cuh"]
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

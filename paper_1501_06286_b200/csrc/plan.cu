@@ -209,6 +209,7 @@ __device__ __forceinline__ double phi_eval(int phi, int64_t i, int64_t N, double
       case QMC_PHI_IDENTITY: return u;
       case QMC_PHI_SHIFT_HALF: return u - 0.5;
       case QMC_PHI_TENT: return 1.0 - fabs(2.0 * u - 1.0);
+      case QMC_PHI_BERNOULLI2: return u * u - u + 1.0 / 6.0;
       default: return normcdfinv(double(2 * i + 1) / double(2 * N));
     }
   }
@@ -218,6 +219,7 @@ __device__ __forceinline__ double phi_eval(int phi, int64_t i, int64_t N, double
     case QMC_PHI_IDENTITY: return u;
     case QMC_PHI_SHIFT_HALF: return u - 0.5;
     case QMC_PHI_TENT: return 1.0 - fabs(2.0 * u - 1.0);
+    case QMC_PHI_BERNOULLI2: return u * u - u + 1.0 / 6.0;
     default: return normcdfinv(u);
   }
 }
@@ -443,7 +445,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   if (!out) return QMC_ENULL;
   *out = nullptr;
   if (!z_host || !plan_ws) return QMC_ENULL;
-  if (phi < QMC_PHI_IDENTITY || phi > QMC_PHI_INVNORM_MID) return QMC_EINVAL_PHI;
+  if (phi < QMC_PHI_IDENTITY || phi > QMC_PHI_BERNOULLI2) return QMC_EINVAL_PHI;
   int64_t N, m;
   int rc = validate_family(family, N_or_D, s, &N, &m);
   if (rc) return rc;

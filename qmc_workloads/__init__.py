@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 # ABI numbering of φ and of the fused f (restated; see include/qmc.h)
-PHI_IDENTITY, PHI_SHIFT_HALF, PHI_TENT, PHI_INVNORM_MID = 0, 1, 2, 3
+PHI_IDENTITY, PHI_SHIFT_HALF, PHI_TENT, PHI_INVNORM_MID, PHI_BERNOULLI2 = 0, 1, 2, 3, 4
 F_IDENTITY, F_AFFINE, F_EXP, F_ROWMEAN_RELU = 0, 1, 2, 3
 
 FAMILY_LATTICE = "lattice"

@@ -413,3 +413,28 @@ def test_shifted_replicate_means(qmc):
         Xo = O.oracle_X_full(index_fn(w), O.phi_table_shifted(W.PHI_SHIFT_HALF, N, d), N, w.A)
         np.testing.assert_allclose(R[r].cpu().numpy(), O.column_means(Xo, O.F_AFFINE, 1.0), rtol=0, atol=1e-12)
     np.testing.assert_allclose(avg.cpu().numpy(), R.cpu().numpy().mean(axis=0), rtol=1e-15)
+
+
+# ------------------------------------------------------------------ CBC (NEXT #4)
+@pytest.mark.parametrize("N,s", [(101, 6), (1021, 12), (4001, 8)])
+def test_cbc_lattice_gpu(qmc, N, s):
+    """GPU fast CBC (qmc_matmul with φ = B_2 + qmc_cbc_step) is a valid CBC
+    run: along the GPU's own choices, every z_d attains the minimum of the
+    oracle's plain step-d criterion (to fp tolerance; exact ties z <-> z^{-1}
+    make several choices valid), z_1 = 1, and the worst-case error matches the
+    oracle's CBC vector's when the vectors coincide."""
+    gam = [0.9 ** (j + 1) for j in range(s)]
+    zg = qmc.cbc_lattice(N, s, gam)
+    assert zg[0] == 1 and np.all((zg >= 1) & (zg <= (N - 1) // 2))
+    B = O.cbc_criterion_table(N)
+    n = np.arange(N, dtype=np.int64)
+    cand = np.arange(1, (N - 1) // 2 + 1, dtype=np.int64)
+    p = np.ones(N)
+    for d in range(s):
+        if d > 0:
+            crit = B[(n[1:, None] * cand[None, :]) % N].T @ p[1:]
+            assert crit[zg[d] - 1] <= crit.min() + 1e-12 * np.abs(crit).max()
+        p = p * (1.0 + gam[d] * 2 * np.pi ** 2 * B[(n * int(zg[d])) % N])
+    zo = O.cbc_lattice(N, s, gam)
+    if np.array_equal(zo, zg):
+        assert abs(O.cbc_error(N, zg, gam) - O.cbc_error(N, zo, gam)) == 0.0

@@ -548,3 +548,44 @@ def test_shift_by_grid_step_permutes_rows(N):
         zinv = pow(int(zj), N - 2, N)
         perm = (np.arange(N) + k * zinv) % N
         np.testing.assert_allclose(Ys[:, j], Y[perm, j], rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------- CBC (NEXT #4)
+@pytest.mark.parametrize("N", [7, 101, 1021])
+def test_cbc_error_one_dimension_closed_form(N):
+    """d = 1, z = 1: Σ_i B_2(i/N) = 1/(6N), so e² = γ 2π²/(6N²) = γ π²/(3N²)."""
+    g = 0.7
+    assert abs(O.cbc_error(N, [1], g) - g * math.pi ** 2 / (3 * N * N)) <= 1e-14
+
+
+def test_cbc_criterion_symmetry_exact():
+    """B_2(1 - u) = B_2(u), so the criterion of z and N - z coincide exactly:
+    the candidate range 1..(N-1)/2 loses nothing (exact rationals)."""
+    N = 13
+    rng = np.random.default_rng(1)
+    p = [Fraction(int(v), 7) for v in rng.integers(1, 20, size=N)]
+    def crit(z):
+        return sum(p[n] * (Fraction(n * z % N, N) ** 2 - Fraction(n * z % N, N) + Fraction(1, 6)) for n in range(1, N))
+    for z in range(1, N):
+        assert crit(z) == crit(N - z)
+
+
+@pytest.mark.parametrize("N,s", [(13, 4), (17, 5), (31, 4)])
+def test_cbc_choices_are_exact_minimisers(N, s):
+    """Each z_d of the oracle's CBC attains, in exact rational arithmetic, the
+    minimum of the step-d criterion, for rational weights γ_j = 1/j².  (Exact
+    ties occur: from step 2 the criterion is invariant under z -> z^{-1} mod N
+    for the z_1 = 1 prefix, e.g. 12 and 13 for N = 31; any minimiser is a
+    valid CBC choice.)"""
+    gam = [Fraction(1, (j + 1) ** 2) for j in range(s)]
+    z = O.cbc_lattice(N, s, [float(g) for g in gam])
+    assert z[0] == 1
+    B = [Fraction(i, N) ** 2 - Fraction(i, N) + Fraction(1, 6) for i in range(N)]
+    pi2 = Fraction(math.pi ** 2)   # the update uses the float 2π²; its exact value cancels in the argmin
+    p = [Fraction(1)] * N
+    for d in range(s):
+        if d > 0:
+            crits = {zc: sum(p[n] * B[n * zc % N] for n in range(1, N)) for zc in range(1, (N - 1) // 2 + 1)}
+            best = min(crits.values())
+            assert crits[int(z[d])] == best
+        p = [p[n] * (1 + gam[d] * 2 * pi2 * B[n * int(z[d]) % N]) for n in range(N)]
