@@ -100,7 +100,10 @@ enum {
 int qmc_plan_workspace_size(int family, int64_t N_or_D, int64_t s, size_t* plan_bytes);
 
 /* Bytes of device scratch one qmc_matmul / qmc_mean call on t columns
- * needs (call_ws).  Independent of A and X. */
+ * needs (call_ws).  Independent of A and X.  Dominated by U, the batch's
+ * row-FFT output (two sets of up to ~768 MB); for ROWMEAN_RELU add one
+ * N-vector of partial row sums per group of 16 column pairs
+ * (8·N·ceil(t/32) bytes). */
 int qmc_call_workspace_size(qmc_plan_t plan, int64_t t, int f, size_t* call_bytes);
 
 /* Rank-1 lattice plan.  N prime, 3 <= N < 2^31;
