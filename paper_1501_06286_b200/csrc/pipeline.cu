@@ -647,7 +647,10 @@ __device__ __forceinline__ void k2_issue(const K2Args& a, int tile, double2* dst
   for (int i = threadIdx.x; i < L1 * CB; i += NT) {
     const int e1 = i / CB, cc = i - e1 * CB;
     const int64_t ii = int64_t(a.L2) * e1 + bx * CB + cc;
-    cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
+    if (ii < a.m)
+      cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
+    else
+      nd[i] = -1;  // zero-padded correlation: not a row of X
   }
 }
 
@@ -702,11 +705,19 @@ __device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2
   const int* nr = nS + c;
   double r[L1];
 #pragma unroll
-  for (int e1 = 0; e1 < L1; ++e1) emit_fast<EP>(E, v[e1], nr[e1 * CB], xk, acc, r[e1]);
+  for (int e1 = 0; e1 < L1; ++e1) {
+    const int n = nr[e1 * CB];  // -1: padding row (uniform over the 16 lanes of the row)
+    if (n >= 0) {
+      emit_fast<EP>(E, v[e1], n, xk, acc, r[e1]);
+    } else {
+      r[e1] = 0.0;
+    }
+  }
   if constexpr (EP == EPK_ROWSUM) {
     static_assert(EP != EPK_ROWSUM || L1 == 16, "row sums of the pipelined K2 need L1 = 16");
     const double sum = rowsum_butterfly16(r);
-    rowpart[nr[(tid & 15) * CB]] = sum;
+    const int n = nr[(tid & 15) * CB];
+    if (n >= 0) rowpart[n] = sum;
   } else {
     if (a.part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
 #pragma unroll
@@ -964,8 +975,11 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   // fast path: whole pair groups, whole pairs, vector X stores, no padded rows
   const bool fast = R == 1 && np % cl.PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L == pl->m &&
                     (pl->sp.L2 % ((R == 1 ? kColThreads : 32) / cl.PG)) == 0;
+  // the pipelined kernel also takes zero-padded lengths (rows i >= m skipped)
+  const bool fastp = R == 1 && np % cl.PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) &&
+                     (pl->sp.L2 % ((R == 1 ? kColThreads : 32) / cl.PG)) == 0;
   if constexpr (R == 1 && (EP != EPK_ROWSUM || L1 == 16)) {
-    if (fast && cl.PG == 16 && !getenv("QMC_K2_NOPIPE")) {
+    if (fastp && cl.PG == 16 && !getenv("QMC_K2_NOPIPE")) {
       constexpr int CBP = QMC_K2_CB;
       constexpr size_t psm = cols_pipe_smem<L1, CBP>();
       auto pk = k_cols_pipe<L1, EP, CBP>;

@@ -596,11 +596,12 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
 #undef QMC_PLAN_LAUNCHED
   pl->nstreams = 1;
   pl->mu = new (std::nothrow) std::mutex();
-  // two internal streams overlap consecutive batches; with rows of 8192 (one
-  // K1 CTA per SM) that overlap measured slower on B200 (config 5: 119 vs
-  // 111 ms/step), so those plans run their batches on the caller's stream
+  // two internal streams overlap consecutive batches; when the column pass
+  // needs the two-stage (non-persistent) K2 (L1 > 16) that overlap measured
+  // slower on B200 (config 5: 119 vs 111 ms/step; config 4, L1 = 16: 2.55 vs
+  // 2.63 ms with two), so those plans run their batches on the caller's stream
   const char* one = getenv("QMC_ONE_STREAM");
-  const bool want2 = one ? one[0] != '1' : sp.L2 < 8192;
+  const bool want2 = one ? one[0] != '1' : sp.L1 <= 16;
   if (want2 && pl->mu &&
       cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
       cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
