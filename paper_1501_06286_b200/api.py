@@ -10,6 +10,8 @@ either is a view.  ``to_device_colmajor`` / ``x_empty`` build such tensors.
 """
 from __future__ import annotations
 
+import sys
+
 import numpy as np
 import torch
 
@@ -138,7 +140,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None:
+        if h is not None and not sys.is_finalizing():
             abi.qmc_plan_destroy(h)
             self.handle = None
 

@@ -609,6 +609,9 @@ constexpr int kPipeStages = QMC_K2_STAGES;
 #ifndef QMC_K2_CB
 #define QMC_K2_CB 8
 #endif
+#ifndef QMC_K2_MINB
+#define QMC_K2_MINB 1
+#endif
 template <int L1, int CB>
 __host__ __device__ constexpr int pipe_pair_stride() { return (CB / kUB) * L1 * kUB + 1; }
 template <int L1, int CB>
@@ -739,7 +742,7 @@ __device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2
 }
 
 template <int L1, int EP, int CB>
-__global__ void __launch_bounds__(16 * CB, 1) k_cols_pipe(K2Args a) {
+__global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
   constexpr int NT = 16 * CB;
   constexpr int STAGE = 16 * pipe_pair_stride<L1, CB>();
   extern __shared__ double2 sm[];
