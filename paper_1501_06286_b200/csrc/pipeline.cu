@@ -129,7 +129,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // shared memory of K1: the padded row, then the staging of CH entries
 template <int L2>
 __host__ __device__ constexpr size_t rows_smem(int CH) {
-  return size_t(PadE<L2, QMC_ROW_E>::size) * 16 + size_t(CH) * (16 + 16 + 4);
+  return size_t(PadE<L2, QMC_ROW_E>::size) * 16 + size_t(CH) * (16 + 16 + 4) + 16;
 }
 
 struct K1Args {
@@ -150,40 +150,68 @@ struct K1Args {
 
 template <int L2>
 struct K1Smem {
-  double2* S;    // padded row
-  double2* stA;  // staging: a
-  double2* stW;  // staging: twiddles
-  int32_t* stE;  // staging: e2q
+  double2* S;     // padded row
+  double2* stA;   // staging: a
+  double2* stW;   // staging: twiddles
+  int32_t* stE;   // staging: e2q
+  uint64_t* bar;  // staging complete (one phase per chunk)
   __device__ K1Smem(double2* base, int CH)
-      : S(base), stA(base + PadE<L2, QMC_ROW_E>::size), stW(stA + CH), stE(reinterpret_cast<int32_t*>(stW + CH)) {}
+      : S(base),
+        stA(base + PadE<L2, QMC_ROW_E>::size),
+        stW(stA + CH),
+        stE(reinterpret_cast<int32_t*>(stW + CH)),
+        bar(reinterpret_cast<uint64_t*>(stE + CH)) {}
 };
 
-// stage chunk c of item it (all threads issue, one commit group)
+// mbarrier + bulk async copy (the staging of K1's scatter input)
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// stage chunk c of item it: three bulk async copies issued by one thread
+// (a of the pair, twiddles of f1, bucket codes), completing on sm.bar.  The
+// staging buffers must be free.  The e2q copy is rounded up to 16 bytes (CH
+// is a multiple of 32; the plan table after e2q absorbs the overread).
 template <int L2>
 __device__ __forceinline__ void k1_issue(const K1Args& a, const K1Smem<L2>& sm, int it, int c) {
-  constexpr int NT = L2 / QMC_ROW_E;
   const int f1 = it % a.L1, p = it / a.L1;
   const int64_t q0 = int64_t(c) * a.CH;
   const int n = int(a.CH < a.s - q0 ? a.CH : a.s - q0);
-  const double2* ga = a.asort + int64_t(p) * a.s + q0 + threadIdx.x;
-  const double2* gw = a.twj + int64_t(f1) * a.s + q0 + threadIdx.x;
-  const int32_t* ge = a.e2q + q0 + threadIdx.x;
-  double2* sa = sm.stA + threadIdx.x;
-  double2* sw = sm.stW + threadIdx.x;
-  int32_t* se = sm.stE + threadIdx.x;
-  for (int i = threadIdx.x; i < n; i += NT, ga += NT, gw += NT, ge += NT, sa += NT, sw += NT, se += NT) {
-    cp_async16(sa, ga);
-    cp_async16(sw, gw);
-    cp_async4(se, ge);
-  }
-  cp_async_commit();
+  const unsigned b16 = unsigned(n) * 16u, b4 = unsigned((n + 3) & ~3) * 4u;
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reads before the async writes
+  mbar_expect_tx(sm.bar, 2 * b16 + b4);
+  bulk_g2s(sm.stA, a.asort + int64_t(p) * a.s + q0, b16, sm.bar);
+  bulk_g2s(sm.stW, a.twj + int64_t(f1) * a.s + q0, b16, sm.bar);
+  bulk_g2s(sm.stE, a.e2q + q0, b4, sm.bar);
 }
 
 // One K1 item (f1, pair); its chunk 0 must have been issued.  next >= 0: the
 // item whose chunk 0 is issued once this item's staging is consumed (it then
 // overlaps this item's FFTs).
 template <int L2>
-__device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, int item, int next) {
+__device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, unsigned& phase, int item, int next) {
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
   double2* S = sm.S;
@@ -193,8 +221,9 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, i
   const int nch = int((a.s + a.CH - 1) / a.CH);
   QMC_TS(0);
   for (int c = 0; c < nch; ++c) {
-    cp_async_wait_all();
-    __syncthreads();  // staging complete; every use of S by the previous item is done
+    mbar_wait(sm.bar, phase);
+    phase ^= 1u;
+    __syncthreads();  // every use of S by the previous item is done
     // scatter a' = P a fused with the first DFT dimension:
     //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
     // The first entry of a bucket (size in e2q >> 13) sums it in j order and
@@ -220,10 +249,11 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, i
       S[padE<E>(pk & 8191)] = cadd(S[padE<E>(pk & 8191)], acc);
     }
     __syncthreads();  // staging consumed
-    if (c + 1 < nch) {
-      k1_issue<L2>(a, sm, item, c + 1);
-    } else if (next >= 0) {
-      k1_issue<L2>(a, sm, next, 0);  // overlaps this item's FFTs
+    if (tid == 0) {
+      if (c + 1 < nch)
+        k1_issue<L2>(a, sm, item, c + 1);
+      else if (next >= 0)
+        k1_issue<L2>(a, sm, next, 0);  // overlaps this item's FFTs
     }
   }
   QMC_TS(1);
@@ -262,10 +292,12 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
   extern __shared__ double2 smem[];
   const K1Smem<L2> sm(smem, a.CH);
   const int nitems = a.L1 * a.np;
-  if (int(blockIdx.x) < nitems) k1_issue<L2>(a, sm, blockIdx.x, 0);
+  if (threadIdx.x == 0) mbar_init(sm.bar, 1);
+  __syncthreads();
+  if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sm, blockIdx.x, 0);
+  unsigned phase = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x)
-    k1_item<L2>(a, sm, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1);
-  cp_async_wait_all();
+    k1_item<L2>(a, sm, phase, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1);
 }
 
 // ---------------------------------------------------------------- K2
