@@ -74,17 +74,18 @@ __device__ __forceinline__ double2 block_sum2(double2 v, double2* red) {
 }
 
 // ---------------------------------------------------------------- K0
-// a of the batch in bucket order: asort[p·s + q] = (A[j_q, k1], A[j_q, k2]),
-// j_q = bent[q].x (the entries of one bucket e2 = e_j mod L2 are adjacent,
-// in increasing j)
+// a of the batch in the K1 order: asort[p·S1 + q] = (A[j_q, k1], A[j_q, k2]),
+// j_q = jq[q] (plan.cu k1_balanced_order; bucket order as fallback), zero for
+// padding slots (j_q = -1)
 __global__ void k_pack(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0, int np,
-                       const int4* __restrict__ bent, int64_t s, double2* __restrict__ asort) {
+                       const int32_t* __restrict__ jq, int64_t S1, double2* __restrict__ asort) {
   const int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int p = blockIdx.y;
-  if (q >= s || p >= np) return;
+  if (q >= S1 || p >= np) return;
   const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-  const int64_t j = __ldg(&bent[q].x);
-  asort[int64_t(p) * s + q] = make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
+  const int64_t j = __ldg(&jq[q]);
+  asort[int64_t(p) * S1 + q] = j < 0 ? make_double2(0.0, 0.0)
+                                     : make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
 }
 
 // ---------------------------------------------------------------- K1
@@ -126,19 +127,23 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
-// shared memory of K1: the padded row, then the staging of CH entries
+// shared memory of K1: the padded row with its padding and overflow slots
+// (k1_row_slots), the staging of CH slots (CH a multiple of 4), the staging
+// mbarrier
 template <int L2>
 __host__ __device__ constexpr size_t rows_smem(int CH) {
-  return size_t(PadE<L2, QMC_ROW_E>::size) * 16 + size_t(CH) * (16 + 16 + 4) + 16;
+  return size_t(k1_row_slots(L2, QMC_ROW_E)) * 16 + size_t(CH) * (16 + 16 + 4) + 16;
 }
 
 struct K1Args {
-  const double2* __restrict__ asort;   // [np][s] a in bucket order (K0)
-  const int32_t* __restrict__ e2q;     // [s]
+  const double2* __restrict__ asort;   // [np][S1] a in the K1 order (K0)
+  const int32_t* __restrict__ e2q;     // [S1] bucket codes
   const uint32_t* __restrict__ occ;    // nonempty buckets
-  int64_t s;
-  int CH;                              // staging entries per chunk
-  const double2* __restrict__ twj;     // [L1][s]
+  int64_t S1;
+  int CH;                              // staging slots (capacity)
+  const int32_t* __restrict__ k1c;     // [nch+1] chunk starts, [nch] regular-round slots
+  int nch, bal;
+  const double2* __restrict__ twj;     // [L1][S1]
   const double2* __restrict__ tws;     // row-FFT stage twiddles
   const double2* __restrict__ W;       // [L1][L2] spectrum
   double2* __restrict__ U;             // [np][L] blocked
@@ -157,7 +162,7 @@ struct K1Smem {
   uint64_t* bar;  // staging complete (one phase per chunk)
   __device__ K1Smem(double2* base, int CH)
       : S(base),
-        stA(base + PadE<L2, QMC_ROW_E>::size),
+        stA(base + k1_row_slots(L2, QMC_ROW_E)),
         stW(stA + CH),
         stE(reinterpret_cast<int32_t*>(stW + CH)),
         bar(reinterpret_cast<uint64_t*>(stE + CH)) {}
@@ -192,18 +197,17 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
 
 // stage chunk c of item it: three bulk async copies issued by one thread
 // (a of the pair, twiddles of f1, bucket codes), completing on sm.bar.  The
-// staging buffers must be free.  The e2q copy is rounded up to 16 bytes (CH
-// is a multiple of 32; the plan table after e2q absorbs the overread).
+// staging buffers must be free.  Chunk starts are multiples of 4 slots; the
+// e2q copy is rounded up to 16 bytes (the table has 16 bytes of slack).
 template <int L2>
 __device__ __forceinline__ void k1_issue(const K1Args& a, const K1Smem<L2>& sm, int it, int c) {
   const int f1 = it % a.L1, p = it / a.L1;
-  const int64_t q0 = int64_t(c) * a.CH;
-  const int n = int(a.CH < a.s - q0 ? a.CH : a.s - q0);
+  const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
   const unsigned b16 = unsigned(n) * 16u, b4 = unsigned((n + 3) & ~3) * 4u;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reads before the async writes
   mbar_expect_tx(sm.bar, 2 * b16 + b4);
-  bulk_g2s(sm.stA, a.asort + int64_t(p) * a.s + q0, b16, sm.bar);
-  bulk_g2s(sm.stW, a.twj + int64_t(f1) * a.s + q0, b16, sm.bar);
+  bulk_g2s(sm.stA, a.asort + int64_t(p) * a.S1 + q0, b16, sm.bar);
+  bulk_g2s(sm.stW, a.twj + int64_t(f1) * a.S1 + q0, b16, sm.bar);
   bulk_g2s(sm.stE, a.e2q + q0, b4, sm.bar);
 }
 
@@ -218,7 +222,7 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
   const int tid = threadIdx.x;
   const int L1 = a.L1;
   const int f1 = item % L1, p = item / L1;
-  const int nch = int((a.s + a.CH - 1) / a.CH);
+  const int nch = a.nch;
   QMC_TS(0);
   for (int c = 0; c < nch; ++c) {
     mbar_wait(sm.bar, phase);
@@ -226,27 +230,52 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
     __syncthreads();  // every use of S by the previous item is done
     // scatter a' = P a fused with the first DFT dimension:
     //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
-    // The first entry of a bucket (size in e2q >> 13) sums it in j order and
-    // stores T (S holds the previous item's data elsewhere: only nonempty
-    // buckets are read back, by the occupancy mask); a bucket continued from
-    // the previous chunk is added to by this chunk's entry 0.
-    const int n = int(a.CH < a.s - int64_t(c) * a.CH ? a.CH : a.s - int64_t(c) * a.CH);
-    for (int i = tid; i < n; i += NT) {
-      const int pk = sm.stE[i];
-      const int len = pk >> 13, e2 = pk & 8191;
-      double2 acc = cmul(sm.stA[i], sm.stW[i]);
-      const int end = min(n, i + len);
-      for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));  // collisions (rare)
-      if (len > 0) S[padE<E>(e2)] = acc;
-    }
-    if (c > 0 && tid == 0 && (sm.stE[0] >> 13) == 0) {
-      // a bucket continued from the previous chunk: its remaining entries
-      // are added by one thread after the heads (S[e2] is not touched by
-      // this chunk's heads, whose buckets all start in this chunk)
-      const int pk = sm.stE[0];
-      double2 acc = cmul(sm.stA[0], sm.stW[0]);
-      for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
-      S[padE<E>(pk & 8191)] = cadd(S[padE<E>(pk & 8191)], acc);
+    // (S holds the previous item's data elsewhere: only nonempty buckets are
+    // read back, by the occupancy mask)
+    const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
+    if (a.bal) {
+      // balanced order: the thread's slots tid, tid + NT, ... hold its
+      // bucket pieces one after the other, in j order; the running sum is
+      // stored after every entry (the last store of a piece is its total)
+      const int nreg = __ldg(&a.k1c[nch + 1 + c]);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int i = tid; i < nreg; i += NT) {
+        const int cd = sm.stE[i];
+        const double2 pr = cmul(sm.stA[i], sm.stW[i]);
+        acc = (cd & kK1First) ? pr : cadd(acc, pr);
+        S[padE<E>(cd & 0x3fff)] = acc;
+      }
+      if (n > nreg) {  // fix-up: later pieces of split buckets, in order
+        __syncthreads();
+        for (int r = nreg + tid; r < n; r += NT) {
+          const int rc = sm.stE[r];
+          const int e2 = rc & 0x3fff, o0 = (rc >> 14) & 63, cnt = rc >> 20;
+          double2 t = S[padE<E>(e2)];
+          for (int k = 0; k < cnt; ++k) t = cadd(t, S[padE<E>(L2 + 1 + o0 + k)]);
+          S[padE<E>(e2)] = t;
+        }
+      }
+    } else {
+      // bucket order: the first entry of a bucket (size in e2q >> 13) sums
+      // it in j order and stores T; a bucket continued from the previous
+      // chunk is added to by this chunk's entry 0
+      for (int i = tid; i < n; i += NT) {
+        const int pk = sm.stE[i];
+        const int len = pk >> 13, e2 = pk & 8191;
+        double2 acc = cmul(sm.stA[i], sm.stW[i]);
+        const int end = min(n, i + len);
+        for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));  // collisions (rare)
+        if (len > 0) S[padE<E>(e2)] = acc;
+      }
+      if (c > 0 && tid == 0 && (sm.stE[0] >> 13) == 0) {
+        // a bucket continued from the previous chunk: its remaining entries
+        // are added by one thread after the heads (S[e2] is not touched by
+        // this chunk's heads, whose buckets all start in this chunk)
+        const int pk = sm.stE[0];
+        double2 acc = cmul(sm.stA[0], sm.stW[0]);
+        for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
+        S[padE<E>(pk & 8191)] = cadd(S[padE<E>(pk & 8191)], acc);
+      }
     }
     __syncthreads();  // staging consumed
     if (tid == 0) {
@@ -886,7 +915,7 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   c.nbx = int((pl->sp.L2 + CB - 1) / CB);
   c.part_stride = int(2 * c.ngroups * c.PG);
   c.off_U = take(size_t(c.nsets) * pairs * pl->sp.L * 16);
-  c.off_asort = take(size_t(c.nsets) * pairs * pl->s * 16);
+  c.off_asort = take(size_t(c.nsets) * pairs * pl->S1 * 16);
   c.off_colsum = take(size_t(std::max<int64_t>(t, 1)) * 8);
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   c.off_part = take(colmean ? size_t(c.nsets) * c.nbx * c.part_stride * 8 : 0);
@@ -902,21 +931,17 @@ static void set_smem_attr(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
-// staging entries of K1 per chunk: the whole scatter input when it fits
-// next to the row at the kernel's residency (2 CTAs per SM for L2 <= 4096)
-static int rows_chunk(int64_t L2, int64_t s) {
-  const int64_t cap = L2 >= 8192 ? 2048 : 1024;
-  return int(std::min<int64_t>(cap, (s + 31) / 32 * 32));
-}
-
 static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                       double* colsum) {
   K1Args a;
   a.asort = asort;
   a.e2q = pl->d_e2q;
   a.occ = pl->d_occ;
-  a.s = pl->s;
-  a.CH = rows_chunk(pl->sp.L2, pl->s);
+  a.S1 = pl->S1;
+  a.CH = pl->k1_ch;
+  a.k1c = pl->d_k1c;
+  a.nch = pl->k1_nch;
+  a.bal = pl->k1_bal;
   a.twj = pl->d_twj;
   a.tws = pl->d_tws;
   a.W = pl->d_W;
@@ -933,7 +958,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
 template <int L2>
 static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                        double* colsum, cudaStream_t st) {
-  const int CH = rows_chunk(L2, pl->s);
+  const int CH = pl->k1_ch;
   const size_t smem = rows_smem<L2>(CH);
   auto kern = k_rows16<L2>;
   set_smem_attr(kern, smem);
@@ -1121,9 +1146,9 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
     double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
     E.rowpart = (double*)(ws + cl.off_rowsum);
-    double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->s;
+    double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->S1;
     prof_begin(KC_PACK, bs);
-    k_pack<<<dim3(nblk(pl->s, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_bent, pl->s, asort);
+    k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
     QMC_LAUNCHED();
     prof_end(KC_PACK, bs);
     prof_begin(KC_ROWS, bs);

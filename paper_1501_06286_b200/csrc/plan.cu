@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <new>
+#include <queue>
 #include <vector>
 
 #include "fft.cuh"
@@ -138,7 +139,8 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_e = take(size_t(s) * 4);
   l.off_bstart = take(size_t(sp.L2 + 1) * 4);
   l.off_bent = take(size_t(s) * 16);
-  l.off_e2q = take(size_t(s) * 4);
+  const int64_t s1 = k1_s1max(s, sp.L2);
+  l.off_e2q = take(size_t(s1) * 4 + 16);
   l.off_occ = take(size_t(sp.L2 / 32 + 1) * 4);
   l.off_zeta = take(size_t(m) * 8);
   l.off_W = take(size_t(sp.L) * 16);
@@ -146,7 +148,9 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_tw2 = take(size_t(sp.L2) * 16);
   l.off_twL = take(size_t(sp.L2) * 16);
   l.off_tws = take(size_t(sp.L2) * 16);
-  l.off_twj = take(size_t(sp.L1) * size_t(s) * 16);
+  l.off_twj = take(size_t(sp.L1) * size_t(s1) * 16);
+  l.off_jq = take(size_t(s1) * 4);
+  l.off_k1c = take(size_t(2 * s1 + 4) * 4);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
   l.total = o;
   return l;
@@ -347,14 +351,118 @@ __global__ void k_stage_twiddles(double2* __restrict__ tws, int N, int E) {
 // twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x: the twiddle of the
 // q-th entry (bucket order) in row f1 of the scatter fused with the first DFT
 // dimension (K1)
-__global__ void k_twj(const int4* __restrict__ bent, int64_t s, int64_t L, int L1, double2* __restrict__ twj) {
+// twj[f1·S1 + q] = ω_L^{(e_j·f1) mod L} for the column j = jq[q] of slot q of
+// the K1 order (0 for padding slots)
+__global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict__ e, int64_t S1, int64_t L, int L1,
+                      double2* __restrict__ twj) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (i >= s * L1) return;
-  const int64_t f1 = i / s, q = i % s;
-  const int64_t x = (int64_t(bent[q].y) * f1) % L;
+  if (i >= S1 * L1) return;
+  const int64_t f1 = i / S1, q = i % S1;
+  const int j = jq[q];
+  if (j < 0) {
+    twj[i] = make_double2(0.0, 0.0);
+    return;
+  }
+  const int64_t x = (int64_t(e[j]) * f1) % L;
   double sv, cv;
   sincospi(2.0 * double(x) / double(L), &sv, &cv);
   twj[i] = make_double2(cv, -sv);
+}
+
+// Staging slots of one K1 chunk (36 B each: a, twiddle, code) that fit next
+// to the row at the row kernel's residency: one CTA per SM for rows of 8192
+// (the whole 227 KB), two otherwise.
+static int k1_slot_budget(int64_t L2) {
+  const int64_t limit = L2 >= 8192 ? 232448 : 115712;
+  const int64_t row = k1_row_slots(L2, QMC_ROW_E) * 16 + 16;  // row slots, mbarrier
+  return int(std::min<int64_t>(4096, (limit - row - 64) / 36) / 4 * 4);
+}
+
+// K1 "balanced" order of the scatter input (pipeline.cu k1_item).  Buckets
+// e2 are cut into chunks of whole buckets.  In a chunk of n entries, with
+// M = ⌈n / NT⌉ (NT threads of the row CTA), every bucket is cut into pieces
+// of at most M entries (j order kept); pieces go, largest first, to the
+// least-loaded thread, whose entries sit at slots base + i·NT + tid.  The
+// scatter of a chunk is then one pass without divergence, each thread
+// keeping a running sum per piece.  A bucket's first piece sums into its own
+// row entry, later pieces into overflow slots, added after a barrier by
+// fix-up records, in piece order.  Padding slots have no column.  Returns
+// false when no chunking fits the staging budget (K1 then uses the
+// bucket-order heads scatter).
+static bool k1_balanced_order(const std::vector<int32_t>& hb, const std::vector<int4>& hbent, int64_t L2, int NT,
+                              int budget, int64_t s1max, std::vector<int32_t>& jq, std::vector<int32_t>& code,
+                              std::vector<int32_t>& cs, std::vector<int32_t>& cr, int& chmax) {
+  struct Piece {
+    int q0, len, v;
+  };
+  using Load = std::pair<int, int>;  // (entries, thread)
+  for (int64_t target = budget; target >= NT; target = target * 3 / 4) {
+    jq.clear();
+    code.clear();
+    cs.assign(1, 0);
+    cr.clear();
+    chmax = 0;
+    bool ok = true;
+    for (int64_t b = 0; b < L2 && ok;) {
+      int64_t e = b + 1;
+      while (e < L2 && hb[e + 1] - hb[b] <= target) ++e;
+      const int64_t n = hb[e] - hb[b];
+      const int M = int(std::max<int64_t>(1, (n + NT - 1) / NT));
+      std::vector<Piece> pc;
+      std::vector<int32_t> rec;
+      int ovf = 0;
+      for (int64_t x = b; x < e && ok; ++x) {
+        const int sz = hb[x + 1] - hb[x];
+        const int np = (sz + M - 1) / M;
+        for (int k = 0; k < np; ++k)
+          pc.push_back({hb[x] + k * M, std::min(M, sz - k * M), k == 0 ? int(x) : int(L2) + 1 + ovf + k - 1});
+        if (np > 1) {
+          if (ovf + np - 1 > kK1Ovf || np - 1 > 15) ok = false;
+          rec.push_back(int(x) | (ovf << 14) | ((np - 1) << 20));
+          ovf += np - 1;
+        }
+      }
+      if (!ok) break;
+      std::stable_sort(pc.begin(), pc.end(), [](const Piece& u, const Piece& v) { return u.len > v.len; });
+      std::vector<std::vector<Piece>> own(NT);
+      std::priority_queue<Load, std::vector<Load>, std::greater<Load>> h;
+      for (int t = 0; t < NT; ++t) h.push({0, t});
+      int mr = 0;
+      for (const Piece& p : pc) {
+        const Load l = h.top();
+        h.pop();
+        own[l.second].push_back(p);
+        h.push({l.first + p.len, l.second});
+        mr = std::max(mr, l.first + p.len);
+      }
+      const int64_t nreg = (int64_t(mr) * NT + 3) / 4 * 4;  // chunk starts stay 16-byte aligned
+      const int64_t slots = nreg + (int64_t(rec.size()) + 3) / 4 * 4;
+      if (slots > budget || int64_t(jq.size()) + slots > s1max) {
+        ok = false;
+        break;
+      }
+      const size_t base = jq.size();
+      jq.resize(base + slots, -1);
+      code.resize(base + nreg, int(L2) | kK1First);
+      code.insert(code.end(), rec.begin(), rec.end());
+      code.resize(base + slots, int(L2));  // no-op records
+      for (int t = 0; t < NT; ++t) {
+        int i = 0;
+        for (const Piece& p : own[t])
+          for (int k = 0; k < p.len; ++k, ++i) {
+            const size_t slot = base + size_t(i) * NT + t;
+            jq[slot] = hbent[p.q0 + k].x;
+            code[slot] = p.v | (k == 0 ? kK1First : 0);
+          }
+      }
+      cr.push_back(int(nreg));
+      cs.push_back(int(jq.size()));
+      chmax = std::max<int>(chmax, int(slots));
+      b = e;
+    }
+    if (ok) return true;
+  }
+  return false;
 }
 
 // W[f1*L2 + f2] = DFT_L(K)[f1 + L1·f2] / L with the correlation kernel
@@ -512,6 +620,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_twL = (double2*)(b + lay.off_twL);
   pl->d_tws = (double2*)(b + lay.off_tws);
   pl->d_twj = (double2*)(b + lay.off_twj);
+  pl->d_jq = (int32_t*)(b + lay.off_jq);
+  pl->d_k1c = (int32_t*)(b + lay.off_k1c);
   cudaStream_t st = pl->stream;
 
   auto fail = [&](int code) {
@@ -588,7 +698,44 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_stage_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tws, int(sp.L2), QMC_ROW_E);
   QMC_PLAN_LAUNCHED();
-  k_twj<<<blocks(sp.L1 * s, 256), 256, 0, st>>>(pl->d_bent, s, sp.L, int(sp.L1), pl->d_twj);
+  {
+    // K1 order of the scatter input (k1_balanced_order, else bucket order)
+    QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
+    std::vector<int32_t> hb(size_t(sp.L2) + 1);
+    std::vector<int4> hbent(static_cast<size_t>(s));
+    QMC_PLAN_CHECK(cudaMemcpy(hb.data(), pl->d_bstart, 4 * hb.size(), cudaMemcpyDeviceToHost) ? QMC_ECUDA : 0);
+    QMC_PLAN_CHECK(cudaMemcpy(hbent.data(), pl->d_bent, 16 * hbent.size(), cudaMemcpyDeviceToHost) ? QMC_ECUDA : 0);
+    const int NT = int(sp.L2 / QMC_ROW_E);
+    std::vector<int32_t> jq, code, cs, cr;
+    int chmax = 0;
+    pl->k1_bal = !getenv("QMC_K1_HEADS") &&
+                 k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2), jq, code, cs, cr,
+                                   chmax);
+    if (pl->k1_bal) {
+      pl->S1 = int64_t(jq.size());
+      pl->k1_ch = chmax;
+      QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
+    } else {
+      // bucket order, chunks of CH entries (CH a multiple of 32)
+      jq.clear();
+      cs.clear();
+      cr.clear();
+      pl->S1 = s;
+      pl->k1_ch = int(std::min<int64_t>(sp.L2 >= 8192 ? 2048 : 1024, (s + 31) / 32 * 32));
+      jq.resize(size_t(s));
+      for (int64_t q = 0; q < s; ++q) jq[q] = hbent[q].x;
+      for (int64_t q0 = 0; q0 < s; q0 += pl->k1_ch) {
+        cr.push_back(int(std::min<int64_t>(pl->k1_ch, s - q0)));
+        cs.push_back(int(q0));
+      }
+      cs.push_back(int(s));
+    }
+    pl->k1_nch = int(cr.size());
+    cs.insert(cs.end(), cr.begin(), cr.end());
+    QMC_PLAN_CHECK(cudaMemcpy(pl->d_jq, jq.data(), 4 * jq.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
+    QMC_PLAN_CHECK(cudaMemcpy(pl->d_k1c, cs.data(), 4 * cs.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
+  }
+  k_twj<<<blocks(sp.L1 * pl->S1, 256), 256, 0, st>>>(pl->d_jq, pl->d_e, pl->S1, sp.L, int(sp.L1), pl->d_twj);
   QMC_PLAN_LAUNCHED();
   QMC_PLAN_CHECK(spectrum_dispatch(pl));
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
@@ -661,6 +808,10 @@ int qmc_plan_info(qmc_plan_t pl, int64_t* info) {
   info[9] = pl->batch_pairs;
   info[10] = pl->D;
   info[11] = int64_t(pl->p);
+  info[12] = pl->k1_bal;
+  info[13] = pl->S1;
+  info[14] = pl->k1_nch;
+  info[15] = pl->k1_ch;
   return QMC_OK;
 }
 

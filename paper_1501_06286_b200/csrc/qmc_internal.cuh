@@ -53,8 +53,22 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // and the create call.
 struct PlanLayout {
   size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_zeta, off_W,
-      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_tmp, total;
+      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_jq, off_k1c, off_tmp, total;
 };
+// K1 scatter-input order (plan.cu k1_order): at most k1_s1max(s, L2) slots
+inline int64_t k1_s1max(int64_t s, int64_t L2) { return 2 * s + L2 + 64; }
+// K1 balanced order (plan.cu k1_balanced_order): slot codes hold the row
+// index v of the running sum in bits 0..13 — a bucket e2 < L2, the padding
+// slot v = L2, or overflow slot v = L2 + 1 + o (o < kK1Ovf) of a bucket's
+// second and later pieces — and kK1First on the first entry of a piece;
+// fix-up records (after a chunk's slots) are e2 | o0 << 14 | count << 20
+// (S[e2] += S[L2+1+o0] + ... in order).
+constexpr int kK1First = 1 << 14;
+constexpr int kK1Ovf = 64;
+// shared-memory row slots of K1: padE(v) for every v <= L2 + kK1Ovf
+__host__ __device__ inline constexpr int64_t k1_row_slots(int64_t L2, int E) {
+  return L2 + kK1Ovf + 1 + (L2 + kK1Ovf) / E + 1;
+}
 PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
 
 // K2 column-pass splits L1 = R·M (pipeline.cu k_cols_x): R = 1 is one thread
@@ -87,6 +101,11 @@ struct qmc_plan {
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
+  // K1 scatter input (plan.cu k1_order): S1 staged slots per pair / per f1
+  // in k1_nch chunks of at most k1_ch slots; k1_bal = 1: balanced
+  // thread-major order of bucket pieces (codes: kK1First), 0: bucket order
+  int64_t S1;
+  int k1_bal, k1_nch, k1_ch;
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
   // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3
@@ -103,8 +122,9 @@ struct qmc_plan {
   int32_t* d_R;      // [N]  R[n] = (m - L[n]) mod m, n >= 1 (tables / tests)
   int32_t* d_e;      // [s]
   int32_t* d_bstart; // [L2+1]
-  int32_t* d_e2q;    // [s]   e2 = e_j mod L2 of the q-th entry in bucket order, | (bucket
-                     //       size << 13) on the first entry of each bucket
+  int32_t* d_e2q;    // [S1]  bucket codes of the K1 order: heads — e2 = e_j mod L2, |
+                     //       (bucket size << 13) on the first entry of each bucket;
+                     //       balanced — see kK1First
   uint32_t* d_occ;   // [L2/32+1] bitmap of the nonempty buckets e2
   int4* d_bent;      // [s]   bucket order (e2 = e_j mod L2, then j): {j, e_j, e2,
                      //       end of this bucket if the entry is its first, else -1}
@@ -114,6 +134,8 @@ struct qmc_plan {
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
   double2* d_tws;    // [L2]  row-FFT stage twiddles, stage-major (fft.cuh reg_stage)
-  double2* d_twj;    // [L1·s] twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x (K1 scatter
-                     //        twiddles in bucket order)
+  double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_L^{(e_j·f1) mod L}, j = jq[q] (K1 scatter
+                     //        twiddles in the K1 order; 0 for padding slots)
+  int32_t* d_jq;     // [S1]  column j of slot q of the K1 order (-1: padding)
+  int32_t* d_k1c;    // [k1_nch+1] chunk starts, then [k1_nch] regular-round slots per chunk
 };

@@ -438,3 +438,35 @@ def test_cbc_lattice_gpu(qmc, N, s):
     zo = O.cbc_lattice(N, s, gam)
     if np.array_equal(zo, zg):
         assert abs(O.cbc_error(N, zg, gam) - O.cbc_error(N, zo, gam)) == 0.0
+
+
+# ------------------------------------------------------------------ K1 scatter-input orders
+# (N, s, t): sparse buckets (s << L2), one chunk; dense (s = L2 = 4096, four
+# chunks); dense rows of 8192 (s = L2, config 5's shape); heavy collisions
+# (~15 entries per bucket: continuation rounds or the bucket-order fallback).
+K1_ORDER_CASES = [(4001, 400, 10), (40961, 4096, 4), (786433, 8192, 2), (65537, 60000, 2)]
+
+
+@pytest.mark.parametrize("N,s,t", K1_ORDER_CASES)
+@pytest.mark.parametrize("heads", [False, True])
+def test_k1_scatter_orders(qmc, monkeypatch, N, s, t, heads):
+    """Both layouts of the row kernel's scatter input (plan.cu
+    k1_balanced_order and the bucket-order fallback, forced by QMC_K1_HEADS)
+    give X within the bar, on sampled rows and on one full column pair."""
+    import torch
+    if heads:
+        monkeypatch.setenv("QMC_K1_HEADS", "1")
+    w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=N + s)
+    plan = qmc.Plan.from_workload(w)
+    if heads:
+        assert plan.info["k1_balanced"] == 0 and plan.info["k1_slots"] == s
+    elif s <= 8192:
+        assert plan.info["k1_balanced"] == 1
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = plan.matmul(A)
+    rows = sample_rows(w.N, 128, seed=s)
+    Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    check_X(w, Xs, X_rows(w, rows))
+    if N * s <= 65537 * 60000:
+        cols = [0, 1]
+        check_X(w, X[:, cols].cpu().numpy(), X_full(w, cols=cols, block=8192), cols=cols)
