@@ -833,6 +833,150 @@ __global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
   cp_async_wait_all();
 }
 
+// Persistent, software-pipelined two-stage K2 (L1 = R·M, R > 1; config 5:
+// 96 = 6·16): tile = (8 pairs, one U column block of kUB = 4 columns e2),
+// i.e. 8 contiguous runs of L1·kUB complex, staged by cp.async one tile
+// ahead with its output row indices.  Stage A, item (p, c, r): the M values
+// f1 = r + R·mm times conj(ω_L^{e2 f1}), M-point inverse DFT, times
+// ω_{L1}^{r k2}, written back in place (position r + R·k2).  Stage B, item
+// (p, c, k2): R-point inverse DFT over r → rows e1 = k2 + M·k1, stored as
+// 8-pair row chunks (128 B) of X.  Same arithmetic as k_cols_x<R, M>.
+constexpr int kP2PG = 8;    // pairs per tile
+constexpr int kP2Thr = 256;
+template <int L1>
+__host__ __device__ constexpr int pipe2_pair_stride() { return L1 * kUB + 1; }  // odd, 16-B units
+template <int L1>
+__host__ __device__ constexpr size_t cols_pipe2_smem() {
+  return size_t(kPipeStages) * (size_t(kP2PG) * pipe2_pair_stride<L1>() * 16 + size_t(L1) * kUB * 4);
+}
+
+template <int L1>
+__device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* dst, int* nd) {
+  constexpr int BLK = L1 * kUB, PSTR = pipe2_pair_stride<L1>();
+  const int bx = tile % a.ntx, g = tile / a.ntx;
+  for (int i = threadIdx.x; i < kP2PG * BLK; i += kP2Thr) {
+    const int pp = i / BLK, o = i - pp * BLK;
+    cp_async16(dst + pp * PSTR + o, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK + o);
+  }
+  for (int i = threadIdx.x; i < L1 * kUB; i += kP2Thr) {
+    const int e1 = i / kUB, cc = i - e1 * kUB;
+    const int64_t ii = int64_t(a.L2) * e1 + bx * kUB + cc;
+    if (ii < a.m)
+      cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
+    else
+      nd[i] = -1;  // zero-padded correlation: not a row of X
+  }
+}
+
+template <int R, int M, int EP>
+__device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2 (*red)[16],
+                                          int lg2L2) {
+  constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = kP2PG;
+  const EpiArgs& E = a.E;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int p = tid % PG;
+  const int bx = tile % a.ntx, g = tile / a.ntx;
+  const int pair = g * PG + p;
+  const int64_t k = 2 * (a.pair0 + pair);
+  double* xk = E.X ? E.X + k : nullptr;
+  double2 acc = make_double2(0.0, 0.0);
+  if (bx == 0 && warp == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
+    const bool okrow = tid < PG;
+    const double phi0 = __ldg(a.scal);
+    const double2 v0 = make_double2(phi0 * a.colsum[k], phi0 * a.colsum[k + 1]);
+    double r0 = 0.0;
+    emit<EP>(E, v0, 0, okrow, true, xk, acc, r0);
+  }
+  // stage A: items (p, c, r), it = p + PG·(c + kUB·r)
+  for (int it = tid; it < PG * kUB * R; it += kP2Thr) {
+    const int c = (it / PG) % kUB, r = it / (PG * kUB);
+    const int e2 = bx * kUB + c;
+    double2* Tp = T + p * PSTR + c;
+    double2 x[M];
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm) x[mm] = Tp[(r + R * mm) * kUB];
+    // conj(ω_L^{e2 (r + R mm)}) = conj(b0 · st^mm)
+    const double2 b0 = omegaL(int64_t(e2) * r, lg2L2, a.L2, a.tw1, a.twL);
+    double2 pw[M];
+    pw[0] = make_double2(1.0, 0.0);
+    if (M > 1) pw[1] = omegaL(int64_t(e2) * R, lg2L2, a.L2, a.tw1, a.twL);
+#pragma unroll
+    for (int q = 2; q < M; ++q) pw[q] = cmul(pw[q / 2], pw[q - q / 2]);
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm) x[mm] = cmulc(x[mm], cmul(b0, pw[mm]));
+    reg_dft<M, +1>(x, a.tw1, L1 / M);
+#pragma unroll
+    for (int k2 = 1; k2 < M; ++k2)
+      if (r) x[k2] = cmul(x[k2], twid<+1>(__ldg(&a.tw1[r * k2])));
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) Tp[(r + R * k2) * kUB] = x[k2];
+  }
+  __syncthreads();
+  // stage B: items (p, c, k2), it = p + PG·(c + kUB·k2); a warp = 8 pairs × 4
+  // columns of one k2, so each output row gets one 128-byte chunk
+  for (int it = tid; it < PG * kUB * M; it += kP2Thr) {
+    const int c = (it / PG) % kUB, k2 = it / (PG * kUB);
+    const double2* Tp = T + p * PSTR + c;
+    double2 z[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[r] = Tp[(r + R * k2) * kUB];
+    reg_dft<R, +1>(z, a.tw1, L1 / R);
+    double rr;
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) {
+      const int n = nS[(k2 + M * k1) * kUB + c];  // -1: padding row (uniform over the 8 lanes of the row)
+      if (n >= 0) emit_fast<EP>(E, z[k1], n, xk, acc, rr);
+    }
+  }
+  if (a.part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
+#pragma unroll
+    for (int o = PG; o < 32; o <<= 1) {
+      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+    }
+    if ((tid & 31) < PG) red[warp][tid & 31] = acc;
+    __syncthreads();
+    if (tid < PG) {
+      double2 sacc = red[0][tid];
+      for (int ww = 1; ww < kP2Thr / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
+      double* dst = a.part + int64_t(bx) * a.part_stride + 2 * pair;
+      dst[0] = sacc.x;
+      dst[1] = sacc.y;
+    }
+  }
+}
+
+template <int R, int M, int EP>
+__global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
+  constexpr int L1 = R * M;
+  constexpr int STAGE = kP2PG * pipe2_pair_stride<L1>();
+  extern __shared__ double2 sm[];
+  int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
+  __shared__ double2 red[kP2Thr / 32][16];
+  const int ntiles = a.ntx * a.ngroups;
+#pragma unroll
+  for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
+    const int tl = blockIdx.x + s0 * gridDim.x;
+    if (tl < ntiles) k2p2_issue<L1>(a, tl, sm + s0 * STAGE, nS + s0 * (L1 * kUB));
+    cp_async_commit();
+  }
+  int it = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+    const int st = it % kPipeStages;
+    const int ahead = tile + (kPipeStages - 1) * gridDim.x;
+    if (ahead < ntiles) {
+      const int sa = (it + kPipeStages - 1) % kPipeStages;
+      k2p2_issue<L1>(a, ahead, sm + sa * STAGE, nS + sa * (L1 * kUB));
+    }
+    cp_async_commit();
+    asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
+    __syncthreads();
+    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), red, lg2L2);
+    __syncthreads();  // stage st and red are reused
+  }
+  cp_async_wait_all();
+}
+
 // out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
 // lane-strided partial sums, then a fixed shuffle tree (deterministic)
 __global__ void k_colpart_reduce(const double* __restrict__ part, int nbx, int part_stride, int ncols, int64_t k0,
@@ -1057,6 +1201,26 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       const int64_t ntiles = int64_t(ntx) * ng;
       const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
       pk<<<grid, 16 * CBP, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum));
+      QMC_LAUNCHED();
+      *nbx_used = ntx;
+      return QMC_OK;
+    }
+  }
+  if constexpr (R > 1 && EP != EPK_ROWSUM && cols_pipe2_smem<R * M>() <= 232448) {
+    // two-stage column pass, pipelined: whole 8-pair groups, whole pairs,
+    // vector X stores, whole U column blocks
+    if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !getenv("QMC_K2_NOPIPE")) {
+      constexpr size_t psm = cols_pipe2_smem<L1>();
+      auto pk = k_cols_pipe2<R, M, EP>;
+      set_smem_attr(pk, psm);
+      int per_sm = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kP2Thr, psm);
+      if (pl->k2_per_sm > 0) per_sm = std::min(per_sm, pl->k2_per_sm);
+      const int ntx = int(pl->sp.L2 / kUB), ng = np / kP2PG;
+      const int64_t ntiles = int64_t(ntx) * ng;
+      const unsigned grid =
+          unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(sm_count_cols()) * std::max(per_sm, 1))));
+      pk<<<grid, kP2Thr, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum), ilog2(pl->sp.L2));
       QMC_LAUNCHED();
       *nbx_used = ntx;
       return QMC_OK;
