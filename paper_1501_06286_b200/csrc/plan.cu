@@ -743,12 +743,13 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
 #undef QMC_PLAN_LAUNCHED
   pl->nstreams = 1;
   pl->mu = new (std::nothrow) std::mutex();
-  // two internal streams overlap consecutive batches; when the column pass
-  // needs the two-stage (non-persistent) K2 (L1 > 16) that overlap measured
-  // slower on B200 (config 5: 119 vs 111 ms/step; config 4, L1 = 16: 2.55 vs
-  // 2.63 ms with two), so those plans run their batches on the caller's stream
+  // two internal streams overlap consecutive batches when the column pass is
+  // a persistent pipelined kernel (k_cols_pipe, k_cols_pipe2: L1 <= 192;
+  // measured on B200, config 5: 98.6 vs 105.0 ms/step).  With the
+  // non-persistent k_cols_x (L1 = 256) the overlap measured slower (config 5
+  // before k_cols_pipe2: 119 vs 111 ms), so such plans use the caller's stream.
   const char* one = getenv("QMC_ONE_STREAM");
-  const bool want2 = one ? one[0] != '1' : sp.L1 <= 16;
+  const bool want2 = one ? one[0] != '1' : sp.L1 <= 192;
   if (want2 && pl->mu &&
       cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
       cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
