@@ -370,6 +370,16 @@ __device__ __forceinline__ void reg_stage(double2 (&v)[E], const double2* __rest
   }
 }
 
+// padE(x + r·stride) = padE(x) + r·pad_step(stride) for every r of a stage
+// when stride is a multiple of E, or stride = 1 with x a multiple of R and
+// R dividing E (the run x .. x + R - 1 stays inside one E-block): then all
+// accesses of a stage are one base address plus immediate offsets.
+template <int E, int R, int STRIDE>
+struct PadStep {
+  static constexpr bool lin = STRIDE % E == 0 || (STRIDE == 1 && E % R == 0);
+  static constexpr int step = STRIDE + STRIDE / E;
+};
+
 // After reg_stage<R,N,E,NS>: v[b + r·BPT] holds output index base_b + r·NS.
 template <int R, int N, int E, int NS>
 __device__ __forceinline__ void store_stage(const double2 (&v)[E], double2* S) {
@@ -379,8 +389,14 @@ __device__ __forceinline__ void store_stage(const double2 (&v)[E], double2* S) {
   for (int b = 0; b < BPT; ++b) {
     const int j = tid + b * NT;
     const int base = (j / NS) * NS * R + (j % NS);
+    if constexpr (PadStep<E, R, NS>::lin) {
+      double2* Sb = S + padE<E>(base);
 #pragma unroll
-    for (int r = 0; r < R; ++r) S[padE<E>(base + r * NS)] = v[b + r * BPT];
+      for (int r = 0; r < R; ++r) Sb[r * PadStep<E, R, NS>::step] = v[b + r * BPT];
+    } else {
+#pragma unroll
+      for (int r = 0; r < R; ++r) S[padE<E>(base + r * NS)] = v[b + r * BPT];
+    }
   }
 }
 
@@ -388,16 +404,28 @@ template <int N, int E>
 __device__ __forceinline__ void load_strided(double2 (&v)[E], const double2* S) {
   constexpr int NT = N / E;
   const int tid = tid_fresh();
+  if constexpr (NT % E == 0) {
+    const double2* Sb = S + padE<E>(tid);
 #pragma unroll
-  for (int q = 0; q < E; ++q) v[q] = S[padE<E>(tid + q * NT)];
+    for (int q = 0; q < E; ++q) v[q] = Sb[q * (NT + NT / E)];
+  } else {
+#pragma unroll
+    for (int q = 0; q < E; ++q) v[q] = S[padE<E>(tid + q * NT)];
+  }
 }
 
 template <int N, int E>
 __device__ __forceinline__ void store_strided(const double2 (&v)[E], double2* S) {
   constexpr int NT = N / E;
   const int tid = tid_fresh();
+  if constexpr (NT % E == 0) {
+    double2* Sb = S + padE<E>(tid);
 #pragma unroll
-  for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = v[q];
+    for (int q = 0; q < E; ++q) Sb[q * (NT + NT / E)] = v[q];
+  } else {
+#pragma unroll
+    for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = v[q];
+  }
 }
 
 // tws: all stages' twiddle tables back to back (stage I >= 1 at offset OFF,
@@ -440,22 +468,25 @@ __device__ __forceinline__ void fftE_fwd_w_rec(double2 (&v)[E], double2* S, cons
       __syncthreads();
       store_stage<RP, N, E, NS / RP>(v, S);
       if constexpr (LAST) {
+        const double2* Wt = Wr + tid_fresh();
 #pragma unroll
-        for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wr[tid_fresh() + q * NT]);
+        for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wt[q * NT]);
       }
       __syncthreads();
       load_strided<N, E>(v, S);
     } else if constexpr (LAST) {
+      const double2* Wt = Wr + tid_fresh();
 #pragma unroll
-      for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wr[tid_fresh() + q * NT]);
+      for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wt[q * NT]);
     }
     reg_stage<R, N, E, NS, -1>(v, tws + OFF, tid);
     if constexpr (LAST) {
       dc = v[0];
 #pragma unroll
       for (int q = 0; q < H; ++q) v[q] = cmul(v[q], wv[q]);
+      const double2* Wt = Wr + tid_fresh();
 #pragma unroll
-      for (int q = H; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[tid_fresh() + q * NT]));
+      for (int q = H; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wt[q * NT]));
     }
     fftE_fwd_w_rec<N, E, NS * R, I + 1, (I > 0 ? OFF + NS * (R - 1) : OFF)>(v, S, tws, tid, Wr, dc);
   }

@@ -287,10 +287,20 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
   }
   QMC_TS(1);
   double2 v[E];
+  {
+    // nonempty buckets only (the rest of S is stale); NT is a multiple of 32
+    const int t0 = tid_fresh();
+    const double2* Sb = S + padE<E>(t0);
+    const uint32_t* ob = a.occ + (t0 >> 5);
 #pragma unroll
-  for (int q = 0; q < E; ++q) {  // nonempty buckets only (the rest of S is stale)
-    const int e2 = tid_fresh() + q * NT;
-    v[q] = (__ldg(&a.occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
+    for (int q = 0; q < E; ++q) {
+      if constexpr (NT % 32 == 0 && NT % E == 0)
+        v[q] = (__ldg(&ob[q * (NT / 32)]) >> (t0 & 31)) & 1u ? Sb[q * (NT + NT / E)] : make_double2(0.0, 0.0);
+      else {
+        const int e2 = t0 + q * NT;
+        v[q] = (__ldg(&a.occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
+      }
+    }
   }
   const double2* Wr = a.W + int64_t(f1) * L2;
   double2 dc;
