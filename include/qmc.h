@@ -156,8 +156,10 @@ int qmc_mean_finalize(qmc_plan_t plan, int f, const double* reduced, int64_t t_t
                       void* stream);
 
 /* End-to-end entry with HOST buffers: copies A_host (pinned or pageable,
- * column-major s×t, lda) into A_dev (device, s*t doubles, ld = s), runs
- * qmc_mean (+ finalize), and copies the result to out_host (1 double for
+ * column-major s×t, lda) into A_dev (device, s*t doubles, ld = s) — batch by
+ * batch of column pairs, each copy on the stream that then runs that batch,
+ * so copies overlap kernels — runs qmc_mean (+ finalize), and copies the
+ * result to out_host (1 double for
  * ROWMEAN_RELU, else t doubles); X_dev (device, ldx) receives X.  out_dev
  * (device) must hold max(N, t) doubles.  X_dev is row-major with ldx >= t.
  * Synchronises `stream`. */

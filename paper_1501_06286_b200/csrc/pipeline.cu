@@ -1274,9 +1274,13 @@ static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2
 
 static unsigned nblk(int64_t n, int b) { return unsigned((n + b - 1) / b); }
 
-// all batches of column pairs; f = -1: X only
+// all batches of column pairs; f = -1: X only.  A_host != NULL: each batch
+// first copies its own columns of A from the host (A_host, leading dimension
+// lda_host) into A on the batch's stream, so that the copy of one batch
+// overlaps the kernels of the other.
 static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int f, double fparam,
-               double* out, double* X, int64_t ldx, void* call_ws, size_t call_ws_bytes, cudaStream_t st) {
+               double* out, double* X, int64_t ldx, void* call_ws, size_t call_ws_bytes, cudaStream_t st,
+               const double* A_host = nullptr, int64_t lda_host = 0) {
   if (!pl) return QMC_ENULL;
   if (t < 0 || lda < pl->s) return QMC_EINVAL_DIM;
   if (X && ldx < t) return QMC_EINVAL_DIM;
@@ -1321,6 +1325,13 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
     E.rowpart = (double*)(ws + cl.off_rowsum);
     double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->S1;
+    if (A_host) {
+      const int64_t c0 = 2 * pair0, nc = std::min<int64_t>(2 * int64_t(np), t - c0);
+      if (cudaMemcpy2DAsync(const_cast<double*>(A) + c0 * lda, size_t(lda) * 8, A_host + c0 * lda_host,
+                            size_t(lda_host) * 8, size_t(pl->s) * 8, size_t(nc), cudaMemcpyHostToDevice,
+                            bs) != cudaSuccess)
+        return QMC_ECUDA;
+    }
     prof_begin(KC_PACK, bs);
     k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
     QMC_LAUNCHED();
@@ -1412,10 +1423,8 @@ int qmc_mean_host(qmc_plan_t pl, const double* A_host, int64_t lda, int64_t t, i
   if (f < QMC_F_IDENTITY || f > QMC_F_ROWMEAN_RELU) return QMC_EINVAL_F;
   if (t < 1 || lda < pl->s) return QMC_EINVAL_DIM;
   cudaStream_t st = (cudaStream_t)stream;
-  if (cudaMemcpy2DAsync(A_dev, size_t(pl->s) * 8, A_host, size_t(lda) * 8, size_t(pl->s) * 8, size_t(t),
-                        cudaMemcpyHostToDevice, st) != cudaSuccess)
-    return QMC_ECUDA;
-  int rc = run(pl, A_dev, pl->s, t, f, f_param, out_dev, X_dev, ldx, call_ws, call_ws_bytes, st);
+  // the H2D copy of A goes batch by batch inside run (overlapping the kernels)
+  int rc = run(pl, A_dev, pl->s, t, f, f_param, out_dev, X_dev, ldx, call_ws, call_ws_bytes, st, A_host, lda);
   if (rc) return rc;
   rc = qmc_mean_finalize(pl, f, out_dev, t, out_dev, stream);
   if (rc) return rc;
