@@ -43,6 +43,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--t", type=int, default=0, help="override the config's t (diagnostics only)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="N > 1: weak = every GPU runs the config's t columns (column block of a "
+                         "G·t-column problem); strong = the config's t columns split over the GPUs")
     return ap.parse_args()
 
 
@@ -161,7 +164,7 @@ def reference_arm(args, rank, world):
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": "strong",
+        "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": w.name, "N": w.N, "s": w.s, "t": w.t},
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "oracle",
@@ -186,10 +189,20 @@ def ours(args, rank, world, local_rank):
     from paper_1501_06286_b200.dist import combine_means, shard_columns
     w = W.config(args.config, t_override=args.t or None)
     G = world
-    c0, c1 = shard_columns(w.t, G, rank)
+    if args.scaling == "weak":
+        # every rank: the config's t columns, as column block `rank` of a
+        # G·t-column problem (blocks of A equal); per-GPU work fixed
+        c0, c1 = rank * w.t, (rank + 1) * w.t
+        t_total = G * w.t
+        A_block = w.A
+    else:
+        # the config's t columns split over the ranks; total work fixed
+        c0, c1 = shard_columns(w.t, G, rank)
+        t_total = w.t
+        A_block = w.A[:, c0:c1]
     tl = c1 - c0
     plan = q.Plan.from_workload(w, device=dev)
-    A_host = np.ascontiguousarray(w.A[:, c0:c1].T)          # (tl, s) row-major = A slab col-major
+    A_host = np.ascontiguousarray(A_block.T)                 # (tl, s) row-major = A slab col-major
     A = torch.from_numpy(A_host).to(dev).t()
     X = q.x_empty(w.N, tl, dev)
     f, fp = w.f, w.f_param
@@ -208,9 +221,9 @@ def ours(args, rank, world, local_rank):
             plan.matmul(A, X)
             return None
         plan.mean(A, f, fp, X=X, out=out)
-        red = combine_means(out, f, w.t, c0)
+        red = combine_means(out, f, t_total, c0)
         if f == W.F_ROWMEAN_RELU:
-            plan.finalize(f, red, w.t, out=res)
+            plan.finalize(f, red, t_total, out=res)
             return res
         return red
 
@@ -250,7 +263,7 @@ def ours(args, rank, world, local_rank):
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms_total = float(t_ms.item())
     ms_step = ms_total / args.steps
-    entries = N * w.t
+    entries = N * t_total
     value = entries * args.steps / (ms_total / 1e3)
 
     # ---- roofline of the dominant kernel (per-class CUDA events, this rank)
@@ -297,7 +310,7 @@ def ours(args, rank, world, local_rank):
         if dom in tf:
             roof["traffic"] = tf[dom]
     # whole-step HBM roofline (north star): compulsory bytes = read A + write X
-    step_bytes = 8.0 * (N + w.s) * w.t
+    step_bytes = 8.0 * (N + w.s) * tl  # this rank's compulsory bytes (rank 0 reports)
     hbm_ach = step_bytes / (ms_step / 1e3) / 1e9
     hbm = {"bytes_per_step": step_bytes, "achieved_GBps": hbm_ach, "peak_GBps": peaks["hbm_gbs"],
            "frac": hbm_ach / peaks["hbm_gbs"], "frac_vs_8TBps_nominal": hbm_ach / 8000.0,
@@ -366,9 +379,10 @@ def ours(args, rank, world, local_rank):
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": G,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": w.name, "family": w.family, "N": N, "s": w.s, "t": w.t,
+                       "t_total": t_total, "t_per_gpu": tl,
                        "phi": PHI_NAMES[w.phi], "f": F_NAMES[w.f], "L": L, "L1": L1, "L2": L2,
                        "batch_pairs": info["batch_pairs"], "parallelism": f"columns/{G}",
                        "l2": "flushed between timed steps (256 MiB write, untimed)"},

@@ -25,27 +25,32 @@ def _free_port():
     return port
 
 
-def _local_results(w, c0, c1, f, f_param):
+def _local_results(w, c0, c1, f, f_param, A=None):
     tab = O.phi_table(w.phi, w.N)
-    A = w.A[:, c0:c1]
+    A = w.A[:, c0:c1] if A is None else A
     X = O.oracle_X_full(lambda r: O.lattice_index_matrix(w.N, w.z, r), tab, w.N, A)
     if f == W.F_ROWMEAN_RELU:
         return X, torch.from_numpy(O.row_sums(X))
     return X, torch.from_numpy(O.column_means(X, f, f_param))
 
 
-def _worker(rank, world, port, w, f, f_param, q):
+def _worker(rank, world, port, w, f, f_param, q, weak=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1501_06286_b200.dist import combine_means, shard_columns
-    c0, c1 = shard_columns(w.t, world, rank)
-    X, local = _local_results(w, c0, c1, f, f_param)
-    red = combine_means(local, f, w.t, c0)
+    if weak:  # bench.py --scaling weak: every rank the full t columns, block `rank` of world·t
+        c0, c1, t_total = rank * w.t, (rank + 1) * w.t, world * w.t
+        X, local = _local_results(w, 0, w.t, f, f_param)
+    else:
+        c0, c1 = shard_columns(w.t, world, rank)
+        t_total = w.t
+        X, local = _local_results(w, c0, c1, f, f_param)
+    red = combine_means(local, f, t_total, c0)
     if f == W.F_ROWMEAN_RELU:
         # finalize semantics of qmc_mean_finalize (reading R10), on the host
         r = red.numpy()
-        out = math.fsum(max(0.0, x / w.t) for x in r) / w.N
+        out = math.fsum(max(0.0, x / t_total) for x in r) / w.N
     else:
         out = red.numpy().copy()
     q.put((rank, c0, c1, X, out))
@@ -53,11 +58,11 @@ def _worker(rank, world, port, w, f, f_param, q):
     dist.destroy_process_group()
 
 
-def _run(world, w, f, f_param):
+def _run(world, w, f, f_param, weak=False):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, w, f, f_param, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, w, f, f_param, q, weak)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in range(world)]
@@ -99,3 +104,25 @@ def test_gloo_world2_matches_unsharded(f, f_param):
         for r in res:
             np.testing.assert_allclose(r[4], want, rtol=0, atol=1e-14)
         assert np.array_equal(res[0][4], res[1][4])   # every rank holds the same vector
+
+
+@pytest.mark.parametrize("f,f_param", [(W.F_ROWMEAN_RELU, 0.0), (W.F_EXP, 0.0)])
+def test_gloo_world2_weak_blocks(f, f_param):
+    """Weak scaling (bench.py --scaling weak): each rank runs all t columns as
+    its block of a 2t-column problem [A, A]; the combined result equals the
+    unsharded oracle on [A, A]."""
+    w = W.custom_lattice(257, 40, 10, W.PHI_INVNORM_MID, seed=19)
+    w.A = np.asfortranarray(w.A * 0.05)
+    res = _run(2, w, f, f_param, weak=True)
+    A2 = np.concatenate([w.A, w.A], axis=1)
+    tab = O.phi_table(w.phi, w.N)
+    Xfull = O.oracle_X_full(lambda r: O.lattice_index_matrix(w.N, w.z, r), tab, w.N, A2)
+    np.testing.assert_allclose(np.concatenate([r[3] for r in res], axis=1), Xfull, rtol=0, atol=1e-12)
+    if f == W.F_ROWMEAN_RELU:
+        want = O.rowmean_relu(Xfull)
+        for r in res:
+            assert abs(r[4] - want) <= 1e-14 * max(1.0, abs(want))
+    else:
+        want = O.column_means(Xfull, f, f_param)
+        for r in res:
+            np.testing.assert_allclose(r[4], want, rtol=0, atol=1e-14)
