@@ -584,14 +584,14 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->ws_bytes = plan_ws_bytes;
   {
     // Batch of column pairs (measured on B200): enough K1 items
-    // (L1 per pair) for ~8192 per launch — persistent CTAs then keep several
+    // (L1 per pair) for ~16384 per launch — persistent CTAs then keep several
     // items each and the long launches amortise their tails — with U (16·L
     // bytes per pair) at least ~128 MB and at most ~768 MB per scratch set;
     // a multiple of the K2 pair group (16, 8 or 4 pairs).  Per call the
     // batch is further capped at half the call's pairs (run() / call_layout),
     // so that two batches can overlap on the two internal streams.
     const int64_t per_pair = 16 * sp.L;
-    int64_t bp = std::max<int64_t>((int64_t(128) << 20) / per_pair, (8192 + sp.L1 - 1) / sp.L1);
+    int64_t bp = std::max<int64_t>((int64_t(128) << 20) / per_pair, (16384 + sp.L1 - 1) / sp.L1);
     bp = std::max<int64_t>(1, std::min<int64_t>(bp, (int64_t(768) << 20) / per_pair));
     bp = std::min<int64_t>(bp, 4096);
     bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
