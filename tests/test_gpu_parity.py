@@ -271,9 +271,11 @@ def test_config5_sampled(qmc):
 # (N, s, t, batch pairs or None): L1 = 16 pipelined K2 (t a multiple of 32),
 # partial pair groups (t = 30, 6: k_cols_x), L1 = 10 (N = 40961), the
 # two-stage column pass L1 = 96 (N = 786433), and several batches on two
-# internal streams (batch 16 of 32 pairs).
+# internal streams (batch 16 of 32 pairs); zero-padded lengths on the
+# pipelined two-stage pass: N = 3079 (L = 6400 = 25·256, L1 = 5·5) and
+# N = 65539 (L = 163840 = 20·8192, L1 = 2·10).
 MEAN_CASES = [(65537, 64, 32, None), (65537, 64, 30, None), (40961, 50, 32, None), (65537, 40, 64, 16),
-              (786433, 16, 6, None)]
+              (786433, 16, 6, None), (786433, 16, 32, None), (3079, 50, 32, None), (65539, 40, 32, None)]
 
 
 @pytest.mark.parametrize("N,s,t,bp", MEAN_CASES)
