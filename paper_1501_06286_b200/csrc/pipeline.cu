@@ -88,6 +88,35 @@ __global__ void k_pack(const double* __restrict__ A, int64_t lda, int64_t t, int
                                      : make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
 }
 
+// Same output, for s up to kPackSmemMax: the CTA first reads the pair's two
+// columns of A into shared memory (coalesced), then gathers from there, so
+// the scattered reads hit shared memory instead of L2 sectors.  blockIdx.x =
+// pair, blockIdx.y = slice of the S1 slots.  (Measured on B200: config 3,
+// s = 4096, 27.0 vs 28.1 ms/step; config 5, s = 8192 with 128 KB per CTA,
+// slower than the direct gather — hence the limit.)
+constexpr int kPackSmemMax = 4096;
+__global__ void __launch_bounds__(256) k_pack_smem(const double* __restrict__ A, int64_t lda, int64_t t,
+                                                   int64_t pair0, const int32_t* __restrict__ jq, int64_t s,
+                                                   int64_t S1, double2* __restrict__ asort) {
+  extern __shared__ double colAB[];  // [2][s]
+  const int p = blockIdx.x;
+  const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+  const double* a1 = A + k1 * lda;
+  const double* a2 = A + k2 * lda;
+  for (int64_t j = threadIdx.x; j < s; j += blockDim.x) {
+    colAB[j] = __ldg(&a1[j]);
+    colAB[s + j] = k2 < t ? __ldg(&a2[j]) : 0.0;
+  }
+  __syncthreads();
+  const int64_t per = (S1 + gridDim.y - 1) / gridDim.y;
+  const int64_t q0 = int64_t(blockIdx.y) * per, q1 = q0 + per < S1 ? q0 + per : S1;
+  double2* dst = asort + int64_t(p) * S1;
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) {
+    const int j = __ldg(&jq[q]);
+    dst[q] = j < 0 ? make_double2(0.0, 0.0) : make_double2(colAB[j], colAB[s + j]);
+  }
+}
+
 // ---------------------------------------------------------------- K1
 // Persistent: CTA b takes the items (f1, p) = b, b + gridDim.x, ... (f1
 // fastest) of the batch; L2/16 threads, 16 points per thread.  Per item:
@@ -1333,7 +1362,17 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
         return QMC_ECUDA;
     }
     prof_begin(KC_PACK, bs);
-    k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
+    if (pl->s <= kPackSmemMax && !getenv("QMC_PACK_GATHER")) {
+      const size_t psm = size_t(pl->s) * 16;
+      set_smem_attr(k_pack_smem, psm);
+      // slices of the slots: ~2 CTAs of work per SM in total
+      const int ny = int(std::max<int64_t>(1, std::min<int64_t>((2 * sm_count_cols() + np - 1) / np,
+                                                                (pl->S1 + 1023) / 1024)));
+      k_pack_smem<<<dim3(unsigned(np), unsigned(ny)), 256, psm, bs>>>(A, lda, t, pair0, pl->d_jq, pl->s, pl->S1,
+                                                                      asort);
+    } else {
+      k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
+    }
     QMC_LAUNCHED();
     prof_end(KC_PACK, bs);
     prof_begin(KC_ROWS, bs);
