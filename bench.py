@@ -344,7 +344,8 @@ def ours(args, rank, world, local_rank):
         e_ms = sum(ee)
         e2e = {"value": entries * args.steps / (e_ms / 1e3), "unit": "entries/s",
                "h2d_bytes_per_step": int(A_pin.numel() * 8), "d2h_bytes_per_step": int(n_res * 8),
-               "ms_per_step": e_ms / args.steps, "api": "qmc_mean_host (C ABI, pinned host A)"}
+               "ms_per_step": e_ms / args.steps, "ms_min": min(ee), "ms_median": sorted(ee)[len(ee) // 2],
+               "ms_max": max(ee), "api": "qmc_mean_host (C ABI, pinned host A)"}
     else:
         A_pin = torch.from_numpy(A_host).pin_memory()
         A_dev2 = torch.empty_like(A_pin, device=dev)
