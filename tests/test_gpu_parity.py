@@ -472,3 +472,18 @@ def test_k1_scatter_orders(qmc, monkeypatch, N, s, t, heads):
     if N * s <= 65537 * 60000:
         cols = [0, 1]
         check_X(w, X[:, cols].cpu().numpy(), X_full(w, cols=cols, block=8192), cols=cols)
+
+
+@pytest.mark.parametrize("N,s,t", [(4001, 400, 10), (40961, 4096, 4)])
+def test_k0_variants_bitwise(qmc, monkeypatch, N, s, t):
+    """K0 through shared memory (s <= 4096) and the direct gather
+    (QMC_PACK_GATHER) produce the same packed input, so X is bitwise equal."""
+    import torch
+    w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=N + 3 * s)
+    plan = qmc.Plan.from_workload(w)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X1 = plan.matmul(A).clone()
+    monkeypatch.setenv("QMC_PACK_GATHER", "1")
+    X2 = plan.matmul(A).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(X1, X2)
