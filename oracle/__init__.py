@@ -18,11 +18,11 @@ generators, no arithmetic of the method).
 
 Parity pins (see tests/test_oracle_pins.py and DESIGN.md §Oracle):
 every function below is pinned by printed values of the paper's worked
-example, closed forms, invariants or brute force, except the two fused
-functionals ``rowmean_relu`` (config 2's scalar) and the ``exp`` column
-mean (config 5) whose value has no closed form:  "parity unpinned"
-beyond the definition itself (they are one-line reductions over the
-pinned X).
+example, closed forms, invariants or brute force.  The two fused
+functionals have no closed form in general and are pinned by special
+cases: ``rowmean_relu`` (config 2's scalar) by the worked example and the
+no-clipping / all-clipped cases, the ``exp`` column mean (config 5) by
+A = 0 and the geometric sum for equal z.
 """
 from .qmc_oracle import *  # noqa: F401,F403
 from .qmc_oracle import __all__  # noqa: F401

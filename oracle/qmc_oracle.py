@@ -16,8 +16,8 @@ Contents
                               selection_P
   the product and means     : oracle_X_rows, oracle_X_rows_fsum,
                               column_means, rowmean_relu
-Pins: tests/test_oracle_pins.py.  ``rowmean_relu`` and ``column_means``
-with f=EXP: parity unpinned (no closed form).
+Pins: tests/test_oracle_pins.py (``rowmean_relu`` and ``column_means``
+with f=EXP by special cases: test_rowmean_relu_pins, test_exp_mean_pins).
 """
 from __future__ import annotations
 
@@ -382,7 +382,8 @@ def oracle_X_full(index_fn, tab: np.ndarray, N: int, A: np.ndarray, cols=None,
 
 def column_means(Xcol: np.ndarray, f: int, param: float = 0.0) -> np.ndarray:
     """(1/N) Σ_{n=0}^{N-1} f(X[n, k]) per column (PAPER.md:60-62 eq_qmc,
-    PAPER.md:154-157), math.fsum per column.  f=EXP: parity unpinned."""
+    PAPER.md:154-157), math.fsum per column.  f=EXP pinned by special cases
+    (A = 0; equal z: geometric sum)."""
     Xcol = np.asarray(Xcol)
     N = Xcol.shape[0]
     if f == F_IDENTITY:
@@ -403,7 +404,7 @@ def row_sums(X: np.ndarray) -> np.ndarray:
 
 def rowmean_relu(X: np.ndarray, t_total: int | None = None) -> float:
     """Config 2's scalar (reading R10): Q = (1/N) Σ_n max(0, (1/t) Σ_k X[n,k]).
-    Parity unpinned (no closed form); a reduction over the pinned X."""
+    Pinned by the worked example and the no-clipping / all-clipped cases."""
     N, t = X.shape
     t = t if t_total is None else t_total
     r = row_sums(X)

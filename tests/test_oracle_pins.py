@@ -369,6 +369,48 @@ def test_config3_means_closed_form():
     np.testing.assert_allclose(means, want, rtol=0, atol=1e-13)
 
 
+# ---------------------------------------------------------------- the fused reductions
+def test_rowmean_relu_pins():
+    """Config 2's scalar Q = (1/N) Σ_n max(0, (1/t) Σ_k X[n,k]) (reading R10):
+    (a) the paper's worked example (N = 7, z = (1,5,3),
+    φ = id) with columns a = (7,7,7) and (-1,0,0): X = (0,9,11,6,15,10,12) and
+    -(0,1,...,6)/7, every row sum >= 0, so Q = (1/14)(63 - 3) = 30/7;
+    (b) A >= 0, φ = id: no clipping, Q = S_φ/(N t)·Σ A = (N-1)/(2 N t)·Σ A
+    (reading R8); (c) A <= 0: every row sum <= 0, Q = 0."""
+    g = load_golden("worked_example_n7.json")
+    tab = O.phi_table(O.PHI_IDENTITY, 7)
+    idx = O.lattice_index_matrix(7, g["g"], np.arange(7))
+    X = O.oracle_X_rows(tab, idx, np.array([[7.0, -1.0], [7.0, 0.0], [7.0, 0.0]]))
+    assert abs(O.rowmean_relu(X) - 30.0 / 7.0) <= 1e-15 * 30
+    N, s, t = 101, 9, 5
+    rng = np.random.default_rng(11)
+    z = rng.integers(1, N, size=s)
+    A = rng.uniform(0.0, 1.0, size=(s, t))
+    tabN = O.phi_table(O.PHI_IDENTITY, N)
+    X = O.oracle_X_full(lambda r: O.lattice_index_matrix(N, z, r), tabN, N, A)
+    want = (N - 1) / (2 * N * t) * math.fsum(A.ravel())
+    assert abs(O.rowmean_relu(X) - want) <= 1e-14 * want
+    Xneg = O.oracle_X_full(lambda r: O.lattice_index_matrix(N, z, r), tabN, N, -A)
+    assert O.rowmean_relu(Xneg) == 0.0
+
+
+def test_exp_mean_pins():
+    """Config 5's mean of exp(X) (PAPER.md:60-62 with f = exp): (a) A = 0 gives
+    1; (b) all z_j equal to 1 and φ = id: X[n,k] = (n/N)·c_k with c_k = Σ_j
+    A[j,k], so the mean is the geometric sum (1/N)(e^{c} - 1)/(e^{c/N} - 1)."""
+    N, s, t = 257, 4, 6
+    tab = O.phi_table(O.PHI_IDENTITY, N)
+    z = np.ones(s, dtype=np.int64)
+    fn = lambda r: O.lattice_index_matrix(N, z, r)  # noqa: E731
+    X0 = O.oracle_X_full(fn, tab, N, np.zeros((s, t)))
+    np.testing.assert_array_equal(O.column_means(X0, O.F_EXP), np.ones(t))
+    A = np.random.default_rng(12).uniform(-2.0, 2.0, size=(s, t))
+    X = O.oracle_X_full(fn, tab, N, A)
+    c = A.sum(axis=0)
+    want = (np.expm1(c) / np.expm1(c / N)) / N
+    np.testing.assert_allclose(O.column_means(X, O.F_EXP), want, rtol=1e-13, atol=0)
+
+
 # ---------------------------------------------------------------- Korobov p-set (SURVEY §8(f) NEXT #1)
 @pytest.mark.parametrize("K", [5, 7, 11, 13, 31])
 def test_pset_columns_are_uniform_multisets(K):
