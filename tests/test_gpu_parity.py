@@ -487,3 +487,25 @@ def test_k0_variants_bitwise(qmc, monkeypatch, N, s, t):
     X2 = plan.matmul(A).clone()
     torch.cuda.synchronize()
     assert torch.equal(X1, X2)
+
+
+def test_fused_reductions_closed_forms_gpu(qmc):
+    """The fused means against closed forms (no oracle in the loop): equal z,
+    φ = id -> mean exp(X[:,k]) = (1/N)(e^c - 1)/(e^{c/N} - 1), c = Σ_j A[j,k];
+    A >= 0, φ = id -> Q = (N-1)/(2 N t)·Σ A (reading R8, no clipping)."""
+    import torch
+    N, s, t = 65537, 8, 32
+    rng = np.random.default_rng(21)
+    A = rng.uniform(-2.0, 2.0, size=(s, t))
+    plan = qmc.Plan.lattice(N, np.ones(s, dtype=np.int64), W.PHI_IDENTITY)
+    m = plan.mean(qmc.to_device_colmajor(A, "cuda"), W.F_EXP, 0.0).cpu().numpy()
+    c = A.sum(axis=0)
+    np.testing.assert_allclose(m, np.expm1(c) / np.expm1(c / N) / N, rtol=1e-12, atol=0)
+    z = rng.integers(1, N, size=s)
+    Ap = rng.uniform(0.0, 1.0, size=(s, t))
+    plan2 = qmc.Plan.lattice(N, z, W.PHI_IDENTITY)
+    rs = plan2.mean(qmc.to_device_colmajor(Ap, "cuda"), W.F_ROWMEAN_RELU, 0.0)
+    Q = float(plan2.finalize(W.F_ROWMEAN_RELU, rs, t).item())
+    want = (N - 1) / (2 * N * t) * Ap.sum()
+    assert abs(Q - want) <= 1e-12 * want
+    torch.cuda.synchronize()
