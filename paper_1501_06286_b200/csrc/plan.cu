@@ -708,7 +708,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     const int NT = int(sp.L2 / QMC_ROW_E);
     std::vector<int32_t> jq, code, cs, cr;
     int chmax = 0;
-    pl->k1_bal = !getenv("QMC_K1_HEADS") &&
+    pl->k1_bal = !getenv("QMC_K1_HEADS") && k1_try_balanced(s, sp.L2) &&
                  k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2), jq, code, cs, cr,
                                    chmax);
     if (pl->k1_bal) {

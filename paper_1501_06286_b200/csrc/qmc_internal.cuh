@@ -55,8 +55,11 @@ struct PlanLayout {
   size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_zeta, off_W,
       off_tw1, off_tw2, off_twL, off_tws, off_twj, off_jq, off_k1c, off_tmp, total;
 };
-// K1 scatter-input order (plan.cu k1_order): at most k1_s1max(s, L2) slots
-inline int64_t k1_s1max(int64_t s, int64_t L2) { return 2 * s + L2 + 64; }
+// K1 scatter-input order (plan.cu k1_balanced_order): tried when the
+// buckets are small enough to balance (s <= 8·L2), at most k1_s1max slots;
+// otherwise the bucket order, s slots
+inline bool k1_try_balanced(int64_t s, int64_t L2) { return s <= 8 * L2; }
+inline int64_t k1_s1max(int64_t s, int64_t L2) { return k1_try_balanced(s, L2) ? 2 * s + L2 + 64 : s; }
 // K1 balanced order (plan.cu k1_balanced_order): slot codes hold the row
 // index v of the running sum in bits 0..13 — a bucket e2 < L2, the padding
 // slot v = L2, or overflow slot v = L2 + 1 + o (o < kK1Ovf) of a bucket's
@@ -101,7 +104,7 @@ struct qmc_plan {
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
-  // K1 scatter input (plan.cu k1_order): S1 staged slots per pair / per f1
+  // K1 scatter input (plan.cu k1_balanced_order): S1 staged slots per pair / per f1
   // in k1_nch chunks of at most k1_ch slots; k1_bal = 1: balanced
   // thread-major order of bucket pieces (codes: kK1First), 0: bucket order
   int64_t S1;
