@@ -142,6 +142,7 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   const int64_t s1 = k1_s1max(s, sp.L2);
   l.off_e2q = take(size_t(s1) * 4 + 16);
   l.off_occ = take(size_t(sp.L2 / 32 + 1) * 4);
+  l.off_cursor = take(size_t(sp.L2) * 4);
   l.off_zeta = take(size_t(m) * 8);
   l.off_W = take(size_t(sp.L) * 16);
   l.off_tw1 = take(size_t(sp.L1) * 16);
@@ -279,27 +280,72 @@ __global__ void k_colmap(const int64_t* __restrict__ z, int64_t s, const int32_t
 // bent[q] = {j, e_j, e2, end of the bucket if q is its first entry else -1};
 // e2q[q] = e2 | (bucket size << 13) if q is the first entry of its bucket,
 // else e2 (K1 stages e2q; L2 <= 8192); occ = bitmap of the nonempty buckets.
-__global__ void k_buckets(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ bstart,
-                          int4* __restrict__ bent, int32_t* __restrict__ e2q, uint32_t* __restrict__ occ) {
-  extern __shared__ int32_t cursor[];
-  for (int i = threadIdx.x; i <= L2; i += blockDim.x) bstart[i] = 0;
-  __syncthreads();
-  for (int64_t j = threadIdx.x; j < s; j += blockDim.x) atomicAdd(&bstart[(e[j] & (L2 - 1)) + 1], 1);
+// Buckets of the column map by e2 = e_j mod L2, entries of a bucket in
+// increasing j (a stable counting sort, in parallel):
+//   count -> inclusive scan (bstart) -> placement by atomic cursors (any order
+//   within a bucket) -> per bucket, sort its j's (insertion sort) and write
+//   bent / e2q / occ.  The result does not depend on the atomic order.
+__global__ void k_bucket_count(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ bstart) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < s) atomicAdd(&bstart[(e[j] & (L2 - 1)) + 1], 1);
+}
+
+// bstart[0..L2] (bstart[0] = 0) -> inclusive prefix sums; cursor[i] = bstart[i]
+__global__ void __launch_bounds__(1024) k_bucket_scan(int32_t* __restrict__ bstart, int L2,
+                                                      int32_t* __restrict__ cursor) {
+  __shared__ int32_t part[1024];
+  const int n = L2 + 1, per = (n + 1023) / 1024;
+  const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+  int32_t run = 0;
+  for (int i = i0; i < i1; ++i) {
+    run += bstart[i];
+    bstart[i] = run;
+  }
+  part[threadIdx.x] = run;
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int i = 1; i <= L2; ++i) bstart[i] += bstart[i - 1];
-    for (int i = 0; i < L2; ++i) cursor[i] = bstart[i];
-    for (int64_t j = 0; j < s; ++j) {
-      const int ej = e[j];
-      const int pos = cursor[ej & (L2 - 1)]++;
-      const int e2 = ej & (L2 - 1);
-      bent[pos] = make_int4(int(j), ej, e2, pos == bstart[e2] ? bstart[e2 + 1] : -1);
-      e2q[pos] = pos == bstart[e2] ? e2 | ((bstart[e2 + 1] - bstart[e2]) << 13) : e2;
+    int32_t acc = 0;
+    for (int w = 0; w < 1024; ++w) {
+      const int32_t v = part[w];
+      part[w] = acc;
+      acc += v;
     }
-    for (int w = 0; w <= L2 / 32; ++w) occ[w] = 0u;
-    for (int i = 0; i < L2; ++i)
-      if (bstart[i + 1] > bstart[i]) occ[i >> 5] |= 1u << (i & 31);
   }
+  __syncthreads();
+  const int32_t off = part[threadIdx.x];
+  for (int i = i0; i < i1; ++i) {
+    bstart[i] += off;
+    if (i < L2) cursor[i] = bstart[i];
+  }
+}
+
+__global__ void k_bucket_place(const int32_t* __restrict__ e, int64_t s, int L2, int32_t* __restrict__ cursor,
+                               int32_t* __restrict__ slot_j) {
+  const int64_t j = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (j < s) slot_j[atomicAdd(&cursor[e[j] & (L2 - 1)], 1)] = int32_t(j);
+}
+
+// one thread per bucket b: e2q[lo, hi) holds its j's on entry, its codes on exit
+__global__ void k_bucket_finish(const int32_t* __restrict__ e, int L2, const int32_t* __restrict__ bstart,
+                                int32_t* __restrict__ e2q, int4* __restrict__ bent, uint32_t* __restrict__ occ) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= L2) return;
+  const int lo = bstart[b], hi = bstart[b + 1];
+  for (int i = lo + 1; i < hi; ++i) {  // insertion sort by j
+    const int32_t v = e2q[i];
+    int k = i - 1;
+    while (k >= lo && e2q[k] > v) {
+      e2q[k + 1] = e2q[k];
+      --k;
+    }
+    e2q[k + 1] = v;
+  }
+  for (int pos = lo; pos < hi; ++pos) {
+    const int j = e2q[pos];
+    bent[pos] = make_int4(j, e[j], b, pos == lo ? hi : -1);
+  }
+  for (int pos = lo; pos < hi; ++pos) e2q[pos] = pos == lo ? b | ((hi - lo) << 13) : b;
+  if (hi > lo) atomicOr(&occ[b >> 5], 1u << (b & 31));
 }
 
 __global__ void k_rtable(const int32_t* __restrict__ L, int64_t N, int64_t m, int32_t* __restrict__ R) {
@@ -633,6 +679,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   std::vector<int64_t> qf = host_prime_factors(m);
   int64_t* d_z = (int64_t*)(b + lay.off_tmp);
   int64_t* d_qf = d_z + s;
+  int32_t* d_cursor = (int32_t*)(b + lay.off_cursor);  // plan-time bucket cursors
   unsigned long long* d_flag = (unsigned long long*)(d_qf + 64);
   auto cleanup = [&]() { cudaStreamSynchronize(st); };
 #define QMC_PLAN_CHECK(expr)              \
@@ -682,8 +729,16 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_colmap<<<blocks(s, 256), 256, 0, st>>>(d_z, s, pl->d_L, pl->d_e);
   QMC_PLAN_LAUNCHED();
-  k_buckets<<<1, 1024, size_t(sp.L2) * 4, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart, pl->d_bent, pl->d_e2q,
-                                                 pl->d_occ);
+  QMC_PLAN_CHECK(cudaMemsetAsync(pl->d_bstart, 0, size_t(sp.L2 + 1) * 4, st) ? QMC_ECUDA : 0);
+  QMC_PLAN_CHECK(cudaMemsetAsync(pl->d_occ, 0, size_t(sp.L2 / 32 + 1) * 4, st) ? QMC_ECUDA : 0);
+  k_bucket_count<<<blocks(s, 256), 256, 0, st>>>(pl->d_e, s, int(sp.L2), pl->d_bstart);
+  QMC_PLAN_LAUNCHED();
+  k_bucket_scan<<<1, 1024, 0, st>>>(pl->d_bstart, int(sp.L2), d_cursor);
+  QMC_PLAN_LAUNCHED();
+  k_bucket_place<<<blocks(s, 256), 256, 0, st>>>(pl->d_e, s, int(sp.L2), d_cursor, pl->d_e2q);
+  QMC_PLAN_LAUNCHED();
+  k_bucket_finish<<<blocks(sp.L2, 128), 128, 0, st>>>(pl->d_e, int(sp.L2), pl->d_bstart, pl->d_e2q, pl->d_bent,
+                                                       pl->d_occ);
   QMC_PLAN_LAUNCHED();
   k_rtable<<<blocks(N, 256), 256, 0, st>>>(pl->d_L, N, m, pl->d_R);
   QMC_PLAN_LAUNCHED();

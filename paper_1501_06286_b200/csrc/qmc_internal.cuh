@@ -52,7 +52,7 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // Plan-workspace carve-up (device pointers), identical for the size query
 // and the create call.
 struct PlanLayout {
-  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_zeta, off_W,
+  size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_cursor, off_zeta, off_W,
       off_tw1, off_tw2, off_twL, off_tws, off_twj, off_jq, off_k1c, off_tmp, total;
 };
 // K1 scatter-input order (plan.cu k1_balanced_order): tried when the
