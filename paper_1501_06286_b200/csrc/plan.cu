@@ -6,7 +6,7 @@
 //       or check x generates F_2[x]/p (p primitive, R2)          k_check_poly
 //   a1  P[k] = β^k mod N  /  x^k mod p      k_pow_table
 //   a2  L[P[k]] = k, L[0] = -1      k_log_table
-//   a3  e_j = L[z_j] = c_j - 1; buckets by e_j mod L2           k_colmap, k_buckets
+//   a3  e_j = L[z_j] = c_j - 1; buckets by e_j mod L2           k_colmap, k_bucket_*
 //       R[n] = (m - L[n]) mod m  (conventional row n is reordered row R[n])
 //   a4  ζ_k = φ(u(P[k])); W = DFT_L(K)/L     k_zeta, k_spectrum_rows
 //
