@@ -184,7 +184,7 @@ def qmc_plan_info(plan) -> dict:
     buf = (C.c_int64 * 16)()
     _check(_lib.qmc_plan_info(plan, buf), "qmc_plan_info")
     keys = ["family", "N", "m", "s", "phi", "gen", "L", "L1", "L2", "batch_pairs", "D", "p",
-            "k1_balanced", "k1_slots", "k1_chunks", "k1_chunk_slots"]
+            "k1_order", "k1_slots", "k1_chunks", "k1_chunk_slots"]
     return dict(zip(keys, list(buf)))
 
 

@@ -117,6 +117,48 @@ __global__ void __launch_bounds__(256) k_pack_smem(const double* __restrict__ A,
   }
 }
 
+// Dense input (plan->k1_dense: every e holds at most one entry and s is too
+// large for the sparse first pass, e.g. the CBC all-generators plan):
+//   k_pack_dense  a'[p][e] = (A[j(e), k1], A[j(e), k2]) (0 where no j), j(e) = jq[e]
+//   k_dense_cols  T[p][f1][e2] = ω_L^{e2 f1} Σ_{e1} a'[p][L2 e1 + e2] ω_{L1}^{e1 f1}
+//                 (the first DFT dimension, an L1-point DFT per column e2)
+// K1 then loads its row T[p][f1][:] instead of scattering.
+__global__ void k_pack_dense(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
+                             const int32_t* __restrict__ jq, int64_t L, double2* __restrict__ ad) {
+  const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
+  if (e >= L) return;
+  const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
+  const int j = __ldg(&jq[e]);
+  ad[int64_t(p) * L + e] = j < 0 ? make_double2(0.0, 0.0)
+                                 : make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
+}
+
+template <int L1>
+__global__ void __launch_bounds__(256) k_dense_cols(const double2* __restrict__ ad, int64_t L, int L2,
+                                                    const double2* __restrict__ tw1,
+                                                    const double2* __restrict__ twL, double2* __restrict__ T,
+                                                    int64_t ldT) {
+  const int e2 = blockIdx.x * blockDim.x + threadIdx.x;
+  const int p = blockIdx.y;
+  if (e2 >= L2) return;
+  const double2* src = ad + int64_t(p) * L + e2;
+  double2 v[L1];
+#pragma unroll
+  for (int e1 = 0; e1 < L1; ++e1) v[e1] = src[int64_t(e1) * L2];
+  reg_dft<L1, -1>(v, tw1);
+  // × ω_L^{e2 f1} = w^f1, w = ω_L^{e2}: running products
+  const double2 w = __ldg(&twL[e2]);
+  double2 tw = w;
+  double2* dst = T + int64_t(p) * ldT + e2;
+  dst[0] = v[0];
+#pragma unroll
+  for (int f1 = 1; f1 < L1; ++f1) {
+    dst[int64_t(f1) * L2] = cmul(v[f1], tw);
+    tw = cmul(tw, w);
+  }
+}
+
 // ---------------------------------------------------------------- K1
 // Persistent: CTA b takes the items (f1, p) = b, b + gridDim.x, ... (f1
 // fastest) of the batch; L2/16 threads, 16 points per thread.  Per item:
@@ -172,6 +214,7 @@ struct K1Args {
   int CH;                              // staging slots (capacity)
   const int32_t* __restrict__ k1c;     // [nch+1] chunk starts, [nch] regular-round slots
   int nch, bal;
+  int dense;                           // asort holds T[p][f1][e2] (k_dense_cols): no scatter
   const double2* __restrict__ twj;     // [L1][S1]
   const double2* __restrict__ tws;     // row-FFT stage twiddles
   const double2* __restrict__ W;       // [L1][L2] spectrum
@@ -316,7 +359,11 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
   }
   QMC_TS(1);
   double2 v[E];
-  {
+  if (a.dense) {  // the first DFT dimension was done by k_dense_cols: load the row
+    const double2* Tr = a.asort + int64_t(p) * a.S1 + int64_t(f1) * L2 + tid_fresh();
+#pragma unroll
+    for (int q = 0; q < E; ++q) v[q] = Tr[q * NT];
+  } else {
     // nonempty buckets only (the rest of S is stale); NT is a multiple of 32
     const int t0 = tid_fresh();
     const double2* Sb = S + padE<E>(t0);
@@ -362,7 +409,7 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
   const int nitems = a.L1 * a.np;
   if (threadIdx.x == 0) mbar_init(sm.bar, 1);
   __syncthreads();
-  if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sm, blockIdx.x, 0);
+  if (threadIdx.x == 0 && int(blockIdx.x) < nitems && a.nch > 0) k1_issue<L2>(a, sm, blockIdx.x, 0);
   unsigned phase = 0;
   for (int item = blockIdx.x; item < nitems; item += gridDim.x)
     k1_item<L2>(a, sm, phase, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1);
@@ -1125,6 +1172,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   a.k1c = pl->d_k1c;
   a.nch = pl->k1_nch;
   a.bal = pl->k1_bal;
+  a.dense = pl->k1_dense;
   a.twj = pl->d_twj;
   a.tws = pl->d_tws;
   a.W = pl->d_W;
@@ -1303,6 +1351,21 @@ static int cols_dispatch(const qmc_plan* pl, const CallLayout& cl, const double2
 
 static unsigned nblk(int64_t n, int b) { return unsigned((n + b - 1) / b); }
 
+static int dense_cols_dispatch(const qmc_plan* pl, const double2* ad, int np, double2* T, cudaStream_t st) {
+  const dim3 g(nblk(pl->sp.L2, 256), unsigned(np));
+  switch (pl->sp.L1) {
+#define QMC_DENSE_CASE(NN)                                                                                      \
+  case NN:                                                                                                      \
+    k_dense_cols<NN><<<g, 256, 0, st>>>(ad, pl->sp.L, int(pl->sp.L2), pl->d_tw1, pl->d_twL, T, pl->S1);          \
+    QMC_LAUNCHED();                                                                                             \
+    return QMC_OK;
+    QMC_DENSE_CASE(1) QMC_DENSE_CASE(2) QMC_DENSE_CASE(3) QMC_DENSE_CASE(4) QMC_DENSE_CASE(5) QMC_DENSE_CASE(6)
+    QMC_DENSE_CASE(8) QMC_DENSE_CASE(9) QMC_DENSE_CASE(10) QMC_DENSE_CASE(12) QMC_DENSE_CASE(15) QMC_DENSE_CASE(16)
+#undef QMC_DENSE_CASE
+  }
+  return QMC_EINVAL_N;
+}
+
 // all batches of column pairs; f = -1: X only.  A_host != NULL: each batch
 // first copies its own columns of A from the host (A_host, leading dimension
 // lda_host) into A on the batch's stream, so that the copy of one batch
@@ -1362,7 +1425,14 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
         return QMC_ECUDA;
     }
     prof_begin(KC_PACK, bs);
-    if (pl->s <= kPackSmemMax && !getenv("QMC_PACK_GATHER")) {
+    if (pl->k1_dense) {
+      // a' into this set's U (K1 overwrites it afterwards), T into asort
+      k_pack_dense<<<dim3(nblk(pl->sp.L, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, pl->d_jq, pl->sp.L,
+                                                                          U);
+      QMC_LAUNCHED();
+      int rc0 = dense_cols_dispatch(pl, U, np, asort, bs);
+      if (rc0) return rc0;
+    } else if (pl->s <= kPackSmemMax && !getenv("QMC_PACK_GATHER")) {
       const size_t psm = size_t(pl->s) * 16;
       set_smem_attr(k_pack_smem, psm);
       // slices of the slots: ~2 CTAs of work per SM in total

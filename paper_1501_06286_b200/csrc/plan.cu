@@ -139,7 +139,7 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_e = take(size_t(s) * 4);
   l.off_bstart = take(size_t(sp.L2 + 1) * 4);
   l.off_bent = take(size_t(s) * 16);
-  const int64_t s1 = k1_s1max(s, sp.L2);
+  const int64_t s1 = k1_s1max(s, sp.L2, sp.L);
   l.off_e2q = take(size_t(s1) * 4 + 16);
   l.off_occ = take(size_t(sp.L2 / 32 + 1) * 4);
   l.off_cursor = take(size_t(sp.L2) * 4);
@@ -764,9 +764,31 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     std::vector<int32_t> jq, code, cs, cr;
     int chmax = 0;
     pl->k1_bal = !getenv("QMC_K1_HEADS") && k1_try_balanced(s, sp.L2) &&
-                 k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2), jq, code, cs, cr,
+                 k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2, sp.L), jq, code, cs, cr,
                                    chmax);
-    if (pl->k1_bal) {
+    // dense input: the balanced order does not apply, a' is at least half
+    // full with every e_j distinct (a permutation, as in the CBC
+    // all-generators plan), and an L1-point column DFT in registers
+    // (k_dense_cols); L slots fit k1_s1max (2s >= L)
+    bool distinct = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) == 1 && sp.L1 <= 16 &&
+                    !getenv("QMC_K1_HEADS");
+    std::vector<int32_t> jofe;
+    if (distinct) {
+      jofe.assign(size_t(sp.L), -1);
+      for (int64_t q = 0; q < s && distinct; ++q) {
+        const int4 be = hbent[q];
+        if (jofe[be.y] >= 0) distinct = false;
+        jofe[be.y] = be.x;
+      }
+    }
+    pl->k1_dense = distinct ? 1 : 0;
+    if (pl->k1_dense) {
+      jq.swap(jofe);
+      cs.assign(1, 0);
+      cr.clear();
+      pl->S1 = sp.L;
+      pl->k1_ch = 4;
+    } else if (pl->k1_bal) {
       pl->S1 = int64_t(jq.size());
       pl->k1_ch = chmax;
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
@@ -790,8 +812,10 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     QMC_PLAN_CHECK(cudaMemcpy(pl->d_jq, jq.data(), 4 * jq.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     QMC_PLAN_CHECK(cudaMemcpy(pl->d_k1c, cs.data(), 4 * cs.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
   }
-  k_twj<<<blocks(sp.L1 * pl->S1, 256), 256, 0, st>>>(pl->d_jq, pl->d_e, pl->S1, sp.L, int(sp.L1), pl->d_twj);
-  QMC_PLAN_LAUNCHED();
+  if (!pl->k1_dense) {  // the dense first pass needs no per-entry twiddles
+    k_twj<<<blocks(sp.L1 * pl->S1, 256), 256, 0, st>>>(pl->d_jq, pl->d_e, pl->S1, sp.L, int(sp.L1), pl->d_twj);
+    QMC_PLAN_LAUNCHED();
+  }
   QMC_PLAN_CHECK(spectrum_dispatch(pl));
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
 #undef QMC_PLAN_CHECK
@@ -864,7 +888,7 @@ int qmc_plan_info(qmc_plan_t pl, int64_t* info) {
   info[9] = pl->batch_pairs;
   info[10] = pl->D;
   info[11] = int64_t(pl->p);
-  info[12] = pl->k1_bal;
+  info[12] = pl->k1_dense ? 2 : pl->k1_bal;
   info[13] = pl->S1;
   info[14] = pl->k1_nch;
   info[15] = pl->k1_ch;

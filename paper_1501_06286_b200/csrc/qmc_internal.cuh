@@ -57,9 +57,12 @@ struct PlanLayout {
 };
 // K1 scatter-input order (plan.cu k1_balanced_order): tried when the
 // buckets are small enough to balance (s <= 8·L2), at most k1_s1max slots;
-// otherwise the bucket order, s slots
+// otherwise the bucket order (s slots) or, when every e_j is distinct, the
+// dense input of L slots (pipeline.cu k_dense_cols)
 inline bool k1_try_balanced(int64_t s, int64_t L2) { return s <= 8 * L2; }
-inline int64_t k1_s1max(int64_t s, int64_t L2) { return k1_try_balanced(s, L2) ? 2 * s + L2 + 64 : s; }
+inline int64_t k1_s1max(int64_t s, int64_t L2, int64_t L) {
+  return k1_try_balanced(s, L2) ? 2 * s + L2 + 64 : (s > L ? s : L);
+}
 // K1 balanced order (plan.cu k1_balanced_order): slot codes hold the row
 // index v of the running sum in bits 0..13 — a bucket e2 < L2, the padding
 // slot v = L2, or overflow slot v = L2 + 1 + o (o < kK1Ovf) of a bucket's
@@ -109,6 +112,7 @@ struct qmc_plan {
   // thread-major order of bucket pieces (codes: kK1First), 0: bucket order
   int64_t S1;
   int k1_bal, k1_nch, k1_ch;
+  int k1_dense;  // 1: dense first pass (k_pack_dense + k_dense_cols), S1 = L, no chunks
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
   // caller's stream) so one batch's K1 overlaps the previous batch's K2/K3

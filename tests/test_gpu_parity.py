@@ -461,9 +461,9 @@ def test_k1_scatter_orders(qmc, monkeypatch, N, s, t, heads):
     w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=N + s)
     plan = qmc.Plan.from_workload(w)
     if heads:
-        assert plan.info["k1_balanced"] == 0 and plan.info["k1_slots"] == s
+        assert plan.info["k1_order"] == 0 and plan.info["k1_slots"] == s
     elif s <= 8192:
-        assert plan.info["k1_balanced"] == 1
+        assert plan.info["k1_order"] == 1
     A = qmc.to_device_colmajor(w.A, "cuda")
     X = plan.matmul(A)
     rows = sample_rows(w.N, 128, seed=s)
@@ -509,3 +509,34 @@ def test_fused_reductions_closed_forms_gpu(qmc):
     want = (N - 1) / (2 * N * t) * Ap.sum()
     assert abs(Q - want) <= 1e-12 * want
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("N,t", [(7681, 6), (40961, 4), (65537, 4)])
+def test_dense_input_all_generators(qmc, N, t):
+    """The all-generators plan (z = 1..N-1, s = m, as in the CBC search) takes
+    the dense first pass (k_pack_dense + k_dense_cols, plan info k1_order 2):
+    X against the oracle on sampled rows (all rows for N = 7681), and against
+    the bucket-order path (QMC_K1_HEADS) within the bar."""
+    import os
+    import torch
+    s = N - 1
+    w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=N)
+    w.z = np.arange(1, N, dtype=np.int64)
+    plan = qmc.Plan.from_workload(w)
+    assert plan.info["k1_order"] == 2 and plan.info["k1_slots"] == plan.info["L"]
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = plan.matmul(A)
+    if N <= 8000:
+        check_X(w, X.cpu().numpy(), X_full(w))
+    else:
+        rows = sample_rows(w.N, 64, seed=N)
+        Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+        check_X(w, Xs, X_rows(w, rows))
+    os.environ["QMC_K1_HEADS"] = "1"
+    try:
+        plan_h = qmc.Plan.from_workload(w)
+    finally:
+        del os.environ["QMC_K1_HEADS"]
+    assert plan_h.info["k1_order"] == 0
+    Xh = plan_h.matmul(A)
+    check_X(w, X.cpu().numpy(), Xh.cpu().numpy())
