@@ -159,6 +159,61 @@ __global__ void __launch_bounds__(256) k_dense_cols(const double2* __restrict__ 
   }
 }
 
+// L1 = R·M > 16: two register stages through shared memory.  CTA = (pair,
+// 32 columns e2); e1 = r + R·mm, f1 = k2 + M·k1:
+//   stage A, item (c, r): y[k2] = ω_{L1}^{r k2} Σ_mm a'[L2 (r + R mm) + e2] ω_M^{mm k2}
+//   stage B, item (c, k2): T[f1 = k2 + M k1] = ω_L^{e2 f1} Σ_r y_r[k2] ω_R^{r k1}
+// columns per CTA of k_dense_cols2 (static shared memory ≤ 48 KB)
+__host__ __device__ constexpr int dense2_cb(int L1) { return L1 > 128 ? 8 : (L1 > 64 ? 16 : 32); }
+
+template <int R, int M>
+__global__ void __launch_bounds__(256) k_dense_cols2(const double2* __restrict__ ad, int64_t L, int L2,
+                                                     const double2* __restrict__ tw1,
+                                                     const double2* __restrict__ twL, double2* __restrict__ T,
+                                                     int64_t ldT) {
+  constexpr int L1 = R * M, CB = dense2_cb(L1), LP = L1 | 1;
+  __shared__ double2 Y[CB * LP];  // [c][r·M + k2]
+  const int p = blockIdx.y, e20 = blockIdx.x * CB;
+  const double2* src = ad + int64_t(p) * L;
+  for (int it = threadIdx.x; it < CB * R; it += blockDim.x) {
+    const int c = it % CB, r = it / CB;
+    const int e2 = e20 + c;
+    double2 x[M];
+#pragma unroll
+    for (int mm = 0; mm < M; ++mm)
+      x[mm] = e2 < L2 ? src[int64_t(r + R * mm) * L2 + e2] : make_double2(0.0, 0.0);
+    reg_dft<M, -1>(x, tw1, L1 / M);
+#pragma unroll
+    for (int k2 = 1; k2 < M; ++k2)
+      if (r) x[k2] = cmul(x[k2], __ldg(&tw1[r * k2]));
+#pragma unroll
+    for (int k2 = 0; k2 < M; ++k2) Y[c * LP + r * M + k2] = x[k2];
+  }
+  __syncthreads();
+  double2* dst = T + int64_t(p) * ldT;
+  for (int it = threadIdx.x; it < CB * M; it += blockDim.x) {
+    const int c = it % CB, k2 = it / CB;
+    const int e2 = e20 + c;
+    if (e2 >= L2) continue;
+    double2 z[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[r] = Y[c * LP + r * M + k2];
+    reg_dft<R, -1>(z, tw1, L1 / R);
+    // × ω_L^{e2 f1}, f1 = k2 + M k1: ω_L^{e2 k2} · (ω_L^{e2 M})^{k1}
+    const double2 w = __ldg(&twL[e2]);
+    double2 b = make_double2(1.0, 0.0);
+    for (int q = 0; q < k2; ++q) b = cmul(b, w);
+    double2 wM = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int q = 0; q < M; ++q) wM = cmul(wM, w);
+#pragma unroll
+    for (int k1 = 0; k1 < R; ++k1) {
+      dst[int64_t(k2 + M * k1) * L2 + e2] = cmul(z[k1], b);
+      b = cmul(b, wM);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K1
 // Persistent: CTA b takes the items (f1, p) = b, b + gridDim.x, ... (f1
 // fastest) of the batch; L2/16 threads, 16 points per thread.  Per item:
@@ -1363,6 +1418,16 @@ static int dense_cols_dispatch(const qmc_plan* pl, const double2* ad, int np, do
     QMC_DENSE_CASE(8) QMC_DENSE_CASE(9) QMC_DENSE_CASE(10) QMC_DENSE_CASE(12) QMC_DENSE_CASE(15) QMC_DENSE_CASE(16)
 #undef QMC_DENSE_CASE
   }
+  const int R = k2_split_R(pl->sp.L1), M = int(pl->sp.L1) / std::max(R, 1);
+  const dim3 g2(nblk(pl->sp.L2, dense2_cb(int(pl->sp.L1))), unsigned(np));
+#define QMC_DENSE2_CASE(RR, MM)                                                                                   \
+  if (RR > 1 && R == RR && M == MM) {                                                                             \
+    k_dense_cols2<RR, MM><<<g2, 256, 0, st>>>(ad, pl->sp.L, int(pl->sp.L2), pl->d_tw1, pl->d_twL, T, pl->S1);     \
+    QMC_LAUNCHED();                                                                                               \
+    return QMC_OK;                                                                                                \
+  }
+  QMC_K2_SPLITS(QMC_DENSE2_CASE)
+#undef QMC_DENSE2_CASE
   return QMC_EINVAL_N;
 }
 

@@ -768,10 +768,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
                                    chmax);
     // dense input: the balanced order does not apply, a' is at least half
     // full with every e_j distinct (a permutation, as in the CBC
-    // all-generators plan), and an L1-point column DFT in registers
-    // (k_dense_cols); L slots fit k1_s1max (2s >= L)
-    bool distinct = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) == 1 && sp.L1 <= 16 &&
-                    !getenv("QMC_K1_HEADS");
+    // all-generators plan); L slots fit k1_s1max (2s >= L)
+    bool distinct = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS");
     std::vector<int32_t> jofe;
     if (distinct) {
       jofe.assign(size_t(sp.L), -1);

@@ -511,10 +511,11 @@ def test_fused_reductions_closed_forms_gpu(qmc):
     torch.cuda.synchronize()
 
 
-@pytest.mark.parametrize("N,t", [(7681, 6), (40961, 4), (65537, 4)])
+@pytest.mark.parametrize("N,t", [(7681, 6), (40961, 4), (65537, 4), (25601, 4)])
 def test_dense_input_all_generators(qmc, N, t):
     """The all-generators plan (z = 1..N-1, s = m, as in the CBC search) takes
-    the dense first pass (k_pack_dense + k_dense_cols, plan info k1_order 2):
+    the dense first pass (k_pack_dense + k_dense_cols / k_dense_cols2 for
+    L1 = 25 = 5·5 at N = 25601; plan info k1_order 2):
     X against the oracle on sampled rows (all rows for N = 7681), and against
     the bucket-order path (QMC_K1_HEADS) within the bar."""
     import os
