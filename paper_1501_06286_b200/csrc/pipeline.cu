@@ -119,19 +119,27 @@ __global__ void __launch_bounds__(256) k_pack_smem(const double* __restrict__ A,
 
 // Dense input (plan->k1_dense: every e holds at most one entry and s is too
 // large for the sparse first pass, e.g. the CBC all-generators plan):
-//   k_pack_dense  a'[p][e] = (A[j(e), k1], A[j(e), k2]) (0 where no j), j(e) = jq[e]
+//   k_pack_dense  a'[p][e] = Σ_{j: e_j = e} (A[j, k1], A[j, k2]) in j order
+//                 (jlist / estart: the entries sorted by e, plan.cu)
 //   k_dense_cols  T[p][f1][e2] = ω_L^{e2 f1} Σ_{e1} a'[p][L2 e1 + e2] ω_{L1}^{e1 f1}
 //                 (the first DFT dimension, an L1-point DFT per column e2)
 // K1 then loads its row T[p][f1][:] instead of scattering.
 __global__ void k_pack_dense(const double* __restrict__ A, int64_t lda, int64_t t, int64_t pair0,
-                             const int32_t* __restrict__ jq, int64_t L, double2* __restrict__ ad) {
+                             const int32_t* __restrict__ jlist, const int32_t* __restrict__ estart, int64_t L,
+                             double2* __restrict__ ad) {
   const int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   const int p = blockIdx.y;
   if (e >= L) return;
   const int64_t k1 = 2 * (pair0 + p), k2 = k1 + 1;
-  const int j = __ldg(&jq[e]);
-  ad[int64_t(p) * L + e] = j < 0 ? make_double2(0.0, 0.0)
-                                 : make_double2(__ldg(&A[k1 * lda + j]), k2 < t ? __ldg(&A[k2 * lda + j]) : 0.0);
+  const double* a1 = A + k1 * lda;
+  const double* a2 = A + k2 * lda;
+  double2 acc = make_double2(0.0, 0.0);
+  for (int q = __ldg(&estart[e]), q1 = __ldg(&estart[e + 1]); q < q1; ++q) {
+    const int j = __ldg(&jlist[q]);
+    acc.x += __ldg(&a1[j]);
+    if (k2 < t) acc.y += __ldg(&a2[j]);
+  }
+  ad[int64_t(p) * L + e] = acc;
 }
 
 template <int L1>
@@ -1492,8 +1500,8 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     prof_begin(KC_PACK, bs);
     if (pl->k1_dense) {
       // a' into this set's U (K1 overwrites it afterwards), T into asort
-      k_pack_dense<<<dim3(nblk(pl->sp.L, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, pl->d_jq, pl->sp.L,
-                                                                          U);
+      k_pack_dense<<<dim3(nblk(pl->sp.L, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, pl->d_jq,
+                                                                          pl->d_e2q, pl->sp.L, U);
       QMC_LAUNCHED();
       int rc0 = dense_cols_dispatch(pl, U, np, asort, bs);
       if (rc0) return rc0;

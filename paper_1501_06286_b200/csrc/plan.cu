@@ -766,22 +766,23 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     pl->k1_bal = !getenv("QMC_K1_HEADS") && k1_try_balanced(s, sp.L2) &&
                  k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2, sp.L), jq, code, cs, cr,
                                    chmax);
-    // dense input: the balanced order does not apply, a' is at least half
-    // full with every e_j distinct (a permutation, as in the CBC
-    // all-generators plan); L slots fit k1_s1max (2s >= L)
-    bool distinct = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS");
-    std::vector<int32_t> jofe;
-    if (distinct) {
-      jofe.assign(size_t(sp.L), -1);
-      for (int64_t q = 0; q < s && distinct; ++q) {
-        const int4 be = hbent[q];
-        if (jofe[be.y] >= 0) distinct = false;
-        jofe[be.y] = be.x;
-      }
-    }
-    pl->k1_dense = distinct ? 1 : 0;
+    // dense input: the balanced order does not apply and a' is at least half
+    // full (e.g. the CBC all-generators plan, a permutation); entries sorted
+    // by e (then j) with per-e starts, so k_pack_dense sums collisions in j
+    // order.  jlist (s) fits jq and estart (L+1) fits e2q: both hold
+    // k1_s1max >= L slots when 2s >= L
+    pl->k1_dense = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS") &&
+                   !getenv("QMC_NO_DENSE");
     if (pl->k1_dense) {
-      jq.swap(jofe);
+      std::vector<int32_t> estart(size_t(sp.L) + 1, 0), jlist(static_cast<size_t>(s));
+      for (int64_t q = 0; q < s; ++q) ++estart[size_t(hbent[q].y) + 1];
+      for (int64_t e = 0; e < sp.L; ++e) estart[e + 1] += estart[e];
+      std::vector<int32_t> cur(estart.begin(), estart.end() - 1);
+      std::vector<int32_t> eofj(static_cast<size_t>(s));
+      for (int64_t q = 0; q < s; ++q) eofj[hbent[q].x] = hbent[q].y;
+      for (int64_t j = 0; j < s; ++j) jlist[cur[eofj[j]]++] = int32_t(j);  // j order within each e
+      jq.swap(jlist);
+      QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, estart.data(), 4 * estart.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
       cs.assign(1, 0);
       cr.clear();
       pl->S1 = sp.L;

@@ -541,3 +541,23 @@ def test_dense_input_all_generators(qmc, N, t):
     assert plan_h.info["k1_order"] == 0
     Xh = plan_h.matmul(A)
     check_X(w, X.cpu().numpy(), Xh.cpu().numpy())
+
+
+@pytest.mark.parametrize("N,s,t", [(7681, 15360, 4), (65537, 70000, 2)])
+def test_dense_input_with_collisions(qmc, monkeypatch, N, s, t):
+    """Dense first pass with repeated columns (s > m, i.i.d. z): k_pack_dense
+    sums the entries of each e in j order; X on sampled rows against the
+    oracle and against the sparse path (QMC_NO_DENSE) within the bar."""
+    import torch
+    w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=N + s)
+    plan = qmc.Plan.from_workload(w)
+    assert plan.info["k1_order"] == 2
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    X = plan.matmul(A)
+    rows = sample_rows(w.N, 64, seed=s)
+    Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    check_X(w, Xs, X_rows(w, rows))
+    monkeypatch.setenv("QMC_NO_DENSE", "1")
+    plan_s = qmc.Plan.from_workload(w)
+    assert plan_s.info["k1_order"] != 2
+    check_X(w, X.cpu().numpy(), plan_s.matmul(A).cpu().numpy())
