@@ -15,10 +15,6 @@
 #pragma once
 #include <cuda_runtime.h>
 
-#ifndef QMC_TW_RECUR
-#define QMC_TW_RECUR 1
-#endif
-
 namespace qmc {
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
@@ -294,16 +290,7 @@ __device__ __forceinline__ void row_fft(double2* S, const double2* __restrict__ 
 
 namespace qmc {
 
-// ----------------------------------------------------------------- register row FFT
-// Length-N FFT with E points per thread (E = 8 or 16, NT = N/E threads):
-// thread `tid` holds element tid + NT·q in v[q] before and after the
-// transform (natural order, strided).  Stages are radix E (plus one smaller
-// radix stage when N is not a power of E); between stages the row is
-// exchanged through shared memory S (padding of one slot per E elements),
-// two barriers per exchange.  A forward transform, a pointwise product and
-// an inverse transform therefore never round-trip through shared memory
-// between them.
-
+// ----------------------------------------------------------------- register row FFT helpers
 // %tid.x read through volatile asm: addresses derived from it cannot be
 // hoisted above the point of use, so each stage holds only its own
 // shared-memory / twiddle addresses live (instead of all stages' at once).
@@ -317,185 +304,313 @@ template <int E> struct Lg;
 template <> struct Lg<8> { static constexpr int v = 3; };
 template <> struct Lg<16> { static constexpr int v = 4; };
 
-// padded shared-memory index: all 8-thread phases of the stage loads and
-// stores hit distinct bank groups; every address of a stage is a per-thread
-// base plus a compile-time offset
+// padded shared-memory index (one pad slot per E elements)
 template <int E>
 __device__ __forceinline__ int padE(int i) { return i + (i >> Lg<E>::v); }
-template <int N, int E> struct PadE { static constexpr int size = N + N / E; };
-__device__ __forceinline__ int swz16(int i) { return padE<16>(i); }
-template <int N> struct Pad16 { static constexpr int size = PadE<N, 16>::size; };
 
-// radix plan: log_E(N) radix-E stages, then the remainder
-template <int N, int E> struct RPlan {
-  static constexpr int count = (N >= E) ? 1 + RPlan<(N >= E ? N / E : 1), E>::count : (N > 1 ? 1 : 0);
-  static __host__ __device__ constexpr int get(int i) {
-    return i == 0 ? (N >= E ? E : N) : RPlan<(N >= E ? N / E : 1), E>::get(i - 1);
+// ----------------------------------------------------------------- DIF / DIT register row FFT (K1)
+// Length-L2 row held by NT = L2/16 threads, 16 points each; on entry and on
+// exit of the round trip thread t holds v[q] = x[t + NT·q] (natural order).
+// L2 = RHO·SUB with SUB = 16^K ∈ {16, 256, 4096} and RHO ∈ {1, 2, 4, 8}.
+//
+// Forward (decimation in frequency): an in-register radix-RHO stage over
+// the stride-L2/RHO pairs a thread already holds (RHO > 1), then per
+// sub-transform of SUB points (G = SUB/16 threads) radix-16 stages whose
+// exchanges shrink from the whole sub (G threads) to one half-warp (16
+// threads), each stage's 16 outputs twiddled by ω_n^{j·k}.  The spectrum
+// ends in digit-reversed order (dif_freq gives the frequency of register r
+// of thread t); the pointwise product uses a spectrum stored in that order,
+// and the inverse (decimation in time) mirrors every step, so no reordering
+// pass exists.  Every exchange writes exactly the shared-memory slots the
+// same thread read in the previous exchange, so one barrier per exchange
+// suffices, at the exchange's own scope: the CTA (RHO-stage, or SUB = L2),
+// half the CTA (named barrier, L2 = 8192), or the half-warp (__syncwarp).
+// Region of sub c: c·REG + lay(r, j) with lay = 272 r + j + (j >> 4)
+// (SUB = 4096), 17 r + j (SUB = 256), r (SUB = 16); padE<16>(t + NT q) is the
+// same slot, so the scatter's row and the region layouts coincide.
+template <int L2>
+struct Dif {
+  static constexpr int NT = L2 / 16;
+  static constexpr int SUB = L2 >= 4096 ? 4096 : (L2 >= 256 ? 256 : 16);
+  static constexpr int RHO = L2 / SUB;
+  static constexpr int G = SUB / 16;
+  static constexpr int REG = SUB / 16 * 17;
+  static_assert(RHO == 1 || RHO == 2 || RHO == 4 || RHO == 8, "unsupported row length");
+};
+
+// frequency index (natural order) of register r of thread t after dif_fwd
+template <int L2>
+__host__ __device__ inline int dif_freq(int t, int r) {
+  constexpr int G = Dif<L2>::G, RHO = Dif<L2>::RHO;
+  int o = 0, sg = 1, j = t;
+  if (RHO > 1) {
+    o = t / G;
+    j = t % G;
+    sg = RHO;
   }
-};
-template <int E> struct RPlan<1, E> {
-  static constexpr int count = 0;
-  static __host__ __device__ constexpr int get(int) { return 1; }
-};
+  for (int g = G; g > 1; g /= 16) {
+    const int gp = g / 16;
+    o += sg * (j / gp);
+    j %= gp;
+    sg *= 16;
+  }
+  return o + sg * r;
+}
 
-// One radix-R stage on registers.  twS = this stage's twiddle table,
-// stage-major: twS[(r-1)·NS + k] = ω_{NS·R}^{k·r} (forward sign), so the
-// loads of consecutive threads (consecutive k) are contiguous.
-template <int R, int N, int E, int NS, int DIR>
-__device__ __forceinline__ void reg_stage(double2 (&v)[E], const double2* __restrict__ twS, int tid) {
-  constexpr int NT = N / E, BPT = E / R;
-#pragma unroll
-  for (int b = 0; b < BPT; ++b) {
-    double2 u[R];
-#pragma unroll
-    for (int r = 0; r < R; ++r) u[r] = v[b + r * BPT];
-    if (NS > 1) {
-      const double2* twk = twS + (tid_fresh() + b * NT) % NS;
-#if QMC_TW_RECUR
-      // one load; w^r by a product tree of depth <= 4 (w^r = w^{r/2} w^{r-r/2})
-      double2 pw[R];
-      pw[1] = twid<DIR>(ldg_ordered(twk));
-#pragma unroll
-      for (int r = 2; r < R; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
-#pragma unroll
-      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], pw[r]);
-#else
-#pragma unroll
-      for (int r = 1; r < R; ++r) u[r] = cmul(u[r], twid<DIR>(ldg_ordered(twk + (r - 1) * NS)));
-#endif
-    }
-    Dft<R, DIR>::run(u);
-#pragma unroll
-    for (int r = 0; r < R; ++r) v[b + r * BPT] = u[r];
+// cos / sin of 2πk/16
+__host__ __device__ constexpr double c16(int k) {
+  constexpr double c[16] = {1.0, 0.92387953251128675613, 0.70710678118654752440, 0.38268343236508977173,
+                            0.0, -0.38268343236508977173, -0.70710678118654752440, -0.92387953251128675613,
+                            -1.0, -0.92387953251128675613, -0.70710678118654752440, -0.38268343236508977173,
+                            0.0, 0.38268343236508977173, 0.70710678118654752440, 0.92387953251128675613};
+  return c[k & 15];
+}
+__host__ __device__ constexpr double s16(int k) { return c16(k - 4); }  // sin(2πk/16) = cos(2π(k-4)/16)
+
+// a · ω_16^k (forward sign: ω = exp(-2πi/16)), k a compile-time constant
+template <int K>
+__device__ __forceinline__ double2 mul_w16(double2 a) {
+  constexpr int k = K & 15;
+  if constexpr (k == 0) return a;
+  else if constexpr (k == 4) return make_double2(a.y, -a.x);
+  else if constexpr (k == 8) return make_double2(-a.x, -a.y);
+  else if constexpr (k == 12) return make_double2(-a.y, a.x);
+  else {
+    constexpr double c = c16(k), s = s16(k);  // ω^k = c - i s
+    return make_double2(fma(a.x, c, a.y * s), fma(a.y, c, -a.x * s));
   }
 }
 
-// padE(x + r·stride) = padE(x) + r·pad_step(stride) for every r of a stage
-// when stride is a multiple of E, or stride = 1 with x a multiple of R and
-// R dividing E (the run x .. x + R - 1 stays inside one E-block): then all
-// accesses of a stage are one base address plus immediate offsets.
-template <int E, int R, int STRIDE>
-struct PadStep {
-  static constexpr bool lin = STRIDE % E == 0 || (STRIDE == 1 && E % R == 0);
-  static constexpr int step = STRIDE + STRIDE / E;
-};
+// v[k] *= w^k (k = 1..15), conjugated for DIR = +1; w forward-sign
+template <int DIR>
+__device__ __forceinline__ void twiddle16(double2 (&v)[16], double2 w) {
+  double2 pw[16];
+  pw[1] = twid<DIR>(w);
+#pragma unroll
+  for (int r = 2; r < 16; ++r) pw[r] = cmul(pw[r / 2], pw[r - r / 2]);
+#pragma unroll
+  for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], pw[r]);
+}
 
-// After reg_stage<R,N,E,NS>: v[b + r·BPT] holds output index base_b + r·NS.
-template <int R, int N, int E, int NS>
-__device__ __forceinline__ void store_stage(const double2 (&v)[E], double2* S) {
-  constexpr int NT = N / E, BPT = E / R;
-  const int tid = tid_fresh();
+// v[k] *= b·w^k (k = 0..15), conjugated for DIR = +1
+template <int DIR>
+__device__ __forceinline__ void twiddle16_fold(double2 (&v)[16], double2 w, double2 b) {
+  double2 wp[9], T[16];
+  wp[1] = twid<DIR>(w);
 #pragma unroll
-  for (int b = 0; b < BPT; ++b) {
-    const int j = tid + b * NT;
-    const int base = (j / NS) * NS * R + (j % NS);
-    if constexpr (PadStep<E, R, NS>::lin) {
-      double2* Sb = S + padE<E>(base);
+  for (int r = 2; r <= 8; ++r) wp[r] = cmul(wp[r / 2], wp[r - r / 2]);
+  T[0] = twid<DIR>(b);
 #pragma unroll
-      for (int r = 0; r < R; ++r) Sb[r * PadStep<E, R, NS>::step] = v[b + r * BPT];
+  for (int k = 1; k < 16; ++k) T[k] = cmul(T[k / 2], wp[k - k / 2]);
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v[k] = cmul(v[k], T[k]);
+}
+
+template <int DIR>
+__device__ __forceinline__ void dft16(double2 (&v)[16]) {
+  Dft<16, DIR>::run(v);
+}
+
+// barrier over the G threads of one sub-transform (SUB = 4096 level)
+template <int L2>
+__device__ __forceinline__ void dif_bar_sub(int c) {
+  if constexpr (Dif<L2>::RHO == 1) {
+    __syncthreads();
+  } else {
+    if (c == 0)
+      asm volatile("bar.sync 1, %0;" ::"n"(Dif<L2>::G) : "memory");
+    else
+      asm volatile("bar.sync 2, %0;" ::"n"(Dif<L2>::G) : "memory");
+  }
+}
+
+// RHO-stage twiddle of (q0, c'): b · ω_{L2}^{(t + NT q0) c'} = b·w^{c'}·ω_16^{q0 c'}
+template <int RHO, int Q0, int CP, int DIR>
+__device__ __forceinline__ double2 rho_apply(double2 a, const double2 (&bw)[8]) {
+  const double2 t = mul_w16<Q0 * CP>(bw[CP]);
+  return cmul(a, twid<DIR>(t));
+}
+
+template <int RHO, int DIR, int Q0>
+__device__ __forceinline__ void rho_stage_fwd(double2 (&v)[16], const double2 (&bw)[8]) {
+  if constexpr (Q0 < 16 / RHO) {
+    constexpr int ST = 16 / RHO;
+    double2 u[RHO];
+#pragma unroll
+    for (int c = 0; c < RHO; ++c) u[c] = v[Q0 + ST * c];
+    Dft<RHO, -1>::run(u);
+    v[Q0] = cmul(u[0], bw[0]);
+    if constexpr (RHO > 1) v[Q0 + ST * 1] = rho_apply<RHO, Q0, 1, -1>(u[1], bw);
+    if constexpr (RHO > 2) v[Q0 + ST * 2] = rho_apply<RHO, Q0, 2, -1>(u[2], bw);
+    if constexpr (RHO > 3) v[Q0 + ST * 3] = rho_apply<RHO, Q0, 3, -1>(u[3], bw);
+    if constexpr (RHO > 4) {
+      v[Q0 + ST * 4] = rho_apply<RHO, Q0, 4, -1>(u[4], bw);
+      v[Q0 + ST * 5] = rho_apply<RHO, Q0, 5, -1>(u[5], bw);
+      v[Q0 + ST * 6] = rho_apply<RHO, Q0, 6, -1>(u[6], bw);
+      v[Q0 + ST * 7] = rho_apply<RHO, Q0, 7, -1>(u[7], bw);
+    }
+    rho_stage_fwd<RHO, DIR, Q0 + 1>(v, bw);
+  }
+}
+
+template <int RHO, int Q0>
+__device__ __forceinline__ void rho_stage_inv(double2 (&v)[16], const double2 (&bw)[8]) {
+  if constexpr (Q0 < 16 / RHO) {
+    constexpr int ST = 16 / RHO;
+    double2 u[RHO];
+    u[0] = cmulc(v[Q0], bw[0]);
+    if constexpr (RHO > 1) u[1] = rho_apply<RHO, Q0, 1, +1>(v[Q0 + ST * 1], bw);
+    if constexpr (RHO > 2) u[2] = rho_apply<RHO, Q0, 2, +1>(v[Q0 + ST * 2], bw);
+    if constexpr (RHO > 3) u[3] = rho_apply<RHO, Q0, 3, +1>(v[Q0 + ST * 3], bw);
+    if constexpr (RHO > 4) {
+      u[4] = rho_apply<RHO, Q0, 4, +1>(v[Q0 + ST * 4], bw);
+      u[5] = rho_apply<RHO, Q0, 5, +1>(v[Q0 + ST * 5], bw);
+      u[6] = rho_apply<RHO, Q0, 6, +1>(v[Q0 + ST * 6], bw);
+      u[7] = rho_apply<RHO, Q0, 7, +1>(v[Q0 + ST * 7], bw);
+    }
+    Dft<RHO, +1>::run(u);
+#pragma unroll
+    for (int c = 0; c < RHO; ++c) v[Q0 + ST * c] = u[c];
+    rho_stage_inv<RHO, Q0 + 1>(v, bw);
+  }
+}
+
+// bw[c'] = b·w^{c'} (c' < RHO), w = ω_{L2}^t
+template <int RHO>
+__device__ __forceinline__ void rho_bases(double2 (&bw)[8], double2 w, double2 b) {
+  bw[0] = b;
+#pragma unroll
+  for (int c = 1; c < RHO; ++c) bw[c] = cmul(bw[c - 1], w);
+}
+
+// Forward DIF of the row (see Dif).  On entry v[q] = x[t + NT q] and the
+// caller has made S safe to write (the thread's own padE slots); tw2 =
+// ω_{L2}^i (i < L2), b = ω_L^{t f1}: the four-step twiddle of the thread's
+// column is folded into the first stage (all 16 inputs share it).
+template <int L2>
+__device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const double2* __restrict__ tw2, double2 b) {
+  using D = Dif<L2>;
+  constexpr int NT = D::NT, RHO = D::RHO, G = D::G, SUB = D::SUB;
+  const int t = tid_fresh();
+  int c = 0, j = t;
+  if constexpr (RHO > 1) {
+    double2 bw[8];
+    rho_bases<RHO>(bw, ldg_ordered(&tw2[t]), b);
+    rho_stage_fwd<RHO, -1, 0>(v, bw);
+    if constexpr (NT % 16 == 0) {
+      double2* St = S + padE<16>(t);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) St[q * (NT + NT / 16)] = v[q];  // padE(t + NT q)
     } else {
 #pragma unroll
-      for (int r = 0; r < R; ++r) S[padE<E>(base + r * NS)] = v[b + r * BPT];
+      for (int q = 0; q < 16; ++q) S[padE<16>(t + NT * q)] = v[q];
+    }
+    __syncthreads();
+    c = t / G;
+    j = t % G;
+    const double2* Sr = S + c * D::REG;
+    if constexpr (SUB == 4096) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = Sr[272 * r + j + (j >> 4)];
+    } else if constexpr (SUB == 256) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = Sr[17 * r + j];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) v[r] = Sr[r];
     }
   }
-}
-
-template <int N, int E>
-__device__ __forceinline__ void load_strided(double2 (&v)[E], const double2* S) {
-  constexpr int NT = N / E;
-  const int tid = tid_fresh();
-  if constexpr (NT % E == 0) {
-    const double2* Sb = S + padE<E>(tid);
+  double2* B = S + c * D::REG;
+  if constexpr (SUB == 4096) {
+    dft16<-1>(v);
+    const double2 w = ldg_ordered(&tw2[j * (L2 / 4096)]);
+    if constexpr (RHO == 1) twiddle16_fold<-1>(v, w, b);
+    else twiddle16<-1>(v, w);
+    double2* Bw = B + j + (j >> 4);
 #pragma unroll
-    for (int q = 0; q < E; ++q) v[q] = Sb[q * (NT + NT / E)];
-  } else {
+    for (int k = 0; k < 16; ++k) Bw[272 * k] = v[k];
+    dif_bar_sub<L2>(c);
+    const int k = j >> 4;
+    j &= 15;
+    B += 272 * k;
 #pragma unroll
-    for (int q = 0; q < E; ++q) v[q] = S[padE<E>(tid + q * NT)];
+    for (int r = 0; r < 16; ++r) v[r] = B[j + 17 * r];
   }
-}
-
-template <int N, int E>
-__device__ __forceinline__ void store_strided(const double2 (&v)[E], double2* S) {
-  constexpr int NT = N / E;
-  const int tid = tid_fresh();
-  if constexpr (NT % E == 0) {
-    double2* Sb = S + padE<E>(tid);
+  if constexpr (SUB >= 256) {
+    dft16<-1>(v);
+    const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);
+    if constexpr (SUB == 256 && RHO == 1) twiddle16_fold<-1>(v, w, b);
+    else twiddle16<-1>(v, w);
 #pragma unroll
-    for (int q = 0; q < E; ++q) Sb[q * (NT + NT / E)] = v[q];
-  } else {
+    for (int k = 0; k < 16; ++k) B[j + 17 * k] = v[k];
+    __syncwarp();
 #pragma unroll
-    for (int q = 0; q < E; ++q) S[padE<E>(tid + q * NT)] = v[q];
+    for (int p = 0; p < 16; ++p) v[p] = B[17 * j + p];
   }
+  dft16<-1>(v);
 }
 
-// tws: all stages' twiddle tables back to back (stage I >= 1 at offset OFF,
-// NS·(R-1) entries each; see qmc_plan.d_tws).
-template <int N, int E, int DIR, int NS, int I, int OFF>
-__device__ __forceinline__ void fftE_rec(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid) {
-  if constexpr (I < RPlan<N, E>::count) {
-    constexpr int R = RPlan<N, E>::get(I);
-    if constexpr (I > 0) {
-      constexpr int RP = RPlan<N, E>::get(I - 1);
-      __syncthreads();
-      store_stage<RP, N, E, NS / RP>(v, S);
-      __syncthreads();
-      load_strided<N, E>(v, S);
+// Inverse DIT, the mirror of dif_fwd (same b): on entry the spectrum in
+// dif_fwd's output order, on exit v[q] = x[t + NT q] (unnormalised).
+template <int L2>
+__device__ __forceinline__ void dif_inv(double2 (&v)[16], double2* S, const double2* __restrict__ tw2, double2 b) {
+  using D = Dif<L2>;
+  constexpr int NT = D::NT, RHO = D::RHO, G = D::G, SUB = D::SUB;
+  const int t = tid_fresh();
+  const int c = RHO > 1 ? t / G : 0;
+  const int j0 = RHO > 1 ? t % G : t;
+  double2* B = S + c * D::REG;
+  dft16<+1>(v);
+  if constexpr (SUB >= 256) {
+    const int k = SUB == 4096 ? (j0 >> 4) : 0, j = j0 & 15;
+    double2* B2 = B + 272 * k;
+#pragma unroll
+    for (int p = 0; p < 16; ++p) B2[17 * j + p] = v[p];
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = B2[j + 17 * r];
+    const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);
+    if constexpr (SUB == 256 && RHO == 1) twiddle16_fold<+1>(v, w, b);
+    else twiddle16<+1>(v, w);
+    dft16<+1>(v);
+    if constexpr (SUB == 4096) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) B2[j + 17 * r] = v[r];
+      dif_bar_sub<L2>(c);
+      const double2* Br = B + j0 + (j0 >> 4);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) v[kk] = Br[272 * kk];
+      const double2 w4 = ldg_ordered(&tw2[j0 * (L2 / 4096)]);
+      if constexpr (RHO == 1) twiddle16_fold<+1>(v, w4, b);
+      else twiddle16<+1>(v, w4);
+      dft16<+1>(v);
     }
-    reg_stage<R, N, E, NS, DIR>(v, tws + OFF, tid);
-    fftE_rec<N, E, DIR, NS * R, I + 1, (I > 0 ? OFF + NS * (R - 1) : OFF)>(v, S, tws, tid);
   }
-}
-
-template <int N, int E, int DIR>
-__device__ __forceinline__ void fftE(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid) {
-  fftE_rec<N, E, DIR, 1, 0, 0>(v, S, tws, tid);
-}
-
-// Forward FFT fused with the pointwise product by the spectrum row Wr
-// (natural order, Wr[tid + q·NT] for v[q]): the first E/2 spectrum values are
-// loaded while the last exchange is in flight, the rest after the last
-// butterflies; dc receives the unmultiplied v[0] (the DC term for tid 0).
-template <int N, int E, int NS, int I, int OFF>
-__device__ __forceinline__ void fftE_fwd_w_rec(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid,
-                                               const double2* __restrict__ Wr, double2& dc) {
-  if constexpr (I < RPlan<N, E>::count) {
-    constexpr int R = RPlan<N, E>::get(I);
-    constexpr bool LAST = I + 1 == RPlan<N, E>::count;
-    constexpr int NT = N / E, H = E / 2;
-    double2 wv[LAST ? H : 1];
-    if constexpr (I > 0) {
-      constexpr int RP = RPlan<N, E>::get(I - 1);
-      __syncthreads();
-      store_stage<RP, N, E, NS / RP>(v, S);
-      if constexpr (LAST) {
-        const double2* Wt = Wr + tid_fresh();
+  if constexpr (RHO > 1) {
+    double2* Bw = B;
+    if constexpr (SUB == 4096) {
 #pragma unroll
-        for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wt[q * NT]);
-      }
-      __syncthreads();
-      load_strided<N, E>(v, S);
-    } else if constexpr (LAST) {
-      const double2* Wt = Wr + tid_fresh();
+      for (int r = 0; r < 16; ++r) Bw[272 * r + j0 + (j0 >> 4)] = v[r];
+    } else if constexpr (SUB == 256) {
 #pragma unroll
-      for (int q = 0; q < H; ++q) wv[q] = ldg_ordered(&Wt[q * NT]);
+      for (int r = 0; r < 16; ++r) Bw[17 * r + j0] = v[r];
+    } else {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) Bw[r] = v[r];
     }
-    reg_stage<R, N, E, NS, -1>(v, tws + OFF, tid);
-    if constexpr (LAST) {
-      dc = v[0];
+    __syncthreads();
+    if constexpr (NT % 16 == 0) {
+      const double2* St = S + padE<16>(t);
 #pragma unroll
-      for (int q = 0; q < H; ++q) v[q] = cmul(v[q], wv[q]);
-      const double2* Wt = Wr + tid_fresh();
+      for (int q = 0; q < 16; ++q) v[q] = St[q * (NT + NT / 16)];
+    } else {
 #pragma unroll
-      for (int q = H; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wt[q * NT]));
+      for (int q = 0; q < 16; ++q) v[q] = S[padE<16>(t + NT * q)];
     }
-    fftE_fwd_w_rec<N, E, NS * R, I + 1, (I > 0 ? OFF + NS * (R - 1) : OFF)>(v, S, tws, tid, Wr, dc);
+    double2 bw[8];
+    rho_bases<RHO>(bw, ldg_ordered(&tw2[t]), b);
+    rho_stage_inv<RHO, 0>(v, bw);
   }
-}
-
-template <int N, int E>
-__device__ __forceinline__ void fftE_fwd_w(double2 (&v)[E], double2* S, const double2* __restrict__ tws, int tid,
-                                           const double2* __restrict__ Wr, double2& dc) {
-  fftE_fwd_w_rec<N, E, 1, 0, 0>(v, S, tws, tid, Wr, dc);
 }
 
 // ----------------------------------------------------------------- register column DFT

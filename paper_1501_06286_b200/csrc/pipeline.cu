@@ -155,8 +155,11 @@ __global__ void __launch_bounds__(256) k_dense_cols(const double2* __restrict__ 
 #pragma unroll
   for (int e1 = 0; e1 < L1; ++e1) v[e1] = src[int64_t(e1) * L2];
   reg_dft<L1, -1>(v, tw1);
-  // × ω_L^{e2 f1} = w^f1, w = ω_L^{e2}: running products
-  const double2 w = __ldg(&twL[e2]);
+  // × ω_L^{(e2 - e2 mod NT) f1} = w^f1, w = ω_L^{e2 - e2 mod NT}: the four-step
+  // twiddle ω_L^{e2 f1} without its row-thread part ω_L^{(e2 mod NT) f1},
+  // which K1 folds into its first stage (NT = L2/16): running products
+  const int NT = L2 / 16;
+  const double2 w = __ldg(&twL[e2 - e2 % NT]);
   double2 tw = w;
   double2* dst = T + int64_t(p) * ldT + e2;
   dst[0] = v[0];
@@ -207,8 +210,9 @@ __global__ void __launch_bounds__(256) k_dense_cols2(const double2* __restrict__
 #pragma unroll
     for (int r = 0; r < R; ++r) z[r] = Y[c * LP + r * M + k2];
     reg_dft<R, -1>(z, tw1, L1 / R);
-    // × ω_L^{e2 f1}, f1 = k2 + M k1: ω_L^{e2 k2} · (ω_L^{e2 M})^{k1}
-    const double2 w = __ldg(&twL[e2]);
+    // × ω_L^{e2' f1}, e2' = e2 - e2 mod (L2/16) (K1 folds the rest),
+    // f1 = k2 + M k1: ω_L^{e2' k2} · (ω_L^{e2' M})^{k1}
+    const double2 w = __ldg(&twL[e2 - e2 % (L2 / 16)]);
     double2 b = make_double2(1.0, 0.0);
     for (int q = 0; q < k2; ++q) b = cmul(b, w);
     double2 wM = make_double2(1.0, 0.0);
@@ -279,8 +283,12 @@ struct K1Args {
   int nch, bal;
   int dense;                           // asort holds T[p][f1][e2] (k_dense_cols): no scatter
   const double2* __restrict__ twj;     // [L1][S1]
-  const double2* __restrict__ tws;     // row-FFT stage twiddles
-  const double2* __restrict__ W;       // [L1][L2] spectrum
+  const double2* __restrict__ tw2;     // [L2] ω_{L2}^i (row-FFT stage twiddles)
+  const double2* __restrict__ tw1;     // [L1] ω_{L1}^i
+  const double2* __restrict__ twL;     // [L2] ω_L^i, i < L2
+  const double2* __restrict__ tw16;    // [16 L1] ω_{16 L1}^i
+  int lg2L2;
+  const double2* __restrict__ W;       // [L1][L2] spectrum, row f1 in the K1 register order (dif_freq)
   double2* __restrict__ U;             // [np][L] blocked
   int64_t L;
   int L1, np;
@@ -441,17 +449,41 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
       }
     }
   }
-  const double2* Wr = a.W + int64_t(f1) * L2;
-  double2 dc;
-  fftE_fwd_w<L2, E>(v, S, a.tws, tid, Wr, dc);
+  // b = ω_L^{t·f1}: the thread's part of the four-step twiddle ω_L^{e2·f1}
+  // (e2 = t + NT q), folded into the first row-FFT stage; the scatter
+  // twiddles (twj) carry the rest, ω_{16 L1}^{q f1} (plan.cu k_twj)
+  const int t0 = tid_fresh();
+  double2 b;
+  {
+    const int x = t0 * f1;  // < NT·L1 = L/16
+    b = cmul(__ldg(&a.tw1[x >> a.lg2L2]), __ldg(&a.twL[x & (L2 - 1)]));
+  }
+  dif_fwd<L2>(v, S, a.tw2, b);
   QMC_TS(2);
-  if (f1 == 0 && tid == 0) {
+  if (f1 == 0 && tid == 0) {  // DC term (register 0 of thread 0) = Σ_j a_j, the row-0 sums
     const int64_t k1 = 2 * (a.pair0 + p);
-    a.colsum[k1] = dc.x;
-    if (k1 + 1 < a.t) a.colsum[k1 + 1] = dc.y;
+    a.colsum[k1] = v[0].x;
+    if (k1 + 1 < a.t) a.colsum[k1 + 1] = v[0].y;
+  }
+  {  // × spectrum (stored in this register order: W[f1][r·NT + t])
+    const double2* Wr = a.W + int64_t(f1) * L2 + tid_fresh();
+#pragma unroll
+    for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[q * NT]));
   }
   QMC_TS(3);
-  fftE<L2, E, +1>(v, S, a.tws, tid);
+  dif_inv<L2>(v, S, a.tw2, b);
+  // the rest of conj(ω_L^{e2 f1}) (the column pass's twiddle): conj(ω_{16 L1}^{q f1})
+  {
+    static_assert(E == 16, "K1's row FFT holds 16 points per thread");
+    const int M16 = 16 * L1;
+    int y = 0;
+#pragma unroll
+    for (int q = 1; q < E; ++q) {
+      y += f1;  // (q·f1) mod 16 L1
+      if (y >= M16) y -= M16;
+      v[q] = cmulc(v[q], __ldg(&a.tw16[y]));
+    }
+  }
   QMC_TS(4);
   // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
   // whole sectors of kUB·16 bytes per f1
@@ -674,22 +706,7 @@ __global__ void __launch_bounds__(kColThreads, 2)
 #pragma unroll
       for (int f1 = 0; f1 < L1; ++f1) v[f1] = make_double2(0.0, 0.0);
     }
-    if (L1 > 1) {
-      // conj(ω_L^{e2 f1}) = conj(w^f1), w = ω_L^{e2}, as w^{4a}·w^b (f1 = 4a + b):
-      // products of depth <= 3, six live twiddles
-      const double2 w1 = __ldg(&twL[okc ? e2 : 0]);
-      const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
-      const double2 w4 = cmul(w2, w2);
-      double2 hi = w4;
-#pragma unroll
-      for (int f1 = 1; f1 < L1; ++f1) {
-        const int b = f1 & 3;
-        if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
-        const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
-        const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
-        v[f1] = cmulc(v[f1], tw);
-      }
-    }
+    // (the twiddle conj(ω_L^{e2 f1}) was applied by K1)
     // this CTA's U blocks (PG pairs × CB/kUB column blocks of L1·kUB complex,
     // read only here) are dead: drop them from L2 without write-back
     if (CB % kUB == 0) {
@@ -739,15 +756,6 @@ __global__ void __launch_bounds__(kColThreads, 2)
         const double2* ub = Up + int64_t(e2 >> 2) * (L1 * kUB) + (e2 & 3);
 #pragma unroll
         for (int mm = 0; mm < M; ++mm) x[mm] = __ldg(&ub[(r + R * mm) * kUB]);
-        // conj(ω_L^{e2 (r + R mm)}) = conj(b0 · st^mm)
-        const double2 b0 = omegaL(int64_t(e2) * r, lg2L2, L2, tw1, twL);
-        double2 pw[M];
-        pw[0] = make_double2(1.0, 0.0);
-        if (M > 1) pw[1] = omegaL(int64_t(e2) * R, lg2L2, L2, tw1, twL);
-#pragma unroll
-        for (int q = 2; q < M; ++q) pw[q] = cmul(pw[q / 2], pw[q - q / 2]);
-#pragma unroll
-        for (int mm = 0; mm < M; ++mm) x[mm] = cmulc(x[mm], cmul(b0, pw[mm]));
       } else {
 #pragma unroll
         for (int mm = 0; mm < M; ++mm) x[mm] = make_double2(0.0, 0.0);
@@ -894,27 +902,11 @@ __device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2
       if (tid == 0) rowpart[0] = r0;
     }
   }
-  const int e2 = bx * CB + c;
   const double2* src = tileS + p * PSTR + (c / kUB) * BLK + (c % kUB);
   double2 v[L1];
 #pragma unroll
   for (int f1 = 0; f1 < L1; ++f1) v[f1] = src[f1 * kUB];
-  if (L1 > 1) {
-    // conj(ω_L^{e2 f1}) = conj(w^f1), w = ω_L^{e2}, as w^{4a}·w^b (f1 = 4a + b)
-    const double2 w1 = __ldg(&a.twL[e2]);
-    const double2 w2 = cmul(w1, w1), w3 = cmul(w2, w1);
-    const double2 w4 = cmul(w2, w2);
-    double2 hi = w4;
-#pragma unroll
-    for (int f1 = 1; f1 < L1; ++f1) {
-      const int b = f1 & 3;
-      if (f1 >= 8 && b == 0) hi = (f1 == 8) ? cmul(w4, w4) : cmul(hi, w4);
-      const double2 lo = b == 1 ? w1 : b == 2 ? w2 : w3;
-      const double2 tw = f1 < 4 ? lo : (b == 0 ? hi : cmul(hi, lo));
-      v[f1] = cmulc(v[f1], tw);
-    }
-  }
-  reg_dft<L1, +1>(v, a.tw1);
+  reg_dft<L1, +1>(v, a.tw1);  // (the twiddle conj(ω_L^{e2 f1}) was applied by K1)
   const int* nr = nS + c;
   double r[L1];
 #pragma unroll
@@ -1039,21 +1031,11 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
   // stage A: items (p, c, r), it = p + PG·(c + kUB·r)
   for (int it = tid; it < PG * kUB * R; it += kP2Thr) {
     const int c = (it / PG) % kUB, r = it / (PG * kUB);
-    const int e2 = bx * kUB + c;
     double2* Tp = T + p * PSTR + c;
     double2 x[M];
 #pragma unroll
     for (int mm = 0; mm < M; ++mm) x[mm] = Tp[(r + R * mm) * kUB];
-    // conj(ω_L^{e2 (r + R mm)}) = conj(b0 · st^mm)
-    const double2 b0 = omegaL(int64_t(e2) * r, lg2L2, a.L2, a.tw1, a.twL);
-    double2 pw[M];
-    pw[0] = make_double2(1.0, 0.0);
-    if (M > 1) pw[1] = omegaL(int64_t(e2) * R, lg2L2, a.L2, a.tw1, a.twL);
-#pragma unroll
-    for (int q = 2; q < M; ++q) pw[q] = cmul(pw[q / 2], pw[q - q / 2]);
-#pragma unroll
-    for (int mm = 0; mm < M; ++mm) x[mm] = cmulc(x[mm], cmul(b0, pw[mm]));
-    reg_dft<M, +1>(x, a.tw1, L1 / M);
+    reg_dft<M, +1>(x, a.tw1, L1 / M);  // (conj(ω_L^{e2 f1}) was applied by K1)
 #pragma unroll
     for (int k2 = 1; k2 < M; ++k2)
       if (r) x[k2] = cmul(x[k2], twid<+1>(__ldg(&a.tw1[r * k2])));
@@ -1181,11 +1163,16 @@ struct CallLayout {
 static int64_t call_batch(const qmc_plan* pl, int64_t t) {
   const int64_t npairs = std::max<int64_t>(1, (t + 1) / 2);
   int64_t b = pl->batch_pairs;
-  if (npairs >= 128 && !getenv("QMC_BATCH_PAIRS")) {  // small calls: one batch (launch-bound)
+  if (npairs >= 128 && !pl->batch_fixed) {  // small calls: one batch (launch-bound)
     const int64_t half = ((npairs + 1) / 2 + 15) / 16 * 16;
     b = std::min(b, half);
   }
-  return std::max<int64_t>(1, std::min(b, npairs));
+  b = std::max<int64_t>(1, b);
+  // every batch but the last starts on a K2 pair-group boundary (the row-sum
+  // slot of a pair group is pair0 / PG + group)
+  const int64_t pg = pair_group(b);
+  b = (b + pg - 1) / pg * pg;
+  return std::min(b, npairs);
 }
 
 static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
@@ -1224,6 +1211,12 @@ static void set_smem_attr(K kernel, size_t bytes) {
   if (bytes > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes));
 }
 
+static int ilog2(int64_t x) {
+  int r = 0;
+  while ((int64_t(1) << r) < x) ++r;
+  return r;
+}
+
 static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                       double* colsum) {
   K1Args a;
@@ -1237,7 +1230,11 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   a.bal = pl->k1_bal;
   a.dense = pl->k1_dense;
   a.twj = pl->d_twj;
-  a.tws = pl->d_tws;
+  a.tw2 = pl->d_tw2;
+  a.tw1 = pl->d_tw1;
+  a.twL = pl->d_twL;
+  a.tw16 = pl->d_tw16;
+  a.lg2L2 = ilog2(pl->sp.L2);
   a.W = pl->d_W;
   a.U = U;
   a.L = pl->sp.L;
@@ -1284,12 +1281,6 @@ static int rows_dispatch(const qmc_plan* pl, const double2* asort, int64_t t, in
   return QMC_EINVAL_N;
 }
 
-static int ilog2(int64_t x) {
-  int r = 0;
-  while ((int64_t(1) << r) < x) ++r;
-  return r;
-}
-
 static int sm_count_cols() {
   static int nsm = 0;
   if (!nsm) {
@@ -1333,7 +1324,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   const bool fastp = R == 1 && np % cl.PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) &&
                      (pl->sp.L2 % ((R == 1 ? kColThreads : 32) / cl.PG)) == 0;
   if constexpr (R == 1 && (EP != EPK_ROWSUM || L1 == 16)) {
-    if (fastp && cl.PG == 16 && !getenv("QMC_K2_NOPIPE")) {
+    if (fastp && cl.PG == 16 && !pl->k2_nopipe) {
       constexpr int CBP = QMC_K2_CB;
       constexpr size_t psm = cols_pipe_smem<L1, CBP>();
       auto pk = k_cols_pipe<L1, EP, CBP>;
@@ -1359,7 +1350,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   if constexpr (R > 1 && EP != EPK_ROWSUM && cols_pipe2_smem<R * M>() <= 232448) {
     // two-stage column pass, pipelined: whole 8-pair groups, whole pairs,
     // vector X stores, whole U column blocks
-    if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !getenv("QMC_K2_NOPIPE")) {
+    if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !pl->k2_nopipe) {
       constexpr size_t psm = cols_pipe2_smem<L1>();
       auto pk = k_cols_pipe2<R, M, EP>;
       set_smem_attr(pk, psm);
@@ -1439,6 +1430,69 @@ static int dense_cols_dispatch(const qmc_plan* pl, const double2* ad, int np, do
   return QMC_EINVAL_N;
 }
 
+// one batch of column pairs [pair0, pair0 + np) on stream bs (scratch set
+// bidx & 1 when two sets are in use): K0, K1, K2 and the column-mean reduce
+static int run_batch(const qmc_plan* pl, const CallLayout& cl, const double* A, int64_t lda, int64_t t, int f,
+                     double* out, EpiArgs E, char* ws, int64_t pairs_b, int64_t pair0, int64_t bidx, cudaStream_t bs,
+                     const double* A_host, int64_t lda_host) {
+  const int64_t npairs_total = (t + 1) / 2;
+  const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
+  const int nsets = cl.nsets;
+  const int ep = f == QMC_F_ROWMEAN_RELU ? EPK_ROWSUM : f == QMC_F_EXP ? EPK_EXP : EPK_LIN;
+  double* colsum = (double*)(ws + cl.off_colsum);
+  const int np = int(std::min<int64_t>(pairs_b, npairs_total - pair0));
+  const int set = nsets == 2 ? int(bidx & 1) : 0;
+  double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
+  double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
+  E.rowpart = (double*)(ws + cl.off_rowsum);
+  double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->S1;
+  if (A_host) {
+    const int64_t c0 = 2 * pair0, nc = std::min<int64_t>(2 * int64_t(np), t - c0);
+    if (cudaMemcpy2DAsync(const_cast<double*>(A) + c0 * lda, size_t(lda) * 8, A_host + c0 * lda_host,
+                          size_t(lda_host) * 8, size_t(pl->s) * 8, size_t(nc), cudaMemcpyHostToDevice,
+                          bs) != cudaSuccess)
+      return QMC_ECUDA;
+  }
+  prof_begin(KC_PACK, bs);
+  if (pl->k1_dense) {
+    // a' into this set's U (K1 overwrites it afterwards), T into asort
+    k_pack_dense<<<dim3(nblk(pl->sp.L, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, pl->d_jq,
+                                                                        pl->d_e2q, pl->sp.L, U);
+    QMC_LAUNCHED();
+    int rc0 = dense_cols_dispatch(pl, U, np, asort, bs);
+    if (rc0) return rc0;
+  } else if (pl->s <= kPackSmemMax && !pl->pack_gather) {
+    const size_t psm = size_t(pl->s) * 16;
+    set_smem_attr(k_pack_smem, psm);
+    // slices of the slots: ~2 CTAs of work per SM in total
+    const int ny = int(std::max<int64_t>(1, std::min<int64_t>((2 * sm_count_cols() + np - 1) / np,
+                                                              (pl->S1 + 1023) / 1024)));
+    k_pack_smem<<<dim3(unsigned(np), unsigned(ny)), 256, psm, bs>>>(A, lda, t, pair0, pl->d_jq, pl->s, pl->S1,
+                                                                    asort);
+  } else {
+    k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
+  }
+  QMC_LAUNCHED();
+  prof_end(KC_PACK, bs);
+  prof_begin(KC_ROWS, bs);
+  int rc = rows_dispatch(pl, asort, t, pair0, U, np, colsum, bs);
+  if (rc) return rc;
+  prof_end(KC_ROWS, bs);
+  prof_begin(KC_COLS, bs);
+  int nbx_used = cl.nbx;
+  rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs, &nbx_used);
+  if (rc) return rc;
+  prof_end(KC_COLS, bs);
+  if (colmean) {
+    prof_begin(KC_REDUCE, bs);
+    k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, nbx_used, cl.part_stride, 2 * np, 2 * pair0, t,
+                                                       pl->N, out);
+    QMC_LAUNCHED();
+    prof_end(KC_REDUCE, bs);
+  }
+  return QMC_OK;
+}
+
 // all batches of column pairs; f = -1: X only.  A_host != NULL: each batch
 // first copies its own columns of A from the host (A_host, leading dimension
 // lda_host) into A on the batch's stream, so that the copy of one batch
@@ -1449,20 +1503,22 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   if (!pl) return QMC_ENULL;
   if (t < 0 || lda < pl->s) return QMC_EINVAL_DIM;
   if (X && ldx < t) return QMC_EINVAL_DIM;
-  if (t == 0) return QMC_OK;
-  if (!A || !call_ws) return QMC_ENULL;
   if (f >= 0 && !out) return QMC_ENULL;
+  if (t == 0) {
+    // an empty slab (e.g. a rank with no columns): the row functional's
+    // partial row sums are all zero, so a later all-reduce stays exact; the
+    // per-column means have no entries
+    if (f == QMC_F_ROWMEAN_RELU && cudaMemsetAsync(out, 0, size_t(pl->N) * 8, st) != cudaSuccess) return QMC_ECUDA;
+    return QMC_OK;
+  }
+  if (!A || !call_ws) return QMC_ENULL;
   if (f < 0 && !X) return QMC_ENULL;
   const CallLayout cl = call_layout(pl, t, f);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
   const int64_t pairs_b = call_batch(pl, t);
-  double* colsum = (double*)(ws + cl.off_colsum);
   const int64_t npairs_total = (t + 1) / 2;
-  const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
-  const int nsets = cl.nsets;
   EpiArgs E;
-  const int ep = f == QMC_F_ROWMEAN_RELU ? EPK_ROWSUM : f == QMC_F_EXP ? EPK_EXP : EPK_LIN;
   E.fparam = f == QMC_F_AFFINE ? fparam : 0.0;
   E.X = X;
   E.ldx = ldx;
@@ -1471,7 +1527,7 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   E.N = pl->N;
   E.rowpart = (double*)(ws + cl.off_rowsum);
   std::unique_lock<std::mutex> lock;
-  const bool two = nsets == 2 && pl->nstreams == 2;
+  const bool two = cl.nsets == 2 && pl->nstreams == 2;
   if (two) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
     if (cudaEventRecord(pl->ev_fork, st) != cudaSuccess ||
@@ -1482,69 +1538,22 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     }
   }
   int64_t bidx = 0;
-  for (int64_t pair0 = 0; pair0 < npairs_total; pair0 += pairs_b, ++bidx) {
-    const int np = int(std::min<int64_t>(pairs_b, npairs_total - pair0));
-    const int set = nsets == 2 ? int(bidx & 1) : 0;
-    const cudaStream_t bs = two ? pl->ist[set] : st;
-    double2* U = (double2*)(ws + cl.off_U) + size_t(set) * pairs_b * pl->sp.L;
-    double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
-    E.rowpart = (double*)(ws + cl.off_rowsum);
-    double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->S1;
-    if (A_host) {
-      const int64_t c0 = 2 * pair0, nc = std::min<int64_t>(2 * int64_t(np), t - c0);
-      if (cudaMemcpy2DAsync(const_cast<double*>(A) + c0 * lda, size_t(lda) * 8, A_host + c0 * lda_host,
-                            size_t(lda_host) * 8, size_t(pl->s) * 8, size_t(nc), cudaMemcpyHostToDevice,
-                            bs) != cudaSuccess)
-        return QMC_ECUDA;
-    }
-    prof_begin(KC_PACK, bs);
-    if (pl->k1_dense) {
-      // a' into this set's U (K1 overwrites it afterwards), T into asort
-      k_pack_dense<<<dim3(nblk(pl->sp.L, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, pl->d_jq,
-                                                                          pl->d_e2q, pl->sp.L, U);
-      QMC_LAUNCHED();
-      int rc0 = dense_cols_dispatch(pl, U, np, asort, bs);
-      if (rc0) return rc0;
-    } else if (pl->s <= kPackSmemMax && !getenv("QMC_PACK_GATHER")) {
-      const size_t psm = size_t(pl->s) * 16;
-      set_smem_attr(k_pack_smem, psm);
-      // slices of the slots: ~2 CTAs of work per SM in total
-      const int ny = int(std::max<int64_t>(1, std::min<int64_t>((2 * sm_count_cols() + np - 1) / np,
-                                                                (pl->S1 + 1023) / 1024)));
-      k_pack_smem<<<dim3(unsigned(np), unsigned(ny)), 256, psm, bs>>>(A, lda, t, pair0, pl->d_jq, pl->s, pl->S1,
-                                                                      asort);
-    } else {
-      k_pack<<<dim3(nblk(pl->S1, 256), unsigned(np)), 256, 0, bs>>>(A, lda, t, pair0, np, pl->d_jq, pl->S1, asort);
-    }
-    QMC_LAUNCHED();
-    prof_end(KC_PACK, bs);
-    prof_begin(KC_ROWS, bs);
-    int rc = rows_dispatch(pl, asort, t, pair0, U, np, colsum, bs);
-    if (rc) return rc;
-    prof_end(KC_ROWS, bs);
-    prof_begin(KC_COLS, bs);
-    int nbx_used = cl.nbx;
-    rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs, &nbx_used);
-
-    if (rc) return rc;
-    prof_end(KC_COLS, bs);
-    if (colmean) {
-      prof_begin(KC_REDUCE, bs);
-      k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, nbx_used, cl.part_stride, 2 * np, 2 * pair0, t,
-                                                         pl->N, out);
-      QMC_LAUNCHED();
-      prof_end(KC_REDUCE, bs);
-    }
+  int rc = QMC_OK;
+  for (int64_t pair0 = 0; pair0 < npairs_total && rc == QMC_OK; pair0 += pairs_b, ++bidx) {
+    rc = run_batch(pl, cl, A, lda, t, f, out, E, ws, pairs_b, pair0, bidx, two ? pl->ist[bidx & 1] : st, A_host,
+                   lda_host);
   }
-  if (two) {  // join
-    if (cudaEventRecord(pl->ev_join[0], pl->ist[0]) != cudaSuccess ||
-        cudaEventRecord(pl->ev_join[1], pl->ist[1]) != cudaSuccess ||
-        cudaStreamWaitEvent(st, pl->ev_join[0], 0) != cudaSuccess ||
-        cudaStreamWaitEvent(st, pl->ev_join[1], 0) != cudaSuccess) {
+  if (two) {  // join (also after an error: the caller's stream must not run ahead of queued batches)
+    const bool ok = cudaEventRecord(pl->ev_join[0], pl->ist[0]) == cudaSuccess &&
+                    cudaEventRecord(pl->ev_join[1], pl->ist[1]) == cudaSuccess &&
+                    cudaStreamWaitEvent(st, pl->ev_join[0], 0) == cudaSuccess &&
+                    cudaStreamWaitEvent(st, pl->ev_join[1], 0) == cudaSuccess;
+    if (!ok) {
       cudaGetLastError();
-      return QMC_ECUDA;
+      if (rc == QMC_OK) rc = QMC_ECUDA;
     }
   }
+  if (rc) return rc;
   if (f == QMC_F_ROWMEAN_RELU) {
     prof_begin(KC_REDUCE, st);
     // parts [group][N], every pair group of the call, fixed order
@@ -1554,7 +1563,6 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   }
   return QMC_OK;
 }
-
 }  // namespace qmc
 
 using namespace qmc;

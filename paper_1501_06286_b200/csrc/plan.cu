@@ -124,6 +124,14 @@ bool choose_split(int64_t m, int64_t s, Split* out) {
   return false;
 }
 
+// the dense first pass is taken whatever the bucket sizes: the balanced
+// order is not tried (s > 8·L2), a' is at least half full and the K2 split
+// exists (create_common decides k1_dense the same way)
+static bool k1_dense_certain(int64_t s, const Split& sp) {
+  return !k1_try_balanced(s, sp.L2) && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS") &&
+         !getenv("QMC_NO_DENSE");
+}
+
 PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   PlanLayout l;
   size_t o = 0;
@@ -148,8 +156,10 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_tw1 = take(size_t(sp.L1) * 16);
   l.off_tw2 = take(size_t(sp.L2) * 16);
   l.off_twL = take(size_t(sp.L2) * 16);
-  l.off_tws = take(size_t(sp.L2) * 16);
-  l.off_twj = take(size_t(sp.L1) * size_t(s1) * 16);
+  l.off_tw16 = take(size_t(16 * sp.L1) * 16);
+  // per-entry twiddles of the sparse first pass; none when the plan is
+  // certain to take the dense first pass (create_common: k1_dense)
+  l.off_twj = take(k1_dense_certain(s, sp) ? 0 : size_t(sp.L1) * size_t(s1) * 16);
   l.off_jq = take(size_t(s1) * 4);
   l.off_k1c = take(size_t(2 * s1 + 4) * 4);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
@@ -344,7 +354,10 @@ __global__ void k_bucket_finish(const int32_t* __restrict__ e, int L2, const int
     const int j = e2q[pos];
     bent[pos] = make_int4(j, e[j], b, pos == lo ? hi : -1);
   }
-  for (int pos = lo; pos < hi; ++pos) e2q[pos] = pos == lo ? b | ((hi - lo) << 13) : b;
+  // the size field only bounds the head's sum inside its chunk (at most 2048
+  // entries), so capping it at 2^18 - 1 keeps the code exact for any bucket
+  const int len = min(hi - lo, (1 << 18) - 1);
+  for (int pos = lo; pos < hi; ++pos) e2q[pos] = pos == lo ? b | (len << 13) : b;
   if (hi > lo) atomicOr(&occ[b >> 5], 1u << (b & 31));
 }
 
@@ -373,34 +386,13 @@ __global__ void k_twiddles(double2* __restrict__ tw, int64_t n, int64_t count) {
   tw[k] = make_double2(cv, -sv);
 }
 
-// Stage-major twiddles of the register row FFT (fft.cuh R16Plan: radix 16
-// stages, then one radix-2/4/8 stage): for stage i >= 1 with span NS and
-// radix R, tws[off_i + (r-1)·NS + k] = ω_{NS·R}^{k·r}, k < NS, 1 <= r < R.
-__global__ void k_stage_twiddles(double2* __restrict__ tws, int N, int E) {
-  int ns = N >= E ? E : N, off = 0, rem = N / ns;
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
-  while (rem > 1) {
-    const int R = rem >= E ? E : rem;
-    const int cnt = ns * (R - 1);
-    if (idx >= off && idx < off + cnt) {
-      const int r = (idx - off) / ns + 1, k = (idx - off) % ns;
-      double sv, cv;
-      sincospi(2.0 * double(k * r) / double(ns * R), &sv, &cv);
-      tws[idx] = make_double2(cv, -sv);
-    }
-    off += cnt;
-    ns *= R;
-    rem /= R;
-  }
-}
-
 // twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x: the twiddle of the
 // q-th entry (bucket order) in row f1 of the scatter fused with the first DFT
 // dimension (K1)
 // twj[f1·S1 + q] = ω_L^{(e_j·f1) mod L} for the column j = jq[q] of slot q of
 // the K1 order (0 for padding slots)
 __global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict__ e, int64_t S1, int64_t L, int L1,
-                      double2* __restrict__ twj) {
+                      int NT, double2* __restrict__ twj) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= S1 * L1) return;
   const int64_t f1 = i / S1, q = i % S1;
@@ -409,7 +401,10 @@ __global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict_
     twj[i] = make_double2(0.0, 0.0);
     return;
   }
-  const int64_t x = (int64_t(e[j]) * f1) % L;
+  // ω_L^{e' f1} with e' = e_j - e_j mod NT: the thread part ω_L^{(e_j mod NT) f1}
+  // of the four-step twiddle is folded into K1's first row-FFT stage
+  const int64_t ej = e[j];
+  const int64_t x = ((ej - ej % NT) * f1) % L;
   double sv, cv;
   sincospi(2.0 * double(x) / double(L), &sv, &cv);
   twj[i] = make_double2(cv, -sv);
@@ -541,10 +536,13 @@ __global__ void __launch_bounds__(RowThreads<L2>::value)
   }
   __syncthreads();
   row_fft<L2, -1>(S, tw2);
+  // stored in K1's register order: slot r·NTk + t holds frequency f2 =
+  // dif_freq(t, r) (NTk = L2/16 threads of the row kernel)
   const double inv = 1.0 / double(L);
-  for (int f2 = threadIdx.x; f2 < L2; f2 += NT) {
-    const double2 v = S[swz(f2)];
-    W[int64_t(f1) * L2 + f2] = make_double2(v.x * inv, v.y * inv);
+  constexpr int NTk = L2 / 16;
+  for (int i = threadIdx.x; i < L2; i += NT) {
+    const double2 v = S[swz(dif_freq<L2>(i % NTk, i / NTk))];
+    W[int64_t(f1) * L2 + i] = make_double2(v.x * inv, v.y * inv);
   }
 }
 
@@ -646,8 +644,13 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     if (const char* ev = getenv("QMC_K2_PER_SM")) pl->k2_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
-      if (v > 0) pl->batch_pairs = v;
+      if (v > 0) {
+        pl->batch_pairs = v;
+        pl->batch_fixed = 1;
+      }
     }
+    pl->k2_nopipe = getenv("QMC_K2_NOPIPE") != nullptr;
+    pl->pack_gather = getenv("QMC_PACK_GATHER") != nullptr;
   }
   char* b = pl->ws;
   pl->d_scal = (double*)(b + lay.off_scal);
@@ -664,7 +667,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_tw1 = (double2*)(b + lay.off_tw1);
   pl->d_tw2 = (double2*)(b + lay.off_tw2);
   pl->d_twL = (double2*)(b + lay.off_twL);
-  pl->d_tws = (double2*)(b + lay.off_tws);
+  pl->d_tw16 = (double2*)(b + lay.off_tw16);
   pl->d_twj = (double2*)(b + lay.off_twj);
   pl->d_jq = (int32_t*)(b + lay.off_jq);
   pl->d_k1c = (int32_t*)(b + lay.off_k1c);
@@ -751,7 +754,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_twL, sp.L, sp.L2);
   QMC_PLAN_LAUNCHED();
-  k_stage_twiddles<<<blocks(sp.L2, 256), 256, 0, st>>>(pl->d_tws, int(sp.L2), QMC_ROW_E);
+  k_twiddles<<<blocks(16 * sp.L1, 256), 256, 0, st>>>(pl->d_tw16, 16 * sp.L1, 16 * sp.L1);
   QMC_PLAN_LAUNCHED();
   {
     // K1 order of the scatter input (k1_balanced_order, else bucket order)
@@ -812,7 +815,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     QMC_PLAN_CHECK(cudaMemcpy(pl->d_k1c, cs.data(), 4 * cs.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
   }
   if (!pl->k1_dense) {  // the dense first pass needs no per-entry twiddles
-    k_twj<<<blocks(sp.L1 * pl->S1, 256), 256, 0, st>>>(pl->d_jq, pl->d_e, pl->S1, sp.L, int(sp.L1), pl->d_twj);
+    k_twj<<<blocks(sp.L1 * pl->S1, 256), 256, 0, st>>>(pl->d_jq, pl->d_e, pl->S1, sp.L, int(sp.L1),
+                                                        int(sp.L2 / QMC_ROW_E), pl->d_twj);
     QMC_PLAN_LAUNCHED();
   }
   QMC_PLAN_CHECK(spectrum_dispatch(pl));

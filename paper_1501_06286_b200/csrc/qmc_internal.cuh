@@ -53,7 +53,7 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // and the create call.
 struct PlanLayout {
   size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_cursor, off_zeta, off_W,
-      off_tw1, off_tw2, off_twL, off_tws, off_twj, off_jq, off_k1c, off_tmp, total;
+      off_tw1, off_tw2, off_twL, off_tw16, off_twj, off_jq, off_k1c, off_tmp, total;
 };
 // K1 scatter-input order (plan.cu k1_balanced_order): tried when the
 // buckets are small enough to balance (s <= 8·L2), at most k1_s1max slots;
@@ -107,6 +107,10 @@ struct qmc_plan {
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
+  // tuning knobs, read from the environment once at plan creation
+  int batch_fixed;      // QMC_BATCH_PAIRS set: no per-call halving of the batch
+  int k2_nopipe;        // QMC_K2_NOPIPE: non-persistent column pass
+  int pack_gather;      // QMC_PACK_GATHER: K0 gathers A straight from global memory
   // K1 scatter input (plan.cu k1_balanced_order): S1 staged slots per pair / per f1
   // in k1_nch chunks of at most k1_ch slots; k1_bal = 1: balanced
   // thread-major order of bucket pieces (codes: kK1First), 0: bucket order
@@ -136,12 +140,12 @@ struct qmc_plan {
   int4* d_bent;      // [s]   bucket order (e2 = e_j mod L2, then j): {j, e_j, e2,
                      //       end of this bucket if the entry is its first, else -1}
   double* d_zeta;    // [m]
-  double2* d_W;      // [L]   W[f1*L2 + f2] = DFT_L(K)[f1 + L1 f2] / L
+  double2* d_W;      // [L]   W[f1*L2 + r*L2/16 + t] = DFT_L(K)[f1 + L1 f2] / L, f2 = dif_freq(t, r)
   double2* d_tw1;    // [L1]  ω_{L1}^k
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
-  double2* d_tws;    // [L2]  row-FFT stage twiddles, stage-major (fft.cuh reg_stage)
-  double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_L^{(e_j·f1) mod L}, j = jq[q] (K1 scatter
+  double2* d_tw16;   // [16 L1] ω_{16 L1}^k (K1: the column-register part of ω_L^{e2 f1})
+  double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_L^{(e'_j·f1) mod L}, e' = e - e mod (L2/16), j = jq[q] (K1 scatter
                      //        twiddles in the K1 order; 0 for padding slots)
   int32_t* d_jq;     // [S1]  column j of slot q of the K1 order (-1: padding)
   int32_t* d_k1c;    // [k1_nch+1] chunk starts, then [k1_nch] regular-round slots per chunk

@@ -36,19 +36,23 @@ def shard_columns(t: int, world: int, rank: int) -> tuple[int, int]:
     return min(2 * p0, t), min(2 * p1, t)
 
 
-def combine_means(local: torch.Tensor, f: int, t_total: int, c0: int, group=None) -> torch.Tensor:
-    """Collective step after each rank's qmc_mean on its slab.
+def combine_means(local: torch.Tensor, f: int, t_total: int, c0: int, c1: int | None = None,
+                  group=None) -> torch.Tensor:
+    """Collective step after each rank's qmc_mean on its slab [c0, c1).
 
-    ROWMEAN_RELU: `local` holds N partial row sums; returns their SUM over
-    ranks (to be finalised by qmc_mean_finalize).  Other f: `local` holds the
-    slab's means; returns the full length-t_total vector."""
+    ROWMEAN_RELU: `local` holds N partial row sums (all zero for an empty
+    slab); returns their SUM over ranks (to be finalised by
+    qmc_mean_finalize).  Other f: `local` holds the slab's means (its first
+    c1 - c0 entries; Plan.mean returns one slot even for an empty slab);
+    returns the full length-t_total vector."""
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     if f == F_ROWMEAN_RELU:
         if world > 1:
             dist.all_reduce(local, op=dist.ReduceOp.SUM, group=group)
         return local
+    n = local.numel() if c1 is None else c1 - c0
     full = torch.zeros(t_total, dtype=local.dtype, device=local.device)
-    full[c0:c0 + local.numel()] = local
+    full[c0:c0 + n] = local[:n]
     if world > 1:
         dist.all_reduce(full, op=dist.ReduceOp.SUM, group=group)
     return full
@@ -58,7 +62,7 @@ def mean_sharded(plan, A_local: torch.Tensor, f: int, f_param: float, t_total: i
                  X_local: torch.Tensor | None = None, group=None) -> torch.Tensor:
     """qmc_mean on this rank's slab + the collective + finalize (GPU path)."""
     local = plan.mean(A_local, f, f_param, X=X_local)
-    red = combine_means(local, f, t_total, c0, group)
+    red = combine_means(local, f, t_total, c0, c0 + A_local.shape[1], group)
     if f == F_ROWMEAN_RELU:
         return plan.finalize(f, red, t_total)
     return red

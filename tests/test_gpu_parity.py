@@ -483,8 +483,9 @@ def test_k0_variants_bitwise(qmc, monkeypatch, N, s, t):
     plan = qmc.Plan.from_workload(w)
     A = qmc.to_device_colmajor(w.A, "cuda")
     X1 = plan.matmul(A).clone()
-    monkeypatch.setenv("QMC_PACK_GATHER", "1")
-    X2 = plan.matmul(A).clone()
+    monkeypatch.setenv("QMC_PACK_GATHER", "1")        # read at plan creation
+    plan2 = qmc.Plan.from_workload(w)
+    X2 = plan2.matmul(A).clone()
     torch.cuda.synchronize()
     assert torch.equal(X1, X2)
 
