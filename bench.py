@@ -1,14 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the fast QMC matrix product X = Y·A on B200 (one process per
-GPU; torchrun for N > 1).
+GPU; `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
+                    [--scaling strong|weak]
 
-A step is one pass of the whole hot path over the configured workload
-(BASELINE.json configs[C-1], default C = 2, the config the metric is quoted
-on): qmc_mean (or qmc_matmul) over this rank's contiguous column slab, X
-written to HBM, plus the collective and finalize for the fused QMC mean.
-Prints ONE JSON line on rank 0.  See DESIGN.md §Measurement.
+A step is one pass of the whole hot path over the configured workload:
+qmc_mean (or qmc_matmul) over this rank's contiguous column slab, X written
+to HBM, plus the collective and finalize of the fused QMC mean.  BASELINE.json's
+metric names no config, so the default is the largest single-GPU config,
+configs[4] (C = 5: N = 786433, s = t = 8192, fused mean of exp X; its 51.5 GB
+X fits one B200).  The other configs are parity cases and optional bench
+lines (--config C).  --scaling strong (default) splits the config's t
+columns over the N ranks in pair-aligned slabs; weak gives
+every rank the config's t columns as its block of an N·t-column problem.
+Prints ONE JSON line on rank 0.  See DESIGN.md §6 (measurement).
 """
 from __future__ import annotations
 
@@ -27,10 +34,18 @@ sys.path.insert(0, ROOT)
 
 METRIC = "fast Y·A output entries/s (fp64) and % HBM roofline at 1/2/4/8 B200"
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}
-FP64_FMA_PER_CLK_PER_SM = 64   # B200: 148 SMs x 64 DFMA/clk x 2 flop x 1.965 GHz = 37.2 TFLOP/s
+# fallback fp64 peak if profiles/fp64_peak.json is absent: 148 SM x 64 DFMA/clk x 2 x 1.965 GHz
+FP64_FMA_PER_CLK_PER_SM = 64
 N_SM = 148
 F_NAMES = {None: "none", 0: "identity_mean", 1: "affine_mean", 2: "exp_mean", 3: "rowmean_relu"}
 PHI_NAMES = {0: "identity", 1: "u-1/2", 2: "tent", 3: "invnorm(u+1/(2N))"}
+# the paper's own best fast-method rate, Table 1, context only:
+# Exp. 1, N = 16001, s = t = 1000, fast 0.741 s on a Xeon E5-2650v2 @ 2.6 GHz (Matlab R2013b)
+PAPER_CONTEXT = {"paper_fast_entries_per_s": 16001 * 1000 / 0.741,
+                 "workload": "Exp. 1, N=16001, s=t=1000, Phi^-1, random upper-triangular A (fast method)",
+                 "hardware": "Intel Xeon E5-2650v2 @ 2.6 GHz, Matlab R2013b, mean of 5 runs",
+                 "cite": "PAPER.md:779-781, 813-830 (Table 1)",
+                 "note": "other hardware and workload: context, not a target (vs_baseline stays null)"}
 
 
 def parse():
@@ -38,14 +53,15 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--t", type=int, default=0, help="override the config's t (diagnostics only)")
-    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
-                    help="N > 1: weak = every GPU runs the config's t columns (column block of a "
-                         "G·t-column problem); strong = the config's t columns split over the GPUs")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
+                    help="N > 1: strong = the config's t columns split over the GPUs (pair-aligned "
+                         "slabs); weak = every GPU runs the config's t columns (column block of a "
+                         "G·t-column problem)")
     return ap.parse_args()
 
 
@@ -54,9 +70,43 @@ def load_peaks():
     if os.path.exists(p):
         with open(p) as f:
             d = json.load(f)
-        return {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
-                "source": "measured (MEASURED_PEAKS.json)"}
-    return dict(PEAKS_FALLBACK, source="fallback (B200_PROFILING.md)")
+        pk = {"hbm_gbs": float(d["hbm_gbs"]), "sm_max_mhz": float(d.get("sm_max_mhz", 1965.0)),
+              "source": "measured (MEASURED_PEAKS.json)"}
+    else:
+        pk = dict(PEAKS_FALLBACK, source="fallback (B200_PROFILING.md)")
+    f = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(f):
+        with open(f) as fh:
+            d = json.load(fh)
+        pk["fp64_tflops"] = float(d["fp64_tflops_fma"])
+        pk["fp64_instr_per_s"] = float(d["instr_peak_per_s"])
+        pk["fp64_source"] = "measured (profiles/fp64_peak.json: DFMA-chain microbenchmark, all SMs, 1965 MHz)"
+    else:
+        pk["fp64_tflops"] = N_SM * FP64_FMA_PER_CLK_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        pk["fp64_instr_per_s"] = pk["fp64_tflops"] * 1e12 / 2
+        pk["fp64_source"] = "derived: 148 SM x 64 DFMA/clk x 2 x sm_max_mhz"
+    return pk
+
+
+def cpu_info():
+    """Host CPU model, sockets and the BLAS thread count the oracle uses."""
+    info = {"cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k.strip()] = v.strip()
+    except Exception:  # noqa: BLE001
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        import numpy as np  # noqa: F401  (loads the BLAS)
+        pools = threadpool_info()
+        info["blas"] = [{"api": p.get("internal_api"), "threads": p.get("num_threads")} for p in pools]
+    except Exception:  # noqa: BLE001
+        pass
+    return info
 
 
 # ----------------------------------------------------------------- clocks
@@ -115,8 +165,9 @@ class ClockSampler:
 # ----------------------------------------------------------------- CPU oracle (baseline)
 def cpu_oracle_rate(w, seconds: float, rows_per_block: int = 2048, seed: int = 0):
     """Entries/s of the oracle (Y by φ-table gather + NumPy GEMM) on the
-    host, over row blocks for about `seconds`; the φ table build is excluded
-    (PAPER.md:800-801)."""
+    host, over random row blocks for about `seconds`; the φ table build is
+    excluded.  The cost is linear in the rows, so the rate
+    extrapolates to all N rows."""
     import numpy as np
     import oracle as O
     tab = O.phi_table(w.phi, w.N)
@@ -142,31 +193,67 @@ def cpu_oracle_rate(w, seconds: float, rows_per_block: int = 2048, seed: int = 0
     return done * w.t / el, done, el, threads
 
 
+def cpu_baseline(w, seconds: float, repeats: int = 5):
+    """BASELINE.md §4 protocol: `repeats` timed samples of random row blocks
+    (each ~seconds/repeats), mean and median rate; host model and BLAS threads."""
+    rates, rows_tot, el_tot, threads = [], 0, 0.0, 1
+    for k in range(repeats):
+        r, rows, el, threads = cpu_oracle_rate(w, seconds / repeats, seed=k)
+        rates.append(r)
+        rows_tot += rows
+        el_tot += el
+    return {"value": statistics.median(rates), "unit": "entries/s", "cores": threads, "kind": "oracle",
+            "mean": statistics.fmean(rates), "median": statistics.median(rates), "repeats": repeats,
+            "sample": f"{repeats} repeats of random 2048-row blocks x all {w.t} columns ({rows_tot} of "
+                      f"N = {w.N} rows in {el_tot:.1f} s); rate extrapolated linearly to all N rows "
+                      f"(phi-table gather + NumPy/OpenBLAS GEMM)",
+            "extrapolated": rows_tot < w.N, "host": cpu_info()}
+
+
+def slab(w, G, rank, scaling):
+    """This rank's column slab [c0, c1) and the job's total columns."""
+    from paper_1501_06286_b200.dist import shard_columns
+    if scaling == "weak":  # every rank the config's t columns, block `rank` of a G·t-column problem
+        return rank * w.t, (rank + 1) * w.t, G * w.t
+    c0, c1 = shard_columns(w.t, G, rank)  # the config's t columns split over the ranks
+    return c0, c1, w.t
+
+
+def config_dict(w, G, scaling, tl):
+    return {"workload": w.name, "family": w.family, "N": w.N, "s": w.s, "t": w.t,
+            "t_total": G * w.t if scaling == "weak" else w.t, "t_per_gpu": tl,
+            "phi": PHI_NAMES[w.phi], "f": F_NAMES[w.f], "parallelism": f"columns/{G}",
+            "l2": "flushed between timed steps (256 MiB write, untimed)"}
+
+
 def reference_arm(args, rank, world):
-    """--impl reference: the oracle, as it stands, on the host cores (rank 0)."""
-    import numpy as np  # noqa: F401
+    """--impl reference: the oracle, as it stands, on the host cores (rank 0
+    alone; other ranks exit without work)."""
     import qmc_workloads as W
     if rank != 0:
         return
     w = W.config(args.config, t_override=args.t or None)
+    c0, c1, _ = slab(w, world, 0, args.scaling)
     rows = 1024
     # warmup + timed steps, each a bounded sample of `rows` rows × all t columns
     for _ in range(args.warmup):
         cpu_oracle_rate(w, 0.0, rows_per_block=rows, seed=1)
     t0 = time.perf_counter()
     done = 0
+    threads = 1
     for k in range(args.steps):
         _, d, _, threads = cpu_oracle_rate(w, 0.0, rows_per_block=rows, seed=100 + k)
         done += d
     el = time.perf_counter() - t0
     value = done * w.t / el
-    sample = f"{rows} random contiguous rows x all {w.t} columns per step (of N={w.N})"
+    sample = (f"{rows} random contiguous rows x all {w.t} columns per step (of N={w.N}); rate "
+              f"extrapolates linearly to all rows")
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "entries/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True, "scaling": args.scaling,
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": w.name, "N": w.N, "s": w.s, "t": w.t},
+        "config": config_dict(w, world, args.scaling, c1 - c0),
         "cpu_baseline": {"value": value, "unit": "entries/s", "cores": threads, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": value, "unit": "entries/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -175,6 +262,14 @@ def reference_arm(args, rank, world):
 
 
 # ----------------------------------------------------------------- our arm
+def k1_fp64_instr_per_item(L2):
+    """fp64 instructions per thread per K1 item (row FFT forward + inverse,
+    ×W, folded twiddles), counted from ncu smsp__sass_thread_inst_executed
+    _op_{dadd,dmul,dfma} of the round-2 build (profiles/r02_fp64_audit.txt);
+    None if not audited for this row length."""
+    return {4096: 1658.0, 8192: 1882.0}.get(L2)
+
+
 def ours(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -183,23 +278,14 @@ def ours(args, rank, world, local_rank):
     import paper_1501_06286_b200 as q
     import qmc_workloads as W
     from paper_1501_06286_b200 import _abi as abi
+    from paper_1501_06286_b200.dist import combine_means
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
-    from paper_1501_06286_b200.dist import combine_means, shard_columns
     w = W.config(args.config, t_override=args.t or None)
     G = world
-    if args.scaling == "weak":
-        # every rank: the config's t columns, as column block `rank` of a
-        # G·t-column problem (blocks of A equal); per-GPU work fixed
-        c0, c1 = rank * w.t, (rank + 1) * w.t
-        t_total = G * w.t
-        A_block = w.A
-    else:
-        # the config's t columns split over the ranks; total work fixed
-        c0, c1 = shard_columns(w.t, G, rank)
-        t_total = w.t
-        A_block = w.A[:, c0:c1]
+    c0, c1, t_total = slab(w, G, rank, args.scaling)
+    A_block = w.A if args.scaling == "weak" else w.A[:, c0:c1]
     tl = c1 - c0
     plan = q.Plan.from_workload(w, device=dev)
     A_host = np.ascontiguousarray(A_block.T)                 # (tl, s) row-major = A slab col-major
@@ -211,17 +297,17 @@ def ours(args, rank, world, local_rank):
         out = torch.empty(N, dtype=torch.float64, device=dev)
         res = torch.empty(1, dtype=torch.float64, device=dev)
     elif f is not None:
-        out = torch.empty(tl, dtype=torch.float64, device=dev)
+        out = torch.empty(max(tl, 1), dtype=torch.float64, device=dev)
     plan.call_workspace(tl, -1 if f is None else f)
 
-    def step():
+    def step(Ain):
         """One pass of the hot path over this rank's column slab + the
         collective of the fused mean (dist.combine_means) + finalize."""
         if f is None:
-            plan.matmul(A, X)
+            plan.matmul(Ain, X)
             return None
-        plan.mean(A, f, fp, X=X, out=out)
-        red = combine_means(out, f, t_total, c0)
+        plan.mean(Ain, f, fp, X=X, out=out)
+        red = combine_means(out, f, t_total, c0, c1)
         if f == W.F_ROWMEAN_RELU:
             plan.finalize(f, red, t_total, out=res)
             return res
@@ -229,7 +315,7 @@ def ours(args, rank, world, local_rank):
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     for _ in range(args.warmup):
-        step()
+        step(A)
     torch.cuda.synchronize()
     if G > 1:
         dist.barrier()
@@ -248,7 +334,7 @@ def ours(args, rank, world, local_rank):
     for k in range(args.steps):
         flush.zero_()                     # L2 flush between timed steps (untimed)
         evs[k][0].record(stream)
-        step()
+        step(A)
         evs[k][1].record(stream)
     torch.cuda.synchronize()
     if G > 1:
@@ -276,24 +362,26 @@ def ours(args, rank, world, local_rank):
     for name, (n, ms) in prof.items():
         if n:
             kernels[name] = {"launches": n, "ms_total": ms, "share": ms / tot_prof}
-    dom = max(kernels, key=lambda k: kernels[k]["ms_total"])
-    dn, dms = kernels[dom]["launches"], kernels[dom]["ms_total"]
-    fp64_peak = N_SM * FP64_FMA_PER_CLK_PER_SM * 2 * peaks["sm_max_mhz"] * 1e6 / 1e12
+    dom = max(kernels, key=lambda k: kernels[k]["ms_total"]) if kernels else None
+    fp64_peak = peaks["fp64_tflops"]
+    roof = None
     if dom == "k_rows":
-        flops = args.steps * npairs * L1 * 2 * 5.0 * L2 * math.log2(L2)
+        dn, dms = kernels[dom]["launches"], kernels[dom]["ms_total"]
+        items = args.steps * npairs * L1
+        flops = items * 2 * 5.0 * L2 * math.log2(L2)
         achieved = flops / (dms / 1e3) / 1e12
         roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": achieved / fp64_peak, "traffic": None, "kernel": dom,
-                "work": "algorithmic fp64 flops = 2 FFTs x 5 L2 log2 L2 per row-CTA",
-                "peak_source": "148 SM x 64 DFMA/clk x 2 x sm_max_mhz (DESIGN.md)"}
-    elif dom == "k_cols":
-        flops = args.steps * npairs * L2 * 5.0 * L1 * math.log2(max(L1, 2))
-        achieved = flops / (dms / 1e3) / 1e12
-        roof = {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp64_peak, "traffic": None, "kernel": dom}
-    else:  # HBM-bound classes: algorithmic bytes
-        if dom == "k_gather":
-            nbytes = args.steps * (8.0 * N * tl + 4.0 * N * dn / args.steps)
+                "work": "algorithmic fp64 flops per launch = K1 items (L1 rows x pairs) x 2 FFTs x "
+                        "5 L2 log2 L2 (DESIGN.md §6)",
+                "peak_source": peaks["fp64_source"]}
+        ipi = k1_fp64_instr_per_item(L2)
+        if ipi:  # the fp64-pipe view: audited instructions per item / measured instruction peak
+            roof["fp64_instr_frac"] = items * (L2 // 16) * ipi / (dms / 1e3) / peaks["fp64_instr_per_s"]
+    elif dom is not None:
+        dn, dms = kernels[dom]["launches"], kernels[dom]["ms_total"]
+        if dom == "k_cols":   # HBM: U read + X written per launch
+            nbytes = args.steps * (16.0 * L * npairs + 8.0 * N * tl)
         elif dom == "k_pack":
             nbytes = args.steps * 8.0 * w.s * tl
         else:
@@ -301,14 +389,15 @@ def ours(args, rank, world, local_rank):
         achieved = nbytes / (dms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": dom}
-    roof["launches"] = dn
-    roof["avg_launch_ms"] = dms / dn
-    traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(traffic_file):
-        with open(traffic_file) as fh:
-            tf = json.load(fh).get(f"c{args.config}", {})
-        if dom in tf:
-            roof["traffic"] = tf[dom]
+    if roof is not None:
+        roof["launches"] = dn
+        roof["avg_launch_ms"] = dms / dn
+        traffic_file = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(traffic_file):
+            with open(traffic_file) as fh:
+                tf = json.load(fh).get(f"c{args.config}", {})
+            if dom in tf and tf.get("_batch_pairs") in (None, info["batch_pairs"]):
+                roof["traffic"] = tf[dom]
     # whole-step HBM roofline (north star): compulsory bytes = read A + write X
     step_bytes = 8.0 * (N + w.s) * tl  # this rank's compulsory bytes (rank 0 reports)
     hbm_ach = step_bytes / (ms_step / 1e3) / 1e9
@@ -316,17 +405,17 @@ def ours(args, rank, world, local_rank):
            "frac": hbm_ach / peaks["hbm_gbs"], "frac_vs_8TBps_nominal": hbm_ach / 8000.0,
            "peak_source": peaks["source"]}
 
-    # ---- e2e: host buffers in, result back to host, through the C ABI
-    e2e = None
+    # ---- e2e: host buffers in, result back to host, through the public API
+    A_pin = torch.from_numpy(A_host).pin_memory()
+    A_dev2 = torch.empty(A_host.shape, dtype=torch.float64, device=dev)
     if G == 1:
-        A_pin = torch.from_numpy(A_host).pin_memory()
-        A_dev2 = torch.empty_like(A_pin, device=dev)
         f_e2e = f if f is not None else W.F_IDENTITY
         n_res = 1 if f_e2e == W.F_ROWMEAN_RELU else tl
         out_pin = torch.empty(n_res, dtype=torch.float64).pin_memory()
         out_dev = torch.empty(max(N, tl), dtype=torch.float64, device=dev)
         ws = plan.call_workspace(tl, f_e2e)
         st = stream.cuda_stream
+
         def e2e_step():
             abi.qmc_mean_host(plan.handle, A_pin, w.s, tl, f_e2e, fp, out_pin, A_dev2, X, max(tl, 1),
                               out_dev, ws, ws.numel(), st)
@@ -347,15 +436,17 @@ def ours(args, rank, world, local_rank):
                "ms_per_step": e_ms / args.steps, "ms_min": min(ee), "ms_median": sorted(ee)[len(ee) // 2],
                "ms_max": max(ee), "api": "qmc_mean_host (C ABI, pinned host A)"}
     else:
-        A_pin = torch.from_numpy(A_host).pin_memory()
-        A_dev2 = torch.empty_like(A_pin, device=dev)
+        A2 = A_dev2.t()  # the copied slab, column-major (s, tl): the step computes on it
         ee = []
+        host = None
         for k in range(args.warmup + args.steps):
             flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
             A_dev2.copy_(A_pin, non_blocking=True)
-            r = step()
+            r = step(A2)
             host = r.cpu() if r is not None else X[0, :1].cpu()
             b.record(stream)
             torch.cuda.synchronize()
@@ -367,37 +458,53 @@ def ours(args, rank, world, local_rank):
         e2e = {"value": entries * args.steps / (e_ms / 1e3), "unit": "entries/s",
                "h2d_bytes_per_step": int(A_pin.numel() * 8),
                "d2h_bytes_per_step": int(host.numel() * 8), "ms_per_step": e_ms / args.steps,
-               "api": "Plan.mean + torch.distributed (pinned host A slab per rank)"}
+               "api": "Plan.mean + torch.distributed (pinned host A slab per rank, copied and "
+                      "computed on every step)"}
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
-        rate, rows, el, threads = cpu_oracle_rate(w, args.cpu_seconds)
-        cpu = {"value": rate, "unit": "entries/s", "cores": threads, "kind": "oracle",
-               "sample": f"{rows} of {w.N} rows x all {w.t} columns in {el:.1f} s "
-                         f"(phi-table gather + NumPy/OpenBLAS GEMM, host has {os.cpu_count()} cpus)"}
+        cpu = cpu_baseline(w, args.cpu_seconds)
 
     if rank == 0:
+        cfg = config_dict(w, G, args.scaling, tl)
         line = {
             "metric": METRIC, "value": value, "unit": "entries/s", "n_gpus": G,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic",
-            "config": {"workload": w.name, "family": w.family, "N": N, "s": w.s, "t": w.t,
-                       "t_total": t_total, "t_per_gpu": tl,
-                       "phi": PHI_NAMES[w.phi], "f": F_NAMES[w.f], "L": L, "L1": L1, "L2": L2,
-                       "batch_pairs": info["batch_pairs"], "parallelism": f"columns/{G}",
-                       "l2": "flushed between timed steps (256 MiB write, untimed)"},
+            "higher_is_better": True, "scaling": args.scaling if G > 1 else "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cfg,
+            "plan": {"L": L, "L1": L1, "L2": L2, "batch_pairs": info["batch_pairs"],
+                     "k1_input": {1: "balanced", 0: "bucket order", 2: "dense"}.get(info["k1_order"])},
             "roofline": roof, "hbm_roofline_step": hbm, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(launches), "clocks": clocks, "kernels": kernels,
+            "paper_context": PAPER_CONTEXT,
         }
         print(json.dumps(line), flush=True)
 
 
+def _free_port():
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # no torchrun environment: re-launch under torch.distributed.run with one rank per GPU
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+               *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: WORLD_SIZE={world} overrides --gpus {args.gpus}", file=sys.stderr)
     if args.impl == "reference":
         reference_arm(args, rank, world)
         return

@@ -14,11 +14,18 @@ def main():
     ap.add_argument("--t", type=int, default=0, help="override t (columns)")
     ap.add_argument("--nox", action="store_true", help="means only: X is not written")
     ap.add_argument("--matmul", action="store_true", help="qmc_matmul instead of the config's f")
+    ap.add_argument("--poly", type=int, default=0, help="D: a polynomial-lattice workload of degree D instead "
+                    "(smallest primitive p, s = 300, t = --t or 16)")
     a = ap.parse_args()
     import torch
     import paper_1501_06286_b200 as q
     import qmc_workloads as W
-    w = W.config(a.config, t_override=a.t or None)
+    if a.poly:
+        # smallest primitive polynomials over F_2 by integer encoding
+        p = {8: 285, 10: 1033, 12: 4179, 14: 16427, 16: 65581}[a.poly]
+        w = W.custom_poly(a.poly, p, 300, a.t or 16, W.PHI_SHIFT_HALF, seed=a.poly)
+    else:
+        w = W.config(a.config, t_override=a.t or None)
     plan = q.Plan.from_workload(w)
     A = q.to_device_colmajor(w.A, "cuda")
     X = q.x_empty(plan.N, w.t, "cuda")
