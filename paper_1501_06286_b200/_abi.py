@@ -12,7 +12,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libqmc.so")
+# QMC_LIB selects another build of the same sources (diagnostic variants, e.g.
+# variants/libqmc_phase.so built with -DQMC_PHASE_TIMING); default: in-tree
+LIB_PATH = os.environ.get("QMC_LIB") or os.path.join(_HERE, "libqmc.so")
 
 QMC_FAMILY_LATTICE, QMC_FAMILY_POLY = 0, 1
 QMC_PHI_IDENTITY, QMC_PHI_SHIFT_HALF, QMC_PHI_TENT, QMC_PHI_INVNORM_MID, QMC_PHI_BERNOULLI2 = 0, 1, 2, 3, 4

@@ -40,7 +40,14 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
+    """Compile libqmc.so (or, with `out`, a variant build with `extra` flags)."""
+    if out is not None:
+        cmd = [_nvcc(), *NVCC_FLAGS, *(extra or []), "-o", out] + [os.path.join(CSRC, f) for f in SOURCES]
+        res = subprocess.run(cmd, capture_output=True, text=True)
+        if res.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        return out
     if not force and not _stale():
         return LIB
     cmd = [_nvcc(), *NVCC_FLAGS, *os.environ.get("QMC_NVCC_EXTRA", "").split()]

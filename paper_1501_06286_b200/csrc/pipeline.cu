@@ -266,11 +266,11 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // shared memory of K1: the padded row with its padding and overflow slots
-// (k1_row_slots), the staging of CH slots (CH a multiple of 4), the staging
-// mbarrier
+// (k1_row_slots); staged plans add the staging of CH slots (a, twiddle, code:
+// 36 B each, CH a multiple of 4) and its mbarrier
 template <int L2>
 __host__ __device__ constexpr size_t rows_smem(int CH) {
-  return size_t(k1_row_slots(L2, QMC_ROW_E)) * 16 + size_t(CH) * (16 + 16 + 4) + 16;
+  return size_t(k1_row_slots(L2, QMC_ROW_E)) * 16 + (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16 : 0);
 }
 
 struct K1Args {
@@ -278,9 +278,9 @@ struct K1Args {
   const int32_t* __restrict__ e2q;     // [S1] bucket codes
   const uint32_t* __restrict__ occ;    // nonempty buckets
   int64_t S1;
-  int CH;                              // staging slots (capacity)
   const int32_t* __restrict__ k1c;     // [nch+1] chunk starts, [nch] regular-round slots
   int nch, bal;
+  int CH;                              // > 0: staged (one chunk of CH slots, prefetched)
   int dense;                           // asort holds T[p][f1][e2] (k_dense_cols): no scatter
   const double2* __restrict__ twj;     // [L1][S1]
   const double2* __restrict__ tw2;     // [L2] ω_{L2}^i (row-FFT stage twiddles)
@@ -296,22 +296,23 @@ struct K1Args {
   double* __restrict__ colsum;
 };
 
+// Staged mode (plans whose balanced order is one chunk of at most CH slots):
+// the scatter input of the NEXT item is copied into shared memory by three
+// bulk async copies (one thread, completing on an mbarrier) while this item's
+// FFTs run, so its L2 latency is hidden.
 template <int L2>
-struct K1Smem {
-  double2* S;     // padded row
+struct K1Stage {
   double2* stA;   // staging: a
   double2* stW;   // staging: twiddles
-  int32_t* stE;   // staging: e2q
-  uint64_t* bar;  // staging complete (one phase per chunk)
-  __device__ K1Smem(double2* base, int CH)
-      : S(base),
-        stA(base + k1_row_slots(L2, QMC_ROW_E)),
+  int32_t* stE;   // staging: codes
+  uint64_t* bar;  // staging complete (one phase per item)
+  __device__ K1Stage(double2* base, int CH)
+      : stA(base + k1_row_slots(L2, QMC_ROW_E)),
         stW(stA + CH),
         stE(reinterpret_cast<int32_t*>(stW + CH)),
         bar(reinterpret_cast<uint64_t*>(stE + CH)) {}
 };
 
-// mbarrier + bulk async copy (the staging of K1's scatter input)
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -338,60 +339,89 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                : "memory");
 }
 
-// stage chunk c of item it: three bulk async copies issued by one thread
-// (a of the pair, twiddles of f1, bucket codes), completing on sm.bar.  The
-// staging buffers must be free.  Chunk starts are multiples of 4 slots; the
-// e2q copy is rounded up to 16 bytes (the table has 16 bytes of slack).
+// stage the single chunk of item it (a of the pair, twiddles of f1, codes);
+// the staging buffers must be free.  The code copy is rounded up to 16 bytes
+// (the table has 16 bytes of slack).
 template <int L2>
-__device__ __forceinline__ void k1_issue(const K1Args& a, const K1Smem<L2>& sm, int it, int c) {
+__device__ __forceinline__ void k1_issue(const K1Args& a, const K1Stage<L2>& sg, int it) {
   const int f1 = it % a.L1, p = it / a.L1;
-  const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
+  const int n = __ldg(&a.k1c[1]);
   const unsigned b16 = unsigned(n) * 16u, b4 = unsigned((n + 3) & ~3) * 4u;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reads before the async writes
-  mbar_expect_tx(sm.bar, 2 * b16 + b4);
-  bulk_g2s(sm.stA, a.asort + int64_t(p) * a.S1 + q0, b16, sm.bar);
-  bulk_g2s(sm.stW, a.twj + int64_t(f1) * a.S1 + q0, b16, sm.bar);
-  bulk_g2s(sm.stE, a.e2q + q0, b4, sm.bar);
+  mbar_expect_tx(sg.bar, 2 * b16 + b4);
+  bulk_g2s(sg.stA, a.asort + int64_t(p) * a.S1, b16, sg.bar);
+  bulk_g2s(sg.stW, a.twj + int64_t(f1) * a.S1, b16, sg.bar);
+  bulk_g2s(sg.stE, a.e2q, b4, sg.bar);
 }
 
-// One K1 item (f1, pair); its chunk 0 must have been issued.  next >= 0: the
-// item whose chunk 0 is issued once this item's staging is consumed (it then
-// overlaps this item's FFTs).
+// One K1 item (f1, pair).  The scatter input of the item — per slot of the
+// plan's order: a_j of the pair (asort, K0), the twiddle of row f1 (twj),
+// the code (e2q) — is read straight from global memory (L2-resident: asort
+// per batch, twj and e2q per plan) into registers, several slots in flight
+// per thread, so no staging buffer, copy or extra barrier is needed.
 template <int L2>
-__device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, unsigned& phase, int item, int next) {
+__device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, int next, unsigned& phase) {
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
-  double2* S = sm.S;
   const int tid = threadIdx.x;
   const int L1 = a.L1;
   const int f1 = item % L1, p = item / L1;
-  const int nch = a.nch;
+  const int nch = a.CH > 0 ? 0 : a.nch;
+  const double2* ap = a.asort + int64_t(p) * a.S1;
+  const double2* tp = a.twj + int64_t(f1) * a.S1;
   QMC_TS(0);
-  for (int c = 0; c < nch; ++c) {
-    mbar_wait(sm.bar, phase);
+  if (a.CH > 0) {  // staged mode: this item's chunk was copied during the previous item
+    const K1Stage<L2> sg(S, a.CH);
+    mbar_wait(sg.bar, phase);
     phase ^= 1u;
     __syncthreads();  // every use of S by the previous item is done
+    const int n = __ldg(&a.k1c[1]), nreg = __ldg(&a.k1c[2]);
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = tid; i < nreg; i += NT) {
+      const int cd = sg.stE[i];
+      const double2 pr = cmul(sg.stA[i], sg.stW[i]);
+      acc = (cd & kK1First) ? pr : cadd(acc, pr);
+      S[padE<E>(cd & 0x3fff)] = acc;
+    }
+    if (n > nreg) {  // fix-up: later pieces of split buckets, in order
+      __syncthreads();
+      for (int r = nreg + tid; r < n; r += NT) {
+        const int rc = sg.stE[r];
+        const int e2 = rc & 0x3fff, o0 = (rc >> 14) & 63, cnt = rc >> 20;
+        double2 t = S[padE<E>(e2)];
+        for (int k = 0; k < cnt; ++k) t = cadd(t, S[padE<E>(L2 + 1 + o0 + k)]);
+        S[padE<E>(e2)] = t;
+      }
+    }
+    __syncthreads();  // staging consumed
+    if (tid == 0 && next >= 0) k1_issue<L2>(a, sg, next);  // overlaps this item's FFTs
+  }
+  for (int c = 0; c < nch; ++c) {
+    const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
+    // every use of S by the previous item (or the previous chunk's fix-ups)
+    // is done before this chunk's stores
+    __syncthreads();
     // scatter a' = P a fused with the first DFT dimension:
-    //   T[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e_j·f1) mod L}
+    //   T'[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e'_j·f1) mod L}
     // (S holds the previous item's data elsewhere: only nonempty buckets are
     // read back, by the occupancy mask)
-    const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
     if (a.bal) {
       // balanced order: the thread's slots tid, tid + NT, ... hold its
       // bucket pieces one after the other, in j order; the running sum is
       // stored after every entry (the last store of a piece is its total)
       const int nreg = __ldg(&a.k1c[nch + 1 + c]);
       double2 acc = make_double2(0.0, 0.0);
-      for (int i = tid; i < nreg; i += NT) {
-        const int cd = sm.stE[i];
-        const double2 pr = cmul(sm.stA[i], sm.stW[i]);
+#pragma unroll 4
+      for (int i = q0 + tid; i < q0 + nreg; i += NT) {
+        const int cd = __ldg(&a.e2q[i]);
+        const double2 pr = cmul(__ldg(&ap[i]), __ldg(&tp[i]));
         acc = (cd & kK1First) ? pr : cadd(acc, pr);
         S[padE<E>(cd & 0x3fff)] = acc;
       }
       if (n > nreg) {  // fix-up: later pieces of split buckets, in order
         __syncthreads();
-        for (int r = nreg + tid; r < n; r += NT) {
-          const int rc = sm.stE[r];
+        for (int r = q0 + nreg + tid; r < q0 + n; r += NT) {
+          const int rc = __ldg(&a.e2q[r]);
           const int e2 = rc & 0x3fff, o0 = (rc >> 14) & 63, cnt = rc >> 20;
           double2 t = S[padE<E>(e2)];
           for (int k = 0; k < cnt; ++k) t = cadd(t, S[padE<E>(L2 + 1 + o0 + k)]);
@@ -399,35 +429,21 @@ __device__ __forceinline__ void k1_item(const K1Args& a, const K1Smem<L2>& sm, u
         }
       }
     } else {
-      // bucket order: the first entry of a bucket (size in e2q >> 13) sums
-      // it in j order and stores T; a bucket continued from the previous
-      // chunk is added to by this chunk's entry 0
+      // bucket order (one chunk): the first entry of a bucket (nonzero size
+      // field e2q >> 13) sums it in j order — up to the next head — and
+      // stores T
       for (int i = tid; i < n; i += NT) {
-        const int pk = sm.stE[i];
-        const int len = pk >> 13, e2 = pk & 8191;
-        double2 acc = cmul(sm.stA[i], sm.stW[i]);
-        const int end = min(n, i + len);
-        for (int k = i + 1; k < end; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));  // collisions (rare)
-        if (len > 0) S[padE<E>(e2)] = acc;
+        const int pk = __ldg(&a.e2q[q0 + i]);
+        if ((pk >> 13) > 0) {
+          double2 acc = cmul(__ldg(&ap[q0 + i]), __ldg(&tp[q0 + i]));
+          for (int k = i + 1; k < n && (__ldg(&a.e2q[q0 + k]) >> 13) == 0; ++k)
+            acc = cadd(acc, cmul(__ldg(&ap[q0 + k]), __ldg(&tp[q0 + k])));
+          S[padE<E>(pk & 8191)] = acc;
+        }
       }
-      if (c > 0 && tid == 0 && (sm.stE[0] >> 13) == 0) {
-        // a bucket continued from the previous chunk: its remaining entries
-        // are added by one thread after the heads (S[e2] is not touched by
-        // this chunk's heads, whose buckets all start in this chunk)
-        const int pk = sm.stE[0];
-        double2 acc = cmul(sm.stA[0], sm.stW[0]);
-        for (int k = 1; k < n && sm.stE[k] == pk; ++k) acc = cadd(acc, cmul(sm.stA[k], sm.stW[k]));
-        S[padE<E>(pk & 8191)] = cadd(S[padE<E>(pk & 8191)], acc);
-      }
-    }
-    __syncthreads();  // staging consumed
-    if (tid == 0) {
-      if (c + 1 < nch)
-        k1_issue<L2>(a, sm, item, c + 1);
-      else if (next >= 0)
-        k1_issue<L2>(a, sm, next, 0);  // overlaps this item's FFTs
     }
   }
+  __syncthreads();  // the row T' is complete
   QMC_TS(1);
   double2 v[E];
   if (a.dense) {  // the first DFT dimension was done by k_dense_cols: load the row
@@ -500,14 +516,16 @@ template <int L2>
 __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_ROWS_MINB512 : QMC_ROWS_MINB))
     k_rows16(K1Args a) {
   extern __shared__ double2 smem[];
-  const K1Smem<L2> sm(smem, a.CH);
   const int nitems = a.L1 * a.np;
-  if (threadIdx.x == 0) mbar_init(sm.bar, 1);
-  __syncthreads();
-  if (threadIdx.x == 0 && int(blockIdx.x) < nitems && a.nch > 0) k1_issue<L2>(a, sm, blockIdx.x, 0);
   unsigned phase = 0;
+  if (a.CH > 0) {
+    const K1Stage<L2> sg(smem, a.CH);
+    if (threadIdx.x == 0) mbar_init(sg.bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sg, blockIdx.x);
+  }
   for (int item = blockIdx.x; item < nitems; item += gridDim.x)
-    k1_item<L2>(a, sm, phase, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1);
+    k1_item<L2>(a, smem, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1, phase);
 }
 
 // ---------------------------------------------------------------- K2
@@ -1224,7 +1242,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   a.e2q = pl->d_e2q;
   a.occ = pl->d_occ;
   a.S1 = pl->S1;
-  a.CH = pl->k1_ch;
+  a.CH = pl->k1_stage;
   a.k1c = pl->d_k1c;
   a.nch = pl->k1_nch;
   a.bal = pl->k1_bal;
@@ -1249,8 +1267,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
 template <int L2>
 static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                        double* colsum, cudaStream_t st) {
-  const int CH = pl->k1_ch;
-  const size_t smem = rows_smem<L2>(CH);
+  const size_t smem = rows_smem<L2>(pl->k1_stage);
   auto kern = k_rows16<L2>;
   set_smem_attr(kern, smem);
   static int nsm = 0;

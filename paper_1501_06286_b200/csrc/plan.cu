@@ -410,14 +410,10 @@ __global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict_
   twj[i] = make_double2(cv, -sv);
 }
 
-// Staging slots of one K1 chunk (36 B each: a, twiddle, code) that fit next
-// to the row at the row kernel's residency: one CTA per SM for rows of 8192
-// (the whole 227 KB), two otherwise.
-static int k1_slot_budget(int64_t L2) {
-  const int64_t limit = L2 >= 8192 ? 232448 : 115712;
-  const int64_t row = k1_row_slots(L2, QMC_ROW_E) * 16 + 16;  // row slots, mbarrier
-  return int(std::min<int64_t>(4096, (limit - row - 64) / 36) / 4 * 4);
-}
+// Slots of one K1 chunk: K1 reads its scatter input straight from global
+// memory, so a chunk is bounded only by the balanced order's overflow slots
+// (kK1Ovf per chunk, 16 pieces per bucket); one chunk normally suffices.
+static int k1_slot_budget(int64_t /*L2*/) { return 1 << 24; }
 
 // K1 "balanced" order of the scatter input (pipeline.cu k1_item).  Buckets
 // e2 are cut into chunks of whole buckets.  In a chunk of n entries, with
@@ -766,7 +762,11 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     const int NT = int(sp.L2 / QMC_ROW_E);
     std::vector<int32_t> jq, code, cs, cr;
     int chmax = 0;
-    pl->k1_bal = !getenv("QMC_K1_HEADS") && k1_try_balanced(s, sp.L2) &&
+    // a' at least half full with more than 2 entries per bucket: the dense
+    // first pass (below) is cheaper than any scatter
+    const bool want_dense = 2 * s >= sp.L && s > 2 * sp.L2 && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS") &&
+                            !getenv("QMC_NO_DENSE");
+    pl->k1_bal = !want_dense && !getenv("QMC_K1_HEADS") && k1_try_balanced(s, sp.L2) &&
                  k1_balanced_order(hb, hbent, sp.L2, NT, k1_slot_budget(sp.L2), k1_s1max(s, sp.L2, sp.L), jq, code, cs, cr,
                                    chmax);
     // dense input: the balanced order does not apply and a' is at least half
@@ -774,8 +774,8 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     // by e (then j) with per-e starts, so k_pack_dense sums collisions in j
     // order.  jlist (s) fits jq and estart (L+1) fits e2q: both hold
     // k1_s1max >= L slots when 2s >= L
-    pl->k1_dense = !pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 && !getenv("QMC_K1_HEADS") &&
-                   !getenv("QMC_NO_DENSE");
+    pl->k1_dense = want_dense || (!pl->k1_bal && 2 * s >= sp.L && k2_split_R(sp.L1) > 0 &&
+                                  !getenv("QMC_K1_HEADS") && !getenv("QMC_NO_DENSE"));
     if (pl->k1_dense) {
       std::vector<int32_t> estart(size_t(sp.L) + 1, 0), jlist(static_cast<size_t>(s));
       for (int64_t q = 0; q < s; ++q) ++estart[size_t(hbent[q].y) + 1];
@@ -793,21 +793,22 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     } else if (pl->k1_bal) {
       pl->S1 = int64_t(jq.size());
       pl->k1_ch = chmax;
+      // one chunk that fits the staging next to the row (36 B per slot, at
+      // the row kernel's residency): staged and prefetched during the
+      // previous item's FFTs; otherwise K1 reads its input from global memory
+      const int64_t limit = sp.L2 >= 8192 ? 232448 : 115712;
+      const int64_t room = (limit - k1_row_slots(sp.L2, QMC_ROW_E) * 16 - 16 - 64) / 36 / 4 * 4;
+      if (cr.size() == 1 && chmax <= room) pl->k1_stage = int((chmax + 3) / 4 * 4);
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     } else {
-      // bucket order, chunks of CH entries (CH a multiple of 32)
+      // bucket order, one chunk
       jq.clear();
-      cs.clear();
-      cr.clear();
       pl->S1 = s;
-      pl->k1_ch = int(std::min<int64_t>(sp.L2 >= 8192 ? 2048 : 1024, (s + 31) / 32 * 32));
+      pl->k1_ch = int(s);
       jq.resize(size_t(s));
       for (int64_t q = 0; q < s; ++q) jq[q] = hbent[q].x;
-      for (int64_t q0 = 0; q0 < s; q0 += pl->k1_ch) {
-        cr.push_back(int(std::min<int64_t>(pl->k1_ch, s - q0)));
-        cs.push_back(int(q0));
-      }
-      cs.push_back(int(s));
+      cs.assign({0, int(s)});
+      cr.assign({int(s)});
     }
     pl->k1_nch = int(cr.size());
     cs.insert(cs.end(), cr.begin(), cr.end());

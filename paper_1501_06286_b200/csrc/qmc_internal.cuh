@@ -116,6 +116,7 @@ struct qmc_plan {
   // thread-major order of bucket pieces (codes: kK1First), 0: bucket order
   int64_t S1;
   int k1_bal, k1_nch, k1_ch;
+  int k1_stage;  // > 0: the balanced order is one chunk of k1_stage slots, staged in shared memory
   int k1_dense;  // 1: dense first pass (k_pack_dense + k_dense_cols), S1 = L, no chunks
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the

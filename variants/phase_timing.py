@@ -31,4 +31,6 @@ for bp in (32, 64):
     d = np.diff(buf[:, :6], axis=1)
     tot = buf[:, 5] - buf[:, 0]
     print(f"c{cfg} batch {bp}: items {n}: median cycles scatter/fwd/W/inv/store:",
-          np.median(d, axis=0).astype(int), "total median", int(np.median(tot)), "max", int(tot.max()))
+          np.median(d, axis=0).astype(int), "total median", int(np.median(tot)), "max", int(tot.max()),
+          "| of the scatter, chunk waits (mbarrier + barrier):", int(np.median(buf[:, 6])),
+          "main loops:", int(np.median(buf[:, 7])))
