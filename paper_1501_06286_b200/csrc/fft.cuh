@@ -627,7 +627,8 @@ __host__ __device__ constexpr int reg_split(int n) {  // R with n = R·M, both d
   return direct_radix(n) ? 1 : 0;
 }
 
-// twN[k·ts] = ω_N^k (a table of a multiple of N read with stride ts).
+// twN[k·ts] = ω_N^k (a table of a multiple of N read with stride ts; global
+// or shared memory).
 template <int N, int DIR>
 __device__ __forceinline__ void reg_dft(double2* v, const double2* __restrict__ twN, int ts = 1) {
   if constexpr (direct_radix(N)) {
@@ -644,7 +645,7 @@ __device__ __forceinline__ void reg_dft(double2* v, const double2* __restrict__ 
       Dft<M, DIR>::run(sv);
 #pragma unroll
       for (int k2 = 0; k2 < M; ++k2)
-        y[r * M + k2] = (r * k2 == 0) ? sv[k2] : cmul(sv[k2], twid<DIR>(__ldg(&twN[r * k2 * ts])));
+        y[r * M + k2] = (r * k2 == 0) ? sv[k2] : cmul(sv[k2], twid<DIR>(twN[r * k2 * ts]));
     }
 #pragma unroll
     for (int k2 = 0; k2 < M; ++k2) {

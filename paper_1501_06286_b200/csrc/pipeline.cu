@@ -1029,7 +1029,7 @@ __device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* d
 
 template <int R, int M, int EP>
 __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2 (*red)[16],
-                                          int lg2L2) {
+                                          const double2* tw1) {
   constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = kP2PG;
   const EpiArgs& E = a.E;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -1053,10 +1053,10 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
     double2 x[M];
 #pragma unroll
     for (int mm = 0; mm < M; ++mm) x[mm] = Tp[(r + R * mm) * kUB];
-    reg_dft<M, +1>(x, a.tw1, L1 / M);  // (conj(ω_L^{e2 f1}) was applied by K1)
+    reg_dft<M, +1>(x, tw1, L1 / M);  // (conj(ω_L^{e2 f1}) was applied by K1)
 #pragma unroll
     for (int k2 = 1; k2 < M; ++k2)
-      if (r) x[k2] = cmul(x[k2], twid<+1>(__ldg(&a.tw1[r * k2])));
+      if (r) x[k2] = cmul(x[k2], twid<+1>(tw1[r * k2]));
 #pragma unroll
     for (int k2 = 0; k2 < M; ++k2) Tp[(r + R * k2) * kUB] = x[k2];
   }
@@ -1069,7 +1069,7 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
     double2 z[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) z[r] = Tp[(r + R * k2) * kUB];
-    reg_dft<R, +1>(z, a.tw1, L1 / R);
+    reg_dft<R, +1>(z, tw1, L1 / R);
     double rr;
 #pragma unroll
     for (int k1 = 0; k1 < R; ++k1) {
@@ -1102,6 +1102,8 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
   extern __shared__ double2 sm[];
   int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
   __shared__ double2 red[kP2Thr / 32][16];
+  __shared__ double2 tw1s[L1];  // ω_{L1}^k: the stage twiddles, read from shared memory
+  for (int i = threadIdx.x; i < L1; i += kP2Thr) tw1s[i] = __ldg(&a.tw1[i]);
   const int ntiles = a.ntx * a.ngroups;
 #pragma unroll
   for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
@@ -1120,7 +1122,7 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
     cp_async_commit();
     asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
     __syncthreads();
-    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), red, lg2L2);
+    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), red, tw1s);
     __syncthreads();  // stage st and red are reused
   }
   cp_async_wait_all();
