@@ -82,6 +82,7 @@ class Plan:
         self.info = abi.qmc_plan_info(self.handle)
         self.N, self.m, self.phi = self.info["N"], self.info["m"], phi
         self._ws = None
+        self._ws_need = {}  # (t, f) -> call-workspace bytes (qmc_call_workspace_size)
 
     @classmethod
     def lattice(cls, N: int, z, phi: int, device=None, delta: float = 0.0) -> "Plan":
@@ -99,7 +100,10 @@ class Plan:
         return cls.lattice(w.N, w.z, w.phi, device)
 
     def call_workspace(self, t: int, f: int = abi.QMC_F_NONE) -> torch.Tensor:
-        nbytes = abi.qmc_call_workspace_size(self.handle, t, f)
+        key = (t, f)
+        nbytes = self._ws_need.get(key)
+        if nbytes is None:
+            nbytes = self._ws_need[key] = abi.qmc_call_workspace_size(self.handle, t, f)
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
         return self._ws

@@ -528,6 +528,142 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
     k1_item<L2>(a, smem, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1, phase);
 }
 
+// ---------------------------------------------------------------- one-row plans
+// L1 = 1 (L = L2 <= 8192, e.g. config 1): the whole path of one column pair
+// in one CTA, one launch per call — the pair's two columns of A into shared
+// memory, per bucket e2 = t + NT q the sum of its a_j (f1 = 0: no twiddles),
+// forward row FFT, ×W, inverse row FFT, then reordered row i = e2 written to
+// conventional row n = P[(m - i) mod m] and row 0 =
+// φ(0) Σ_j a_j, with the column's fused mean (the CTA
+// owns the whole column pair: no cross-CTA reduction).
+constexpr int kSmallMaxS = 2048;  // A's two columns, the bucket lists in shared memory
+// the row, the pair's two columns of A, the columns in bucket order, the bucket starts
+inline size_t small_smem(int64_t L2, int64_t s) {
+  return size_t(k1_row_slots(L2, 16)) * 16 + size_t(s) * 20 + size_t(L2 + 1) * 4 + 16;
+}
+
+// epilogue kinds (compile time) of the column passes: LIN writes c + X (c = 0
+// unless AFFINE) and sums it per column; EXP writes X and sums exp(X) per
+// column; ROWSUM writes X and row sums; NONE (one-row kernel) writes X only
+enum { EPK_NONE = -1, EPK_LIN = 0, EPK_EXP = 1, EPK_ROWSUM = 2 };
+
+struct SmallArgs {
+  const double* __restrict__ A;
+  int64_t lda, t;
+  const int32_t* __restrict__ bstart;  // [L2+1]
+  const int4* __restrict__ bent;       // [s] bucket order {j, e_j, e2, ...}
+  int64_t s, m, N;
+  const double2* __restrict__ tw2;
+  const double2* __restrict__ W;
+  const int32_t* __restrict__ P;
+  const double* __restrict__ scal;     // [0] = φ(0)
+  double* __restrict__ X;
+  int64_t ldx;
+  double fparam;
+  double* __restrict__ out;
+};
+
+template <int L2, int EP>
+__global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
+  constexpr int NT = L2 / 16;
+  extern __shared__ double2 smem[];
+  double2* S = smem;
+  double* colA = reinterpret_cast<double*>(smem + k1_row_slots(L2, 16));  // [2][s]
+  int* js = reinterpret_cast<int*>(colA + 2 * a.s);                        // [s] columns, bucket order
+  int* bs = js + a.s;                                                       // [L2 + 1] bucket starts
+  const int p = blockIdx.x, t = threadIdx.x;
+  const int64_t k1 = 2 * int64_t(p), k2 = k1 + 1;
+  const bool has2 = k2 < a.t;
+  const double* a1 = a.A + k1 * a.lda;
+  const double* a2 = a.A + (has2 ? k2 : k1) * a.lda;
+#pragma unroll 8
+  for (int j = t; j < int(a.s); j += NT) {  // independent loads, many in flight
+    colA[j] = __ldg(&a1[j]);
+    colA[a.s + j] = has2 ? __ldg(&a2[j]) : 0.0;
+    js[j] = __ldg(&a.bent[j]).x;
+  }
+#pragma unroll 8
+  for (int i = t; i <= L2; i += NT) bs[i] = __ldg(&a.bstart[i]);
+  __syncthreads();
+  double2 v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {  // bucket e2 = t + NT q, entries in j order
+    const int e2 = t + NT * q;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int i = bs[e2], i1 = bs[e2 + 1]; i < i1; ++i) {
+      const int j = js[i];
+      acc.x += colA[j];
+      acc.y += colA[a.s + j];
+    }
+    v[q] = acc;
+  }
+  const double2 one = make_double2(1.0, 0.0);
+  dif_fwd<L2>(v, S, a.tw2, one);
+  const double2 dc = v[0];  // thread 0: Σ_j a_j (the row-0 sums)
+  {
+    const double2* Wr = a.W + t;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], __ldg(&Wr[q * NT]));
+  }
+  dif_inv<L2>(v, S, a.tw2, one);
+  double2 acc = make_double2(0.0, 0.0);
+  double* xk = a.X ? a.X + k1 : nullptr;
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t i = t + int64_t(NT) * q;  // reordered row (i >= m: zero padding)
+    if (i < a.m) {
+      const int64_t n = __ldg(&a.P[i == 0 ? 0 : a.m - i]);
+      double2 x = v[q];
+      if (EP == EPK_LIN) {
+        x.x += a.fparam;
+        x.y += a.fparam;
+      }
+      if (xk) {
+        xk[n * a.ldx] = x.x;
+        if (has2) xk[n * a.ldx + 1] = x.y;
+      }
+      if (EP == EPK_LIN) {
+        acc.x += x.x;
+        acc.y += x.y;
+      } else if (EP == EPK_EXP) {
+        acc.x += exp(x.x);
+        acc.y += exp(x.y);
+      }
+    }
+  }
+  if (t == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
+    const double phi0 = __ldg(a.scal);
+    double2 x = make_double2(phi0 * dc.x, phi0 * dc.y);
+    if (EP == EPK_LIN) {
+      x.x += a.fparam;
+      x.y += a.fparam;
+    }
+    if (xk) {
+      xk[0] = x.x;
+      if (has2) xk[1] = x.y;
+    }
+    if (EP == EPK_LIN) {
+      acc.x += x.x;
+      acc.y += x.y;
+    } else if (EP == EPK_EXP) {
+      acc.x += exp(x.x);
+      acc.y += exp(x.y);
+    }
+  }
+  if (EP >= 0 && a.out) {  // the column means, a fixed-order reduction over the CTA
+    __syncthreads();
+    double2* red = S;
+    red[t] = acc;
+    __syncthreads();
+    if (t == 0) {
+      double2 sum = red[0];
+      for (int u = 1; u < NT; ++u) sum = cadd(sum, red[u]);
+      a.out[k1] = sum.x / double(a.N);
+      if (has2) a.out[k2] = sum.y / double(a.N);
+    }
+  }
+}
+
 // ---------------------------------------------------------------- K2
 // Column pass, un-permutation and epilogue; X is row-major (X[n·ldx + k]).
 //
@@ -547,7 +683,6 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
 // sums it per column; EXP writes X and sums exp(X) per column; ROWSUM writes
 // X and the row sums over the pair group (warp transpose through shared
 // memory, then a fixed-order sum).
-enum { EPK_LIN = 0, EPK_EXP = 1, EPK_ROWSUM = 2 };
 
 struct EpiArgs {
   double fparam;     // c of AFFINE (0 otherwise)
@@ -1271,15 +1406,20 @@ static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int6
                        double* colsum, cudaStream_t st) {
   const size_t smem = rows_smem<L2>(pl->k1_stage);
   auto kern = k_rows16<L2>;
-  set_smem_attr(kern, smem);
   static int nsm = 0;
+  static size_t last_smem = 0;  // attribute and occupancy of the last shared-memory size (per instantiation)
+  static int last_per_sm = 0;
   if (!nsm) {
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, L2 / QMC_ROW_E, smem);
+  if (smem != last_smem) {
+    set_smem_attr(kern, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&last_per_sm, kern, L2 / QMC_ROW_E, smem);
+    last_smem = smem;
+  }
+  int per_sm = last_per_sm;
   if (pl->k1_per_sm > 0) per_sm = std::min(per_sm, pl->k1_per_sm);
   const int64_t items = pl->sp.L1 * int64_t(np);
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, int64_t(nsm) * std::max(per_sm, 1))));
@@ -1347,15 +1487,15 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       constexpr int CBP = QMC_K2_CB;
       constexpr size_t psm = cols_pipe_smem<L1, CBP>();
       auto pk = k_cols_pipe<L1, EP, CBP>;
-      set_smem_attr(pk, psm);
-      static int nsm = 0;
-      if (!nsm) {
+      static int nsm = 0, per_sm0 = -1;  // per instantiation: constant shared memory
+      if (per_sm0 < 0) {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        set_smem_attr(pk, psm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm0, pk, 16 * CBP, psm);
       }
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, 16 * CBP, psm);
+      int per_sm = per_sm0;
       if (pl->k2_per_sm > 0) per_sm = std::min(per_sm, pl->k2_per_sm);
       const int ntx = int(pl->sp.L2 / CBP), ng = (np + 15) / 16;
       const int64_t ntiles = int64_t(ntx) * ng;
@@ -1372,9 +1512,12 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
     if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !pl->k2_nopipe) {
       constexpr size_t psm = cols_pipe2_smem<L1>();
       auto pk = k_cols_pipe2<R, M, EP>;
-      set_smem_attr(pk, psm);
-      int per_sm = 0;
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pk, kP2Thr, psm);
+      static int per_sm0 = -1;  // per instantiation: constant shared memory
+      if (per_sm0 < 0) {
+        set_smem_attr(pk, psm);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm0, pk, kP2Thr, psm);
+      }
+      int per_sm = per_sm0;
       if (pl->k2_per_sm > 0) per_sm = std::min(per_sm, pl->k2_per_sm);
       const int ntx = int(pl->sp.L2 / kUB), ng = np / kP2PG;
       const int64_t ntiles = int64_t(ntx) * ng;
@@ -1446,6 +1589,38 @@ static int dense_cols_dispatch(const qmc_plan* pl, const double2* ad, int np, do
   }
   QMC_K2_SPLITS(QMC_DENSE2_CASE)
 #undef QMC_DENSE2_CASE
+  return QMC_EINVAL_N;
+}
+
+template <int L2, int EP>
+static int launch_small(const SmallArgs& sa, int64_t npairs, cudaStream_t st) {
+  const size_t smem = small_smem(L2, sa.s);
+  auto kern = k_small<L2, EP>;
+  static bool attr = false;  // per instantiation: the largest smem this process may request
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem(L2, kSmallMaxS)));
+    attr = true;
+  }
+  kern<<<unsigned(npairs), L2 / 16, smem, st>>>(sa);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
+template <int L2>
+static int launch_small_f(const SmallArgs& sa, int f, int64_t npairs, cudaStream_t st) {
+  if (f < 0) return launch_small<L2, EPK_NONE>(sa, npairs, st);
+  if (f == QMC_F_EXP) return launch_small<L2, EPK_EXP>(sa, npairs, st);
+  return launch_small<L2, EPK_LIN>(sa, npairs, st);
+}
+
+static int small_dispatch(const qmc_plan* pl, const SmallArgs& sa, int f, int64_t npairs, cudaStream_t st) {
+  switch (pl->sp.L2) {
+#define QMC_SMALL_CASE(NN) \
+  case NN: return launch_small_f<NN>(sa, f, npairs, st);
+    QMC_SMALL_CASE(16) QMC_SMALL_CASE(32) QMC_SMALL_CASE(64) QMC_SMALL_CASE(128) QMC_SMALL_CASE(256)
+    QMC_SMALL_CASE(512) QMC_SMALL_CASE(1024) QMC_SMALL_CASE(2048) QMC_SMALL_CASE(4096) QMC_SMALL_CASE(8192)
+#undef QMC_SMALL_CASE
+  }
   return QMC_EINVAL_N;
 }
 
@@ -1532,6 +1707,34 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   }
   if (!A || !call_ws) return QMC_ENULL;
   if (f < 0 && !X) return QMC_ENULL;
+  if (pl->sp.L1 == 1 && pl->s <= kSmallMaxS && f != QMC_F_ROWMEAN_RELU) {
+    // one-row plan: one fused launch per call
+    if (A_host && cudaMemcpy2DAsync(const_cast<double*>(A), size_t(lda) * 8, A_host, size_t(lda_host) * 8,
+                                    size_t(pl->s) * 8, size_t(t), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return QMC_ECUDA;
+    SmallArgs sa;
+    sa.A = A;
+    sa.lda = lda;
+    sa.t = t;
+    sa.bstart = pl->d_bstart;
+    sa.bent = pl->d_bent;
+    sa.s = pl->s;
+    sa.m = pl->m;
+    sa.N = pl->N;
+    sa.tw2 = pl->d_tw2;
+    sa.W = pl->d_W;
+    sa.P = pl->d_P;
+    sa.scal = pl->d_scal;
+    sa.X = X;
+    sa.ldx = ldx;
+    sa.fparam = f == QMC_F_AFFINE ? fparam : 0.0;
+    sa.out = f >= 0 ? out : nullptr;
+    prof_begin(KC_ROWS, st);
+    const int rc = small_dispatch(pl, sa, f, (t + 1) / 2, st);
+    if (rc) return rc;
+    prof_end(KC_ROWS, st);
+    return QMC_OK;
+  }
   const CallLayout cl = call_layout(pl, t, f);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
