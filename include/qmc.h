@@ -92,7 +92,8 @@ enum {
   QMC_ENULL = -6,         /* required pointer is NULL                         */
   QMC_ECUDA = -7,         /* CUDA launch / runtime error                      */
   QMC_EWORKSPACE = -8,    /* workspace too small or misaligned (256 B)        */
-  QMC_EINVAL_F = -9       /* unknown f                                        */
+  QMC_EINVAL_F = -9,      /* unknown f                                        */
+  QMC_EUNSUPPORTED = -10  /* valid request this entry point does not cover    */
 };
 
 /* Bytes of device memory the plan needs (plan_ws).  family/N_or_D/s as in
@@ -154,6 +155,21 @@ int qmc_mean(qmc_plan_t plan, const double* A, int64_t lda, int64_t t, int f, do
  * (reduced → out, may alias).  Device pointers. */
 int qmc_mean_finalize(qmc_plan_t plan, int f, const double* reduced, int64_t t_total, double* out,
                       void* stream);
+
+/* The union of all Korobov lattice point sets (SURVEY
+ * §8(f) NEXT #1): N_pset = (K-1)^2 points x_{n,g} = ({n g^j / K})_{j<s},
+ * n, g = 1..K-1, K prime, in the conventional order row = (g-1)(K-1) + (n-1)
+ * (reading R24).  X = Y_pset · A for a lattice plan with N = K and the p-set's
+ * dimension s (its generating vector is not used): every block g is Z·P_g
+ * with the plan's one circulant Z (Eq. Y_pset), so the
+ * plan's spectrum, power and log tables serve all K-1 blocks, and the block
+ * index is a grid dimension of one launch (column map e_{g,j} = j·L[g] mod
+ * (K-1), computed on the device).  A: device, column-major s×t (lda >= s);
+ * X: device, row-major (K-1)^2 × t (ldx >= t).  One-row plans only
+ * (L1 = 1, i.e. K <= 4097, and s <= 2048): QMC_EUNSUPPORTED otherwise (the
+ * caller then runs one lattice plan per block).  Asynchronous on `stream`. */
+int qmc_pset_matmul(qmc_plan_t plan, const double* A, int64_t lda, int64_t t, double* X, int64_t ldx,
+                    void* stream);
 
 /* End-to-end entry with HOST buffers: copies A_host (pinned or pageable,
  * column-major s×t, lda) into A_dev (device, s*t doubles, ld = s) — batch by

@@ -26,8 +26,9 @@ EXPORTS = [
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
-    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step",
+    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step", "qmc_pset_matmul",
 ]
+QMC_EUNSUPPORTED = -10
 
 
 class QMCError(RuntimeError):
@@ -56,6 +57,7 @@ _sig = {
     "qmc_plan_create_poly": (_i32, [C.POINTER(_vp), _i32, C.c_uint64, _i64, _P64, _i32, _vp, _sz, _vp]),
     "qmc_plan_create_shifted": (_i32, [C.POINTER(_vp), _i64, _i64, _P64, _i32, _d, _vp, _sz, _vp]),
     "qmc_matmul": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp]),
+    "qmc_pset_matmul": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "qmc_mean": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _i64, _vp, _sz, _vp]),
     "qmc_mean_finalize": (_i32, [_vp, _i32, _vp, _i64, _vp, _vp]),
     "qmc_mean_host": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _vp, _i64, _vp, _vp, _sz, _vp]),
@@ -149,6 +151,14 @@ def qmc_plan_create_poly(D: int, p: int, s: int, q, phi: int, plan_ws, plan_ws_b
 def qmc_matmul(plan, A, lda: int, t: int, X, ldx: int, call_ws, call_ws_bytes: int, stream=None):
     _check(_lib.qmc_matmul(plan, ptr(A), lda, t, ptr(X), ldx, ptr(call_ws), call_ws_bytes, stream),
            "qmc_matmul")
+
+
+def qmc_pset_matmul(plan, A, lda: int, t: int, X, ldx: int, stream=None) -> int:
+    """Returns the status (QMC_OK or QMC_EUNSUPPORTED); raises on other errors."""
+    rc = _lib.qmc_pset_matmul(plan, ptr(A), lda, t, ptr(X), ldx, stream)
+    if rc != QMC_EUNSUPPORTED:
+        _check(rc, "qmc_pset_matmul")
+    return rc
 
 
 def qmc_mean(plan, A, lda: int, t: int, f: int, f_param: float, out, X_or_null, ldx: int,

@@ -152,16 +152,17 @@ class Plan:
 class KorobovPSet:
     """The union of all Korobov lattice point sets (SURVEY
     §8(f) NEXT #1): N = (K-1)^2 points x_{n,g} = ({n g^j / K})_{j<s}, n, g =
-    1..K-1, K prime, in the conventional order row = (g-1)(K-1) + (n-1).
+    1..K-1, K prime, in the conventional order row = (g-1)(K-1) + (n-1)
+    (reading R24).
 
     Block g is the Korobov rank-1 lattice z = (1, g, g^2, ...) mod K without
     its row n = 0; in the paper's reordering every block is Z·P_g with the
-    same circulant Z, only the column map changes.  Here each block runs the
-    library's lattice fast path (one plan per block: the same kernels, the
-    spectrum rebuilt per block) and writes its K rows straight into X; blocks
-    run in decreasing g so that a block's row 0 lands on the row the next
-    (lower) block overwrites with its last row — X is a view of an (N+1)-row
-    buffer.  A batched block dimension inside K1/K2 is the next step."""
+    same circulant Z.  So one lattice plan (N = K: one spectrum, one P/L) and
+    one launch serve all blocks (qmc_pset_matmul: the block index is a grid
+    dimension, the column map e_{g,j} = j·L[g] mod (K-1) is computed on the
+    device).  Plans the batched kernel does not cover (K > 4097, i.e. rows
+    longer than one row FFT, or s > 2048) run one lattice plan per block, each
+    writing its K rows straight into X."""
 
     def __init__(self, K: int, s: int, phi: int, device=None):
         if not torch.cuda.is_available():
@@ -169,26 +170,43 @@ class KorobovPSet:
         self.K, self.s, self.phi = int(K), int(s), int(phi)
         self.N = (self.K - 1) ** 2
         self.device = torch.device(device if device is not None else "cuda")
-        self.plans = []
-        for g in range(1, self.K):
-            z = np.array([pow(g, j, self.K) for j in range(self.s)], dtype=np.int64)
-            self.plans.append(Plan.lattice(self.K, z, self.phi, device=self.device))
+        # the shared plan (its generating vector is not used by qmc_pset_matmul)
+        self.plan = Plan.lattice(self.K, np.ones(self.s, dtype=np.int64), self.phi, device=self.device)
+        self.plans = None  # per-block plans, built on first use when the batched kernel does not apply
         self._ws = None
 
-    def matmul(self, A: torch.Tensor) -> torch.Tensor:
-        """X = Y·A for the p-set; A (s, t) column-major; returns X (N, t) row-major."""
+    def _block_plans(self):
+        if self.plans is None:
+            self.plans = []
+            for g in range(1, self.K):
+                z = np.array([pow(g, j, self.K) for j in range(self.s)], dtype=np.int64)
+                self.plans.append(Plan.lattice(self.K, z, self.phi, device=self.device))
+        return self.plans
+
+    def matmul(self, A: torch.Tensor, per_block: bool = False) -> torch.Tensor:
+        """X = Y·A for the p-set; A (s, t) column-major; returns X (N, t) row-major.
+        per_block=True forces the one-plan-per-block path (comparison)."""
         lda = _ld(A, self.s)
         t = A.shape[1]
+        st = _stream(self.device)
+        if not per_block:
+            X = torch.empty((self.N, t), dtype=torch.float64, device=self.device)
+            with torch.cuda.device(self.device):
+                rc = abi.qmc_pset_matmul(self.plan.handle, A, lda, t, X, max(t, 1), st)
+            if rc == 0:
+                return X
+        plans = self._block_plans()
         buf = torch.empty((self.N + 1, t), dtype=torch.float64, device=self.device)
         ldx = max(t, 1)
-        nbytes = max(abi.qmc_call_workspace_size(p.handle, t, abi.QMC_F_NONE) for p in self.plans)
+        nbytes = max(abi.qmc_call_workspace_size(p.handle, t, abi.QMC_F_NONE) for p in plans)
         if self._ws is None or self._ws.numel() < nbytes:
             self._ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=self.device)
-        st = _stream(self.device)
         with torch.cuda.device(self.device):
+            # decreasing g: each block's row 0 lands on the row the next (lower)
+            # block overwrites with its last row; X is a view of N+1 rows
             for g in range(self.K - 1, 0, -1):
                 Xg = buf[(g - 1) * (self.K - 1):]          # rows n = 0..K-1 of block g
-                abi.qmc_matmul(self.plans[g - 1].handle, A, lda, t, Xg, ldx, self._ws, self._ws.numel(), st)
+                abi.qmc_matmul(plans[g - 1].handle, A, lda, t, Xg, ldx, self._ws, self._ws.numel(), st)
         return buf[1:]
 
 

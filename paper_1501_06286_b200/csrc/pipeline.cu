@@ -664,6 +664,111 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
   }
 }
 
+// ---------------------------------------------------------------- Korobov p-set
+// The union of all Korobov lattices: block g = 1..K-1 is
+// the rank-1 lattice with z_j = g^j mod K (j = 0..s-1) without its row 0.
+// In the reordered indexing every block is Z·P_g with the SAME circulant Z
+// (one plan: one ζ, one spectrum W, one P/L), only the column map changes:
+// e_{g,j} = L[g^j] = j·ℓ_g mod m, ℓ_g = L[g] (the paper's c_{g,j} - 1 =
+// (j-1)(g-1) mod (K-1) with 1-based j and g = β^{g-1}).  One CTA per (pair,
+// block); bucket e receives the j with j·ℓ ≡ e (mod m): with d = gcd(ℓ, m)
+// and u = (ℓ/d)^{-1} mod m/d these are j ≡ (e/d)·u (mod m/d), summed in
+// increasing j (deterministic).  Conventional row n of block g is p-set row
+// (g-1)(K-1) + n-1 (reading R24).  One-row plans only (L1 = 1).
+__device__ __forceinline__ int64_t gcd64(int64_t a, int64_t b) {
+  while (b) {
+    const int64_t r = a % b;
+    a = b;
+    b = r;
+  }
+  return a;
+}
+// x^{-1} mod mm for gcd(x, mm) = 1, mm >= 1 (extended Euclid)
+__device__ __forceinline__ int64_t modinv64(int64_t x, int64_t mm) {
+  if (mm == 1) return 0;
+  int64_t r0 = mm, r1 = x % mm, s0 = 0, s1 = 1;
+  while (r1) {
+    const int64_t qq = r0 / r1;
+    int64_t tmp = r0 - qq * r1;
+    r0 = r1;
+    r1 = tmp;
+    tmp = s0 - qq * s1;
+    s0 = s1;
+    s1 = tmp;
+  }
+  return ((s0 % mm) + mm) % mm;
+}
+
+template <int L2>
+__global__ void __launch_bounds__(L2 / 16) k_pset(SmallArgs a, const int32_t* __restrict__ Ltab) {
+  constexpr int NT = L2 / 16;
+  extern __shared__ double2 smem[];
+  double2* S = smem;
+  double* colA = reinterpret_cast<double*>(smem + k1_row_slots(L2, 16));  // [2][s]
+  const int p = blockIdx.x, g = blockIdx.y + 1, t = threadIdx.x;
+  const int64_t m = a.m;
+  const int64_t k1 = 2 * int64_t(p), k2 = k1 + 1;
+  const bool has2 = k2 < a.t;
+  const double* a1 = a.A + k1 * a.lda;
+  const double* a2 = a.A + (has2 ? k2 : k1) * a.lda;
+#pragma unroll 8
+  for (int j = t; j < int(a.s); j += NT) {
+    colA[j] = __ldg(&a1[j]);
+    colA[a.s + j] = has2 ? __ldg(&a2[j]) : 0.0;
+  }
+  const int64_t ell = __ldg(&Ltab[g]);      // ℓ_g = L[g]
+  const int64_t d = ell ? gcd64(ell, m) : m;
+  const int64_t mm = m / d;
+  const int64_t u = modinv64(ell / d, mm);
+  __syncthreads();
+  double2 v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t e2 = t + int64_t(NT) * q;
+    double2 acc = make_double2(0.0, 0.0);
+    if (e2 < m && e2 % d == 0) {
+      for (int64_t j = ((e2 / d) * u) % mm; j < a.s; j += mm) {
+        acc.x += colA[j];
+        acc.y += colA[a.s + j];
+      }
+    }
+    v[q] = acc;
+  }
+  const double2 one = make_double2(1.0, 0.0);
+  dif_fwd<L2>(v, S, a.tw2, one);
+  {
+    const double2* Wr = a.W + t;
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], __ldg(&Wr[q * NT]));
+  }
+  dif_inv<L2>(v, S, a.tw2, one);
+  double* xk = a.X + k1 + int64_t(g - 1) * m * a.ldx;  // block g: rows (g-1)(K-1) + n-1
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    const int64_t i = t + int64_t(NT) * q;
+    if (i < m) {
+      const int64_t n = __ldg(&a.P[i == 0 ? 0 : m - i]);  // conventional row n in 1..K-1
+      xk[(n - 1) * a.ldx] = v[q].x;
+      if (has2) xk[(n - 1) * a.ldx + 1] = v[q].y;
+    }
+  }
+}
+
+template <int L2>
+static int launch_pset(const qmc_plan* pl, const SmallArgs& sa, int64_t npairs, cudaStream_t st) {
+  const size_t smem = size_t(k1_row_slots(L2, 16)) * 16 + size_t(2 * sa.s) * 8;
+  auto kern = k_pset<L2>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         int(size_t(k1_row_slots(L2, 16)) * 16 + size_t(2 * kSmallMaxS) * 8));
+    attr = true;
+  }
+  kern<<<dim3(unsigned(npairs), unsigned(pl->m)), L2 / 16, smem, st>>>(sa, pl->d_L);
+  QMC_LAUNCHED();
+  return QMC_OK;
+}
+
 // ---------------------------------------------------------------- K2
 // Column pass, un-permutation and epilogue; X is row-major (X[n·ldx + k]).
 //
@@ -1785,6 +1890,17 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   }
   return QMC_OK;
 }
+static int pset_dispatch(const qmc_plan* pl, const SmallArgs& sa, int64_t npairs, cudaStream_t st) {
+  switch (pl->sp.L2) {
+#define QMC_PSET_CASE(NN) \
+  case NN: return launch_pset<NN>(pl, sa, npairs, st);
+    QMC_PSET_CASE(16) QMC_PSET_CASE(32) QMC_PSET_CASE(64) QMC_PSET_CASE(128) QMC_PSET_CASE(256)
+    QMC_PSET_CASE(512) QMC_PSET_CASE(1024) QMC_PSET_CASE(2048) QMC_PSET_CASE(4096) QMC_PSET_CASE(8192)
+#undef QMC_PSET_CASE
+  }
+  return QMC_EINVAL_N;
+}
+
 }  // namespace qmc
 
 using namespace qmc;
@@ -1809,6 +1925,39 @@ int qmc_mean(qmc_plan_t pl, const double* A, int64_t lda, int64_t t, int f, doub
              void* stream) {
   if (f < QMC_F_IDENTITY || f > QMC_F_ROWMEAN_RELU) return QMC_EINVAL_F;
   return run(pl, A, lda, t, f, f_param, out, X_or_null, ldx, call_ws, call_ws_bytes, (cudaStream_t)stream);
+}
+
+int qmc_pset_matmul(qmc_plan_t pl, const double* A, int64_t lda, int64_t t, double* X, int64_t ldx,
+                    void* stream) {
+  if (!pl) return QMC_ENULL;
+  if (pl->family != QMC_FAMILY_LATTICE || pl->delta != 0.0) return QMC_EINVAL_N;
+  if (pl->sp.L1 != 1 || pl->s > kSmallMaxS) return QMC_EUNSUPPORTED;
+  if (t < 0 || lda < pl->s || ldx < t) return QMC_EINVAL_DIM;
+  if (t == 0) return QMC_OK;
+  if (!A || !X) return QMC_ENULL;
+  SmallArgs sa;
+  sa.A = A;
+  sa.lda = lda;
+  sa.t = t;
+  sa.bstart = nullptr;
+  sa.bent = nullptr;
+  sa.s = pl->s;
+  sa.m = pl->m;
+  sa.N = pl->N;
+  sa.tw2 = pl->d_tw2;
+  sa.W = pl->d_W;
+  sa.P = pl->d_P;
+  sa.scal = pl->d_scal;
+  sa.X = X;
+  sa.ldx = ldx;
+  sa.fparam = 0.0;
+  sa.out = nullptr;
+  cudaStream_t st = (cudaStream_t)stream;
+  prof_begin(KC_ROWS, st);
+  const int rc = pset_dispatch(pl, sa, (t + 1) / 2, st);
+  if (rc) return rc;
+  prof_end(KC_ROWS, st);
+  return QMC_OK;
 }
 
 int qmc_mean_finalize(qmc_plan_t pl, int f, const double* reduced, int64_t t_total, double* out,

@@ -968,6 +968,7 @@ const char* qmc_strerror(int code) {
     case QMC_ENULL: return "required pointer is NULL";
     case QMC_ECUDA: return "CUDA error";
     case QMC_EWORKSPACE: return "workspace too small or not 256-byte aligned";
+    case QMC_EUNSUPPORTED: return "request not covered by this entry point";
     case QMC_EINVAL_F: return "unknown f";
   }
   return "unknown status";

@@ -348,6 +348,29 @@ def test_korobov_pset(qmc, K, s, t, phi):
     err = np.abs(X.cpu().numpy() - Xo).max(axis=0)
     assert X.shape == ((K - 1) ** 2, t)
     assert np.all(err <= tol), (err / tol).max()
+    # the one-plan batched launch (qmc_pset_matmul) against one plan per block
+    Xb = ps.matmul(qmc.to_device_colmajor(A, "cuda"), per_block=True)
+    torch.cuda.synchronize()
+    assert np.all(np.abs(Xb.cpu().numpy() - Xo).max(axis=0) <= tol)
+
+
+@pytest.mark.parametrize("K,s,t", [(1021, 32, 8), (4001, 16, 4)])
+def test_korobov_pset_large(qmc, K, s, t):
+    """K = 1021 (N = 1,040,400 points; padded row of 2048, one launch for all
+    1020 blocks) and K = 4001 (rows split L1 = 2: one plan per block), on
+    sampled rows against the oracle's plain definition."""
+    import torch
+    rng = np.random.default_rng(K + s)
+    A = rng.standard_normal((s, t))
+    ps = qmc.KorobovPSet(K, s, W.PHI_SHIFT_HALF)
+    X = ps.matmul(qmc.to_device_colmajor(A, "cuda"))
+    torch.cuda.synchronize()
+    rows = np.unique(np.concatenate([sample_rows((K - 1) ** 2, 400, seed=K), [0, K - 2, K - 1, (K - 1) ** 2 - 1]]))
+    tab = O.phi_table(W.PHI_SHIFT_HALF, K)
+    Xo = O.point_matrix_rows(tab, O.pset_index_matrix(K, s, rows)) @ A
+    Xs = X.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy()
+    tol = 1e-11 * np.abs(A).sum(axis=0) * np.abs(tab).max()
+    assert np.all(np.abs(Xs - Xo).max(axis=0) <= tol)
 
 
 # ------------------------------------------------------------------ Experiment 2 (NEXT #2)
