@@ -191,8 +191,9 @@ int qmc_mean_host(qmc_plan_t plan, const double* A_host, int64_t lda, int64_t t,
  * by qmc_matmul: K diagonal entries then the K-1 entries (k, k+1) (B is
  * symmetric).  d0, e0: the diagonal and off-diagonal entries of A_0.
  * Solves B(y_n) û^(n) = ĝ for every n IN PLACE (X row n: û^(n) in its first
- * K slots afterwards; the other slots are scratch) by the Thomas algorithm,
- * one thread per sample, and writes mean_out[k] = (1/N) Σ_n û_k^(n)
+ * K slots afterwards; the other slots are scratch) by the Thomas algorithm
+ * (one warp per 32 samples, lane = sample, 32-unknown tiles of the rows
+ * staged through shared memory), and writes mean_out[k] = (1/N) Σ_n û_k^(n)
  * (PAPER.md:665-668), summed in increasing n.  rhs: device ĝ (K doubles) or
  * NULL for ĝ = (1, ..., 1).  B must be positive definite
  * (true for this ODE: a >= 2 - ζ(3/2)/2 > 0).  Asynchronous on `stream`. */
@@ -243,6 +244,11 @@ int qmc_plan_tables(qmc_plan_t plan, int64_t* gen, int32_t* P, int32_t* L, int32
 
 /* Kernels this library has launched since it was loaded (all entry points). */
 int64_t qmc_launch_count(void);
+
+/* Build flags of this library: bit 0 = the checked build (-DQMC_CHECK:
+ * device-side bounds checks of the computed indices, tools/check_build.sh),
+ * bit 1 = phase timing (-DQMC_PHASE_TIMING).  0 for the product build. */
+int qmc_build_flags(void);
 
 /* Per-kernel-class timing for roofline reporting.  qmc_profile_enable(1)
  * makes every later hot-path call record CUDA events on its stream around

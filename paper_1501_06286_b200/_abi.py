@@ -26,7 +26,7 @@ EXPORTS = [
     "qmc_plan_create_poly", "qmc_matmul", "qmc_mean", "qmc_mean_finalize", "qmc_mean_host",
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
-    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step", "qmc_pset_matmul",
+    "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step", "qmc_pset_matmul", "qmc_build_flags",
 ]
 QMC_EUNSUPPORTED = -10
 
@@ -67,6 +67,7 @@ _sig = {
     "qmc_cbc_step": (_i32, [_i64, _vp, _i64, _d, _vp, _vp, _i64, _vp]),
     "qmc_plan_tables": (_i32, [_vp, _P64, _P32, _P32, _P32, _PD]),
     "qmc_launch_count": (_i64, []),
+    "qmc_build_flags": (_i32, []),
     "qmc_plan_destroy": (None, [_vp]),
     "qmc_strerror": (C.c_char_p, [_i32]),
     "qmc_profile_enable": (_i32, [_i32]),
@@ -77,6 +78,10 @@ for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
     _f.restype = _res
     _f.argtypes = _args
+
+
+def qmc_build_flags() -> int:
+    return int(_lib.qmc_build_flags())
 
 
 def strerror(code: int) -> str:

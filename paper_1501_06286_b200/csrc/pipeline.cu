@@ -4,24 +4,32 @@
 //
 // Per column pair (k1, k2) packed as a = A[:,k1] + i·A[:,k2] (ζ is real, so
 // one complex correlation serves two real columns), with the plan's split
-// L = L1·L2 (e = L2·e1 + e2, f = f1 + L1·f2):
+// L = L1·L2 (e = L2·e1 + e2, f = f1 + L1·f2, NT = L2/16 row threads, e2 =
+// t + NT q):
 //
-//   K1 k_rows16    T[f1,e2] = Σ_{j: e_j ≡ e2} a_j ω_L^{e_j f1}   (scatter a' = P a
-//                  fused with the first FFT dimension)
-//                  → FFT_L2 → ·W → IFFT_L2 → U[p][f1][e2]           (registers)
-//   K2 k_cols_x    ·conj(ω_L^{e2 f1}), IFFT_L1 over f1 → B'[L2 e1 + e2]; the
-//                  reordered row i = L2 e1 + e2 is conventional row
-//                  n = β^{-i} = P[(m - i) mod m], so K2
-//                  writes the row chunk X[n, 2p..2p+1 of the pair group]
-//                  directly (X row-major); X[0,k] = φ(0) Σ_j A[j,k]
-//                  (PAPER.md:305-311); fused f, per-column partial sums or
-//                  per-row partial sums
+//   K0 k_pack*     a of the batch in the K1 slot order (or the dense a', then
+//                  the first DFT dimension by k_dense_cols*)
+//   K1 k_rows16    T'[f1,e2] = Σ_{j: e_j ≡ e2} a_j ω_L^{e'_j f1}   (scatter a' = P a
+//                  fused with the first FFT dimension, PAPER.md:355-357;
+//                  e' = e - e mod NT, the thread part ω_L^{t f1} of the
+//                  four-step twiddle folded into the row FFT's first stage)
+//                  → FFT_L2 → ·W → IFFT_L2 → ·conj(ω_L^{e2 f1}) → U[p][f1][e2]
+//                  (fft.cuh dif_fwd / dif_inv, registers + shared memory)
+//   K2 k_cols_*    IFFT_L1 over f1 → B'[L2 e1 + e2]; the reordered row
+//                  i = L2 e1 + e2 is conventional row n = β^{-i} =
+//                  P[(m - i) mod m], so K2 writes the row
+//                  chunk X[n, 2p..2p+1 of the pair group] directly (X
+//                  row-major); X[0,k] = φ(0) Σ_j A[j,k];
+//                  fused f, per-column or per-row partial sums
 //   K3 k_colpart_reduce / k_rowsum_reduce   fixed-order reductions
+//   one-row plans (L1 = 1): k_small, the whole call in one kernel;
+//   Korobov p-sets: k_pset, all blocks of one plan in one launch
 //
 // B'[i] = Σ_j a_j ζ[(e_j - i) mod m] = (Z P a)_i is a cyclic correlation,
 // computed as IDFT(DFT(a') · DFT(K)), K[d] = ζ[(-d) mod m] (zero-padded to
 // L >= 2m-1 when m does not split into supported radices).  U of a batch of
-// column pairs is sized (plan->batch_pairs) to stay in L2.
+// column pairs (plan->batch_pairs) round-trips through DRAM between K1 and
+// K2; the batch is sized for launch efficiency.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -381,12 +389,15 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       const int cd = sg.stE[i];
       const double2 pr = cmul(sg.stA[i], sg.stW[i]);
       acc = (cd & kK1First) ? pr : cadd(acc, pr);
+      QMC_CHECK_IDX(i, a.CH);
+      QMC_CHECK_IDX(padE<E>(cd & 0x3fff), k1_row_slots(L2, E));
       S[padE<E>(cd & 0x3fff)] = acc;
     }
     if (n > nreg) {  // fix-up: later pieces of split buckets, in order
       __syncthreads();
       for (int r = nreg + tid; r < n; r += NT) {
         const int rc = sg.stE[r];
+        QMC_CHECK_IDX(padE<E>(L2 + 1 + ((rc >> 14) & 63) + (rc >> 20)), k1_row_slots(L2, E) + 1);
         const int e2 = rc & 0x3fff, o0 = (rc >> 14) & 63, cnt = rc >> 20;
         double2 t = S[padE<E>(e2)];
         for (int k = 0; k < cnt; ++k) t = cadd(t, S[padE<E>(L2 + 1 + o0 + k)]);
@@ -416,12 +427,15 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
         const int cd = __ldg(&a.e2q[i]);
         const double2 pr = cmul(__ldg(&ap[i]), __ldg(&tp[i]));
         acc = (cd & kK1First) ? pr : cadd(acc, pr);
+        QMC_CHECK_IDX(i, a.S1);
+        QMC_CHECK_IDX(padE<E>(cd & 0x3fff), k1_row_slots(L2, E));
         S[padE<E>(cd & 0x3fff)] = acc;
       }
       if (n > nreg) {  // fix-up: later pieces of split buckets, in order
         __syncthreads();
         for (int r = q0 + nreg + tid; r < q0 + n; r += NT) {
           const int rc = __ldg(&a.e2q[r]);
+          QMC_CHECK_IDX(padE<E>(L2 + 1 + ((rc >> 14) & 63) + (rc >> 20)), k1_row_slots(L2, E) + 1);
           const int e2 = rc & 0x3fff, o0 = (rc >> 14) & 63, cnt = rc >> 20;
           double2 t = S[padE<E>(e2)];
           for (int k = 0; k < cnt; ++k) t = cadd(t, S[padE<E>(L2 + 1 + o0 + k)]);
@@ -504,9 +518,11 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
   // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
   // whole sectors of kUB·16 bytes per f1
   double2* Up = a.U + int64_t(p) * a.L + int64_t(f1) * kUB;
+  QMC_CHECK_IDX(p, a.np);
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const int e2 = tid + q * NT;
+    QMC_CHECK_IDX(int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB) + int64_t(f1) * kUB, a.L);
     Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
   }
   QMC_TS(5);
@@ -592,6 +608,7 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
     double2 acc = make_double2(0.0, 0.0);
     for (int i = bs[e2], i1 = bs[e2 + 1]; i < i1; ++i) {
       const int j = js[i];
+      QMC_CHECK_IDX(j, a.s);
       acc.x += colA[j];
       acc.y += colA[a.s + j];
     }
@@ -613,6 +630,7 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
     const int64_t i = t + int64_t(NT) * q;  // reordered row (i >= m: zero padding)
     if (i < a.m) {
       const int64_t n = __ldg(&a.P[i == 0 ? 0 : a.m - i]);
+      QMC_CHECK_IDX(n, a.N);
       double2 x = v[q];
       if (EP == EPK_LIN) {
         x.x += a.fparam;
@@ -748,6 +766,7 @@ __global__ void __launch_bounds__(L2 / 16) k_pset(SmallArgs a, const int32_t* __
     const int64_t i = t + int64_t(NT) * q;
     if (i < m) {
       const int64_t n = __ldg(&a.P[i == 0 ? 0 : m - i]);  // conventional row n in 1..K-1
+      QMC_CHECK_IDX(n - 1, m);
       xk[(n - 1) * a.ldx] = v[q].x;
       if (has2) xk[(n - 1) * a.ldx + 1] = v[q].y;
     }
@@ -809,6 +828,7 @@ __device__ __forceinline__ void emit(const EpiArgs& E, double2 v, int64_t n, boo
   }
   if (!has2) v.y = 0.0;
   if (ok && xk) {
+    QMC_CHECK_IDX(n, E.N);
     double* xp = xk + n * E.ldx;
     if (E.xvec && has2) {
       QMC_XST2(xp, v);
@@ -841,6 +861,7 @@ __device__ __forceinline__ void emit_fast(const EpiArgs& E, double2 v, int n, do
     v.x += E.fparam;
     v.y += E.fparam;
   }
+  QMC_CHECK_IDX(n, E.N);
   if (xk) QMC_XST2(xk + int64_t(n) * E.ldx, v);
   if (EP == EPK_LIN) {
     acc.x += v.x;

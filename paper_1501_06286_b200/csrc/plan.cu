@@ -912,6 +912,17 @@ int qmc_plan_tables(qmc_plan_t pl, int64_t* gen, int32_t* P, int32_t* L, int32_t
 
 int64_t qmc_launch_count(void) { return g_launches.load(); }
 
+int qmc_build_flags(void) {
+  int f = 0;
+#ifdef QMC_CHECK
+  f |= 1;
+#endif
+#ifdef QMC_PHASE_TIMING
+  f |= 2;
+#endif
+  return f;
+}
+
 int qmc_profile_enable(int on) {
   g_prof.on = on != 0;
   return QMC_OK;

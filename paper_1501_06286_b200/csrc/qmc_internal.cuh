@@ -16,6 +16,28 @@ constexpr size_t kAlign = 256;
 
 inline size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
+// Bounds checks of the checked build (-DQMC_CHECK, tools/check_build.sh):
+// every shared-memory row slot, staged slot, U and X index the kernels
+// compute is tested against its buffer; a violation prints and traps.
+// compute-sanitizer is closed on this GPU pool, so this build (run on the
+// GPU parity suite) and the guard-zone tests (tests/test_guards_gpu.py)
+// stand in for memcheck.  Compiles to nothing otherwise.
+#ifdef QMC_CHECK
+#include <stdio.h>
+#define QMC_CHECK_IDX(i, n)                                                                          \
+  do {                                                                                               \
+    const long long _i = (long long)(i), _n = (long long)(n);                                        \
+    if (_i < 0 || _i >= _n) {                                                                        \
+      printf("QMC_CHECK %s:%d: index %lld outside [0, %lld)\n", __FILE__, __LINE__, _i, _n);         \
+      __trap();                                                                                      \
+    }                                                                                                \
+  } while (0)
+#else
+#define QMC_CHECK_IDX(i, n) \
+  do {                      \
+  } while (0)
+#endif
+
 // number of kernels launched by the library (qmc_launch_count)
 extern std::atomic<int64_t> g_launches;
 
