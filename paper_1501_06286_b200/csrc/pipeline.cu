@@ -273,6 +273,14 @@ __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// slots of the direct scatter in flight per thread (loop unroll)
+#ifndef QMC_K1_UNROLL
+#define QMC_K1_UNROLL 4
+#endif
+#define QMC_PRAGMA_(x) _Pragma(#x)
+#define QMC_UNROLL_(n) QMC_PRAGMA_(unroll n)
+#define QMC_UNROLL(n) QMC_UNROLL_(n)
+
 // shared memory of K1: the padded row with its padding and overflow slots
 // (k1_row_slots); staged plans add the staging of CH slots (a, twiddle, code:
 // 36 B each, CH a multiple of 4) and its mbarrier
@@ -422,7 +430,7 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       // stored after every entry (the last store of a piece is its total)
       const int nreg = __ldg(&a.k1c[nch + 1 + c]);
       double2 acc = make_double2(0.0, 0.0);
-#pragma unroll 4
+      QMC_UNROLL(QMC_K1_UNROLL)
       for (int i = q0 + tid; i < q0 + nreg; i += NT) {
         const int cd = __ldg(&a.e2q[i]);
         const double2 pr = cmul(__ldg(&ap[i]), __ldg(&tp[i]));
