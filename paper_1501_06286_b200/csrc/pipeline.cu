@@ -1556,7 +1556,9 @@ static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int6
   int per_sm = last_per_sm;
   if (pl->k1_per_sm > 0) per_sm = std::min(per_sm, pl->k1_per_sm);
   const int64_t items = pl->sp.L1 * int64_t(np);
-  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, int64_t(nsm) * std::max(per_sm, 1))));
+  int64_t cap = int64_t(nsm) * std::max(per_sm, 1);
+  if (pl->k1_grid_cap > 0) cap = std::min<int64_t>(cap, pl->k1_grid_cap);
+  const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, cap)));
   kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(k1_args(pl, asort, t, pair0, U, np, colsum));
   QMC_LAUNCHED();
   return QMC_OK;

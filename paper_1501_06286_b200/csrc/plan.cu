@@ -638,6 +638,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     pl->batch_pairs = bp;
     if (const char* ev = getenv("QMC_K1_PER_SM")) pl->k1_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_K2_PER_SM")) pl->k2_per_sm = int(strtol(ev, nullptr, 10));  // tuning
+    if (const char* ev = getenv("QMC_K1_GRID")) pl->k1_grid_cap = int(strtol(ev, nullptr, 10));     // tuning
     if (const char* ev = getenv("QMC_BATCH_PAIRS")) {  // tuning override
       const long v = strtol(ev, nullptr, 10);
       if (v > 0) {

@@ -129,6 +129,7 @@ struct qmc_plan {
   int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
+  int k1_grid_cap;      // QMC_K1_GRID: cap on K1's persistent grid (0: none; leaves SMs to the other stream)
   // tuning knobs, read from the environment once at plan creation
   int batch_fixed;      // QMC_BATCH_PAIRS set: no per-call halving of the batch
   int k2_nopipe;        // QMC_K2_NOPIPE: non-persistent column pass
