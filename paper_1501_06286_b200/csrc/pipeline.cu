@@ -1297,7 +1297,7 @@ __device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* d
 }
 
 template <int R, int M, int EP>
-__device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2 (*red)[16],
+__device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2& acc,
                                           const double2* tw1) {
   constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = kP2PG;
   const EpiArgs& E = a.E;
@@ -1307,7 +1307,6 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
   const int pair = g * PG + p;
   const int64_t k = 2 * (a.pair0 + pair);
   double* xk = E.X ? E.X + k : nullptr;
-  double2 acc = make_double2(0.0, 0.0);
   if (bx == 0 && warp == 0) {  // row 0: X[0, k] = φ(0) Σ_j A[j, k]
     const bool okrow = tid < PG;
     const double phi0 = __ldg(a.scal);
@@ -1346,22 +1345,32 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
       if (n >= 0) emit_fast<EP>(E, z[k1], n, xk, acc, rr);
     }
   }
-  if (a.part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
+}
+
+// per-column partial sums of a CTA's run of tiles in pair group g (lanes with
+// equal pair, then warps in order) -> part[blockIdx.x][pairs of g]; a CTA
+// visits each pair group in one run of consecutive tiles (tile = blockIdx.x
+// + k·gridDim.x, g = tile / ntx nondecreasing), so the slot row of every
+// group it visits is written once and the rest stays zero
+__device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc, double2 (*red)[16]) {
+  constexpr int PG = kP2PG;
+  const int tid = threadIdx.x, warp = tid >> 5;
 #pragma unroll
-    for (int o = PG; o < 32; o <<= 1) {
-      acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
-      acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
-    }
-    if ((tid & 31) < PG) red[warp][tid & 31] = acc;
-    __syncthreads();
-    if (tid < PG) {
-      double2 sacc = red[0][tid];
-      for (int ww = 1; ww < kP2Thr / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
-      double* dst = a.part + int64_t(bx) * a.part_stride + 2 * pair;
-      dst[0] = sacc.x;
-      dst[1] = sacc.y;
-    }
+  for (int o = PG; o < 32; o <<= 1) {
+    acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+    acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
   }
+  if ((tid & 31) < PG) red[warp][tid & 31] = acc;
+  __syncthreads();
+  if (tid < PG) {
+    double2 sacc = red[0][tid];
+    for (int ww = 1; ww < kP2Thr / 32; ++ww) sacc = cadd(sacc, red[ww][tid]);
+    double* dst = a.part + int64_t(blockIdx.x) * a.part_stride + 2 * (g * PG + tid);
+    dst[0] = sacc.x;
+    dst[1] = sacc.y;
+  }
+  __syncthreads();  // red is reused
+  acc = make_double2(0.0, 0.0);
 }
 
 template <int R, int M, int EP>
@@ -1373,27 +1382,31 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
   __shared__ double2 red[kP2Thr / 32][16];
   __shared__ double2 tw1s[L1];  // ω_{L1}^k: the stage twiddles, read from shared memory
   for (int i = threadIdx.x; i < L1; i += kP2Thr) tw1s[i] = __ldg(&a.tw1[i]);
+  if (a.part)  // this CTA's slot row of column partials starts at zero
+    for (int i = threadIdx.x; i < a.part_stride; i += kP2Thr) a.part[int64_t(blockIdx.x) * a.part_stride + i] = 0.0;
   const int ntiles = a.ntx * a.ngroups;
-#pragma unroll
-  for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
-    const int tl = blockIdx.x + s0 * gridDim.x;
-    if (tl < ntiles) k2p2_issue<L1>(a, tl, sm + s0 * STAGE, nS + s0 * (L1 * kUB));
-    cp_async_commit();
-  }
+  if (int(blockIdx.x) < ntiles) k2p2_issue<L1>(a, blockIdx.x, sm, nS);
+  cp_async_commit();
+  double2 acc = make_double2(0.0, 0.0);
+  int gcur = int(blockIdx.x) / a.ntx;
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-    const int st = it % kPipeStages;
-    const int ahead = tile + (kPipeStages - 1) * gridDim.x;
-    if (ahead < ntiles) {
-      const int sa = (it + kPipeStages - 1) % kPipeStages;
-      k2p2_issue<L1>(a, ahead, sm + sa * STAGE, nS + sa * (L1 * kUB));
-    }
-    cp_async_commit();
-    asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
+    const int st = it & 1;
+    // this tile's data has landed, and every thread is done with the
+    // previous tile: its buffer takes the next tile (one barrier per tile)
+    cp_async_wait_all();
     __syncthreads();
-    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), red, tw1s);
-    __syncthreads();  // stage st and red are reused
+    const int g = tile / a.ntx;
+    if (a.part && g != gcur) {
+      k2p2_flush(a, gcur, acc, red);
+      gcur = g;
+    }
+    const int ahead = tile + gridDim.x;
+    if (ahead < ntiles) k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB));
+    cp_async_commit();
+    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
   }
+  if (a.part && int(blockIdx.x) < ntiles) k2p2_flush(a, gcur, acc, red);
   cp_async_wait_all();
 }
 
@@ -1661,7 +1674,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
           unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(sm_count_cols()) * std::max(per_sm, 1))));
       pk<<<grid, kP2Thr, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum), ilog2(pl->sp.L2));
       QMC_LAUNCHED();
-      *nbx_used = ntx;
+      *nbx_used = int(grid);  // one partial slot row per CTA (k2p2_flush)
       return QMC_OK;
     }
   }
