@@ -487,8 +487,14 @@ __device__ __forceinline__ void rho_bases(double2 (&bw)[8], double2 w, double2 b
 // caller has made S safe to write (the thread's own padE slots); tw2 =
 // ω_{L2}^i (i < L2), b = ω_L^{t f1}: the four-step twiddle of the thread's
 // column is folded into the first stage (all 16 inputs share it).
+// Wr != nullptr: the spectrum row in this register order (Wr[q·NT] for
+// v[q] of the calling thread, Wr already offset by the thread): v leaves
+// multiplied by it, dc receives v[0] before the product.
 template <int L2>
-__device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const double2* __restrict__ tw2, double2 b) {
+__device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const double2* __restrict__ tw2, double2 b,
+                                        const double2* __restrict__ Wr = nullptr, double2* dcp = nullptr) {
+  double2 dc_unused;
+  double2& dc = dcp ? *dcp : dc_unused;
   using D = Dif<L2>;
   constexpr int NT = D::NT, RHO = D::RHO, G = D::G, SUB = D::SUB;
   const int t = tid_fresh();
@@ -536,6 +542,11 @@ __device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const doub
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = B[j + 17 * r];
   }
+#ifndef QMC_W_AHEAD
+#define QMC_W_AHEAD 0
+#endif
+  constexpr int WA = QMC_W_AHEAD;  // spectrum values loaded during the last exchange
+  double2 wv[WA > 0 ? WA : 1];
   if constexpr (SUB >= 256) {
     dft16<-1>(v);
     const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);
@@ -543,11 +554,28 @@ __device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const doub
     else twiddle16<-1>(v, w);
 #pragma unroll
     for (int k = 0; k < 16; ++k) B[j + 17 * k] = v[k];
+    // v is dead until the exchange's reads: the first half of the spectrum
+    // row goes in flight now (its latency overlaps the exchange and the last
+    // butterflies)
+    if (Wr) {
+#pragma unroll
+      for (int q = 0; q < WA; ++q) wv[q] = ldg_ordered(&Wr[q * NT]);
+    }
     __syncwarp();
 #pragma unroll
     for (int p = 0; p < 16; ++p) v[p] = B[17 * j + p];
+  } else if (Wr) {
+#pragma unroll
+    for (int q = 0; q < WA; ++q) wv[q] = ldg_ordered(&Wr[q * NT]);
   }
   dft16<-1>(v);
+  if (Wr) {  // × the spectrum row (this register order), v[0] of thread 0 = DC term first
+    dc = v[0];
+#pragma unroll
+    for (int q = 0; q < WA; ++q) v[q] = cmul(v[q], wv[q]);
+#pragma unroll
+    for (int q = WA; q < 16; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[q * NT]));
+  }
 }
 
 // Inverse DIT, the mirror of dif_fwd (same b): on entry the spectrum in

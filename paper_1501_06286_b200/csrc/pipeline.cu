@@ -496,17 +496,15 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
     const int x = t0 * f1;  // < NT·L1 = L/16
     b = cmul(__ldg(&a.tw1[x >> a.lg2L2]), __ldg(&a.twL[x & (L2 - 1)]));
   }
-  dif_fwd<L2>(v, S, a.tw2, b);
+  // forward row FFT, then × the spectrum row (stored in this register order:
+  // W[f1][r·NT + t]), half of it loaded during the last exchange
+  double2 dc;
+  dif_fwd<L2>(v, S, a.tw2, b, a.W + int64_t(f1) * L2 + tid_fresh(), &dc);
   QMC_TS(2);
   if (f1 == 0 && tid == 0) {  // DC term (register 0 of thread 0) = Σ_j a_j, the row-0 sums
     const int64_t k1 = 2 * (a.pair0 + p);
-    a.colsum[k1] = v[0].x;
-    if (k1 + 1 < a.t) a.colsum[k1 + 1] = v[0].y;
-  }
-  {  // × spectrum (stored in this register order: W[f1][r·NT + t])
-    const double2* Wr = a.W + int64_t(f1) * L2 + tid_fresh();
-#pragma unroll
-    for (int q = 0; q < E; ++q) v[q] = cmul(v[q], ldg_ordered(&Wr[q * NT]));
+    a.colsum[k1] = dc.x;
+    if (k1 + 1 < a.t) a.colsum[k1 + 1] = dc.y;
   }
   QMC_TS(3);
   dif_inv<L2>(v, S, a.tw2, b);
