@@ -1,6 +1,6 @@
 #!/bin/bash
 # The driver's bench commands (default = config 5) plus the other configs' lines -> gpurun_out/$TAG
-TAG=${TAG:-r2/final}
+TAG=${TAG:-r2/final2}
 mkdir -p gpurun_out/$TAG
 timeout 900 python bench.py --impl reference > gpurun_out/$TAG/ref_default.log 2> gpurun_out/$TAG/ref_default.err; echo "ref rc=$?"
 timeout 900 python bench.py > gpurun_out/$TAG/bench_default.log 2> gpurun_out/$TAG/bench_default.err; echo "bench rc=$?"
