@@ -55,7 +55,13 @@ def _ldx(x: torch.Tensor, N: int, t: int) -> int:
     return max(x.stride(0), t, 1) if N > 1 else max(t, 1)
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(device) -> int:
+    """The caller's current CUDA stream on `device` (raw handle)."""
+    if _raw_stream is not None:
+        return _raw_stream(device.index if device.index is not None else torch.cuda.current_device())
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -83,6 +89,7 @@ class Plan:
         self.N, self.m, self.phi = self.info["N"], self.info["m"], phi
         self._ws = None
         self._ws_need = {}  # (t, f) -> call-workspace bytes (qmc_call_workspace_size)
+        self._last_mm, self._last_mm_dims = None, None  # the last matmul's checked (A, X) layouts
 
     @classmethod
     def lattice(cls, N: int, z, phi: int, device=None, delta: float = 0.0) -> "Plan":
@@ -109,11 +116,17 @@ class Plan:
         return self._ws
 
     def matmul(self, A: torch.Tensor, X: torch.Tensor | None = None) -> torch.Tensor:
-        lda = _ld(A, self.s)
-        t = A.shape[1]
-        if X is None:
-            X = x_empty(self.N, t, self.device)
-        ldx = _ldx(X, self.N, t)
+        key = (A.data_ptr(), A.shape, A.stride(), None if X is None else (X.data_ptr(), X.shape, X.stride()))
+        if X is not None and key == self._last_mm:   # same tensors as the last call: layouts already checked
+            lda, t, ldx = self._last_mm_dims
+        else:
+            lda = _ld(A, self.s)
+            t = A.shape[1]
+            if X is None:
+                X = x_empty(self.N, t, self.device)
+            ldx = _ldx(X, self.N, t)
+            if key[3] is not None:
+                self._last_mm, self._last_mm_dims = key, (lda, t, ldx)
         ws = self.call_workspace(t)
         abi.qmc_matmul(self.handle, A, lda, t, X, ldx, ws, ws.numel(), _stream(self.device))
         return X

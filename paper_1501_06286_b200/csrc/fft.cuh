@@ -561,7 +561,7 @@ __device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const doub
 #pragma unroll
       for (int q = 0; q < WA; ++q) wv[q] = ldg_ordered(&Wr[q * NT]);
     }
-    __syncwarp();
+    __syncwarp(NT >= 32 ? 0xffffffffu : 0xffffu);  // the half-warp group (rows of 256: 16 lanes exist)
 #pragma unroll
     for (int p = 0; p < 16; ++p) v[p] = B[17 * j + p];
   } else if (Wr) {
@@ -594,7 +594,7 @@ __device__ __forceinline__ void dif_inv(double2 (&v)[16], double2* S, const doub
     double2* B2 = B + 272 * k;
 #pragma unroll
     for (int p = 0; p < 16; ++p) B2[17 * j + p] = v[p];
-    __syncwarp();
+    __syncwarp(NT >= 32 ? 0xffffffffu : 0xffffu);  // the half-warp group (rows of 256: 16 lanes exist)
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = B2[j + 17 * r];
     const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);

@@ -561,7 +561,8 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
 constexpr int kSmallMaxS = 2048;  // A's two columns, the bucket lists in shared memory
 // the row, the pair's two columns of A, the columns in bucket order, the bucket starts
 inline size_t small_smem(int64_t L2, int64_t s) {
-  return size_t(k1_row_slots(L2, 16)) * 16 + size_t(s) * 20 + size_t(L2 + 1) * 4 + 16;
+  return size_t(k1_row_slots(L2, 16)) * 16 + size_t(s) * 20 + size_t(L2 + 4) * 4 + 32 +
+         (L2 == 256 ? size_t(L2) * 20 : 0);  // rows of 256: the spectrum row and the row map too
 }
 
 // epilogue kinds (compile time) of the column passes: LIN writes c + X (c = 0
@@ -585,9 +586,15 @@ struct SmallArgs {
   double* __restrict__ out;
 };
 
+// threads of the one-row kernel: rows of 256 (NT = 16) take 128 threads for
+// the loads and bucket sums (the row FFT of that length synchronises only
+// within its half-warp, so the other threads may leave after the sums)
+template <int L2>
+__host__ __device__ constexpr int small_threads() { return L2 == 256 ? 128 : L2 / 16; }
+
 template <int L2, int EP>
-__global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
-  constexpr int NT = L2 / 16;
+__global__ void __launch_bounds__(small_threads<L2>()) k_small(SmallArgs a) {
+  constexpr int NT = L2 / 16, BT = small_threads<L2>();
   extern __shared__ double2 smem[];
   double2* S = smem;
   double* colA = reinterpret_cast<double*>(smem + k1_row_slots(L2, 16));  // [2][s]
@@ -599,18 +606,24 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
   const double* a1 = a.A + k1 * a.lda;
   const double* a2 = a.A + (has2 ? k2 : k1) * a.lda;
 #pragma unroll 8
-  for (int j = t; j < int(a.s); j += NT) {  // independent loads, many in flight
+  for (int j = t; j < int(a.s); j += BT) {  // independent loads, many in flight
     colA[j] = __ldg(&a1[j]);
     colA[a.s + j] = has2 ? __ldg(&a2[j]) : 0.0;
     js[j] = __ldg(&a.bent[j]).x;
   }
 #pragma unroll 8
-  for (int i = t; i <= L2; i += NT) bs[i] = __ldg(&a.bstart[i]);
+  for (int i = t; i <= L2; i += BT) bs[i] = __ldg(&a.bstart[i]);
+  // rows of 256: the spare threads also bring the spectrum row and the row map
+  double2* Ws = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(bs + L2 + 1) + 15) & ~uintptr_t(15));  // [L2]
+  int* Ps = reinterpret_cast<int*>(Ws + L2);                        // [L2]: P[(m - i) mod m]
+  if constexpr (BT > NT) {
+    for (int i = t; i < L2; i += BT) {
+      Ws[i] = __ldg(&a.W[i]);
+      Ps[i] = i < a.m ? __ldg(&a.P[i == 0 ? 0 : a.m - i]) : -1;
+    }
+  }
   __syncthreads();
-  double2 v[16];
-#pragma unroll
-  for (int q = 0; q < 16; ++q) {  // bucket e2 = t + NT q, entries in j order
-    const int e2 = t + NT * q;
+  for (int e2 = t; e2 < L2; e2 += BT) {  // bucket e2's entries in j order -> row slot
     double2 acc = make_double2(0.0, 0.0);
     for (int i = bs[e2], i1 = bs[e2 + 1]; i < i1; ++i) {
       const int j = js[i];
@@ -618,12 +631,20 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
       acc.x += colA[j];
       acc.y += colA[a.s + j];
     }
-    v[q] = acc;
+    S[padE<16>(e2)] = acc;
   }
+  __syncthreads();
+  if (BT > NT && t >= NT) return;  // (rows of 256: no CTA-wide barrier follows)
+  double2 v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = S[padE<16>(t + NT * q)];
   const double2 one = make_double2(1.0, 0.0);
   dif_fwd<L2>(v, S, a.tw2, one);
   const double2 dc = v[0];  // thread 0: Σ_j a_j (the row-0 sums)
-  {
+  if constexpr (BT > NT) {
+#pragma unroll
+    for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], Ws[t + q * NT]);
+  } else {
     const double2* Wr = a.W + t;
 #pragma unroll
     for (int q = 0; q < 16; ++q) v[q] = cmul(v[q], __ldg(&Wr[q * NT]));
@@ -635,7 +656,7 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
   for (int q = 0; q < 16; ++q) {
     const int64_t i = t + int64_t(NT) * q;  // reordered row (i >= m: zero padding)
     if (i < a.m) {
-      const int64_t n = __ldg(&a.P[i == 0 ? 0 : a.m - i]);
+      const int64_t n = BT > NT ? int64_t(Ps[i]) : int64_t(__ldg(&a.P[i == 0 ? 0 : a.m - i]));
       QMC_CHECK_IDX(n, a.N);
       double2 x = v[q];
       if (EP == EPK_LIN) {
@@ -674,11 +695,11 @@ __global__ void __launch_bounds__(L2 / 16) k_small(SmallArgs a) {
       acc.y += exp(x.y);
     }
   }
-  if (EP >= 0 && a.out) {  // the column means, a fixed-order reduction over the CTA
-    __syncthreads();
+  if (EP >= 0 && a.out) {  // the column means, a fixed-order reduction over the row's threads
+    if constexpr (BT > NT) __syncwarp(0xffffu); else __syncthreads();
     double2* red = S;
     red[t] = acc;
-    __syncthreads();
+    if constexpr (BT > NT) __syncwarp(0xffffu); else __syncthreads();
     if (t == 0) {
       double2 sum = red[0];
       for (int u = 1; u < NT; ++u) sum = cadd(sum, red[u]);
@@ -1748,7 +1769,7 @@ static int launch_small(const SmallArgs& sa, int64_t npairs, cudaStream_t st) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(small_smem(L2, kSmallMaxS)));
     attr = true;
   }
-  kern<<<unsigned(npairs), L2 / 16, smem, st>>>(sa);
+  kern<<<unsigned(npairs), small_threads<L2>(), smem, st>>>(sa);
   QMC_LAUNCHED();
   return QMC_OK;
 }
