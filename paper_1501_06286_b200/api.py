@@ -90,6 +90,7 @@ class Plan:
         self._ws = None
         self._ws_need = {}  # (t, f) -> call-workspace bytes (qmc_call_workspace_size)
         self._last_mm, self._last_mm_dims = None, None  # the last matmul's checked (A, X) layouts
+        self._last_mean, self._last_mean_dims = None, None
 
     @classmethod
     def lattice(cls, N: int, z, phi: int, device=None, delta: float = 0.0) -> "Plan":
@@ -133,12 +134,17 @@ class Plan:
 
     def mean(self, A: torch.Tensor, f: int, f_param: float = 0.0, X: torch.Tensor | None = None,
              out: torch.Tensor | None = None) -> torch.Tensor:
-        lda = _ld(A, self.s)
-        t = A.shape[1]
+        key = (A.data_ptr(), A.shape, A.stride(), None if X is None else (X.data_ptr(), X.shape, X.stride()))
+        if key == self._last_mean:   # same tensors as the last call: layouts already checked
+            lda, t, ldx = self._last_mean_dims
+        else:
+            lda = _ld(A, self.s)
+            t = A.shape[1]
+            ldx = _ldx(X, self.N, t) if X is not None else max(t, 1)
+            self._last_mean, self._last_mean_dims = key, (lda, t, ldx)
         n_out = self.N if f == abi.QMC_F_ROWMEAN_RELU else t
         if out is None:
             out = torch.empty(max(n_out, 1), dtype=torch.float64, device=self.device)
-        ldx = _ldx(X, self.N, t) if X is not None else max(t, 1)
         ws = self.call_workspace(t, f)
         abi.qmc_mean(self.handle, A, lda, t, f, f_param, out, X, ldx, ws, ws.numel(),
                      _stream(self.device))
