@@ -275,7 +275,9 @@ def test_config5_sampled(qmc):
 # pipelined two-stage pass: N = 3079 (L = 6400 = 25·256, L1 = 5·5) and
 # N = 65539 (L = 163840 = 20·8192, L1 = 2·10).
 MEAN_CASES = [(65537, 64, 32, None), (65537, 64, 30, None), (40961, 50, 32, None), (65537, 40, 64, 16),
-              (786433, 16, 6, None), (786433, 16, 32, None), (3079, 50, 32, None), (65539, 40, 32, None)]
+              (786433, 16, 6, None), (786433, 16, 32, None), (3079, 50, 32, None), (65539, 40, 32, None),
+              # one-row plans (the fused k_small): rows of 256 with s > m and odd t; rows of 32 (2 threads)
+              (257, 300, 7, None), (13, 5, 4, None)]
 
 
 @pytest.mark.parametrize("N,s,t,bp", MEAN_CASES)
