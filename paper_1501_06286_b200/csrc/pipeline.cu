@@ -1315,7 +1315,7 @@ __device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* d
   }
 }
 
-template <int R, int M, int EP>
+template <int R, int M, int EP, bool PAD>
 __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2& acc,
                                           const double2* tw1) {
   constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = kP2PG;
@@ -1361,7 +1361,7 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
 #pragma unroll
     for (int k1 = 0; k1 < R; ++k1) {
       const int n = nS[(k2 + M * k1) * kUB + c];  // -1: padding row (uniform over the 8 lanes of the row)
-      if (n >= 0) emit_fast<EP>(E, z[k1], n, xk, acc, rr);
+      if (!PAD || n >= 0) emit_fast<EP>(E, z[k1], n, xk, acc, rr);  // PAD: zero-padded length
     }
   }
 }
@@ -1392,7 +1392,7 @@ __device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc,
   acc = make_double2(0.0, 0.0);
 }
 
-template <int R, int M, int EP>
+template <int R, int M, int EP, bool PAD>
 __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
   constexpr int L1 = R * M;
   constexpr int STAGE = kP2PG * pipe2_pair_stride<L1>();
@@ -1423,7 +1423,7 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
     const int ahead = tile + gridDim.x;
     if (ahead < ntiles) k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB));
     cp_async_commit();
-    k2p2_tile<R, M, EP>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
+    k2p2_tile<R, M, EP, PAD>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
   }
   if (a.part && int(blockIdx.x) < ntiles) k2p2_flush(a, gcur, acc, red);
   cp_async_wait_all();
@@ -1679,10 +1679,12 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
     // vector X stores, whole U column blocks
     if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !pl->k2_nopipe) {
       constexpr size_t psm = cols_pipe2_smem<L1>();
-      auto pk = k_cols_pipe2<R, M, EP>;
-      static int per_sm0 = -1;  // per instantiation: constant shared memory
+      // zero-padded lengths (L > m) skip the rows i >= m; exact lengths need no test
+      auto pk = pl->sp.L != pl->m ? k_cols_pipe2<R, M, EP, true> : k_cols_pipe2<R, M, EP, false>;
+      static int per_sm0 = -1;  // per instantiation (both variants): constant shared memory
       if (per_sm0 < 0) {
-        set_smem_attr(pk, psm);
+        set_smem_attr(k_cols_pipe2<R, M, EP, true>, psm);
+        set_smem_attr(k_cols_pipe2<R, M, EP, false>, psm);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm0, pk, kP2Thr, psm);
       }
       int per_sm = per_sm0;
