@@ -267,7 +267,7 @@ def k1_fp64_instr_per_item(L2):
     ×W, folded twiddles), counted from ncu smsp__sass_thread_inst_executed
     _op_{dadd,dmul,dfma} of the round-2 build (profiles/r02_fp64_audit.txt);
     None if not audited for this row length."""
-    return {4096: 1658.0, 8192: 1882.0}.get(L2)
+    return {4096: 1658.0, 8192: 1871.0}.get(L2)
 
 
 def ours(args, rank, world, local_rank):
