@@ -1924,7 +1924,11 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   // (measured on B200: c2 0.61 vs 0.68 ms, c3 24.2 vs 26.7, c4 2.37 vs 2.47;
   // c5 (L1 = 96) 78.8 vs 79.0 ms — equal, so its device calls run on the
   // caller's stream, where each kernel's event time is its own)
+#ifdef QMC_DIAG_TWO_ALWAYS
+  const bool two = cl.nsets == 2 && pl->nstreams == 2;
+#else
   const bool two = cl.nsets == 2 && pl->nstreams == 2 && (A_host || pl->sp.L1 <= 16);
+#endif
   if (two) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
     if (cudaEventRecord(pl->ev_fork, st) != cudaSuccess ||
