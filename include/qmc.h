@@ -129,6 +129,30 @@ int qmc_plan_create(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host
 int qmc_plan_create_shifted(qmc_plan_t* out, int64_t N, int64_t s, const int64_t* z_host, int phi,
                             double delta, void* plan_ws, size_t plan_ws_bytes, void* stream);
 
+/* Shifted replicate of a lattice plan (with an equal shift
+ * only the circulant base ζ — so φ(x_0) and the spectrum of Z — depends on
+ * Δ).  *out shares every table of `base` (P, L, e, the K1 scatter order and
+ * twiddles: they live in base's plan_ws, which must outlive *out) and owns
+ * only ζ, φ(x_0) and W, built in shift_ws (device, 256-B aligned, at least
+ * qmc_shift_workspace_size(base) bytes ≈ 8m + 16L; caller-owned, must
+ * outlive *out).  The result computes the same as qmc_plan_create_shifted
+ * (N, z, phi, Δ) and is used like any plan (qmc_matmul / qmc_mean / ...);
+ * free it with qmc_plan_destroy (base's tables are not touched).  base must
+ * be a lattice plan (else QMC_EUNSUPPORTED); its own Δ is ignored.
+ * Δ outside [0, 1) -> QMC_EINVAL_PHI.  Synchronises `stream`. */
+int qmc_shift_workspace_size(qmc_plan_t base, size_t* shift_bytes);
+int qmc_plan_shift(qmc_plan_t* out, qmc_plan_t base, double delta, void* shift_ws, size_t shift_ws_bytes,
+                   void* stream);
+
+/* Randomised-QMC estimate from R replicates (the R shifted rules above;
+ * reading R28): means[r*ld + k], r < R, k < t (device) ->
+ * mean_out[k] = (1/R) Σ_r means[r,k], summed in the fixed order r = 0..R-1
+ * (bit-reproducible), and, if stderr_out is not NULL,
+ * stderr_out[k] = sqrt(Σ_r (means[r,k] - mean_out[k])^2 / (R (R-1)))
+ * (NaN for R = 1).  R >= 1, t >= 0, ld >= t, else QMC_EINVAL_DIM. */
+int qmc_replicate_mean(const double* means, int64_t R, int64_t t, int64_t ld, double* mean_out,
+                       double* stderr_out, void* stream);
+
 /* Polynomial lattice over F_2 (PAPER.md:456-459 Remark; reading R2/R3):
  * p has bit D set, 2 <= D <= 24, and must be primitive (checked on the
  * device: x has order 2^D-1); q_host: s values in [1, 2^D-1] (integer

@@ -16,6 +16,7 @@ Contents
                               selection_P
   the product and means     : oracle_X_rows, oracle_X_rows_fsum,
                               column_means, rowmean_relu
+  randomised QMC            : replicate_estimate (reading R28)
 Pins: tests/test_oracle_pins.py (``rowmean_relu`` and ``column_means``
 with f=EXP by special cases: test_rowmean_relu_pins, test_exp_mean_pins).
 """
@@ -37,7 +38,7 @@ __all__ = [
     "phi_value", "phi_table", "lattice_index_matrix", "polylattice_index_matrix",
     "point_matrix_rows", "reordered_lattice_point", "circulant_Z", "selection_P",
     "oracle_X_rows", "oracle_X_rows_fsum", "oracle_X_full", "column_means",
-    "rowmean_relu", "row_sums",
+    "rowmean_relu", "row_sums", "replicate_estimate",
     "pset_index_matrix", "pset_c", "pset_reordered_point",
     "pde1d_fe_mean", "pde1d_lognormal_fe_mean", "phi_value_shifted", "phi_table_shifted",
     "cbc_criterion_table", "cbc_lattice", "cbc_error",
@@ -395,6 +396,22 @@ def column_means(Xcol: np.ndarray, f: int, param: float = 0.0) -> np.ndarray:
     else:
         raise ValueError("unknown f")
     return np.array([math.fsum(F[:, k]) / N for k in range(F.shape[1])])
+
+
+def replicate_estimate(Q: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """Randomised-QMC estimate from R independently shifted replicates
+    (reading R28; the shifts are the equal shifts PAPER.md:466-468 allows):
+    Q̄_k = (1/R) Σ_r Q[r,k] and the standard error
+    sqrt(Σ_r (Q[r,k] - Q̄_k)^2 / (R (R-1))) (NaN for R = 1), math.fsum.
+    Pinned against statistics.fmean / statistics.stdev / sqrt(R) and the
+    R = 2 closed form |Q_0 - Q_1| / 2 (test_replicate_estimate_pins)."""
+    Q = np.asarray(Q, dtype=np.float64)
+    R, t = Q.shape
+    mean = np.array([math.fsum(Q[:, k]) / R for k in range(t)])
+    if R < 2:
+        return mean, np.full(t, np.nan)
+    err = np.array([math.sqrt(math.fsum((Q[:, k] - mean[k]) ** 2) / (R * (R - 1))) for k in range(t)])
+    return mean, err
 
 
 def row_sums(X: np.ndarray) -> np.ndarray:

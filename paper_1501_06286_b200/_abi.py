@@ -27,6 +27,7 @@ EXPORTS = [
     "qmc_plan_info", "qmc_plan_tables", "qmc_launch_count", "qmc_plan_destroy", "qmc_strerror",
     "qmc_profile_enable", "qmc_profile_read", "qmc_profile_class_name", "qmc_tridiag_solve_mean",
     "qmc_fe1d_lognormal_solve_mean", "qmc_plan_create_shifted", "qmc_cbc_step", "qmc_pset_matmul", "qmc_build_flags",
+    "qmc_shift_workspace_size", "qmc_plan_shift", "qmc_replicate_mean",
 ]
 QMC_EUNSUPPORTED = -10
 
@@ -56,6 +57,9 @@ _sig = {
     "qmc_plan_create": (_i32, [C.POINTER(_vp), _i64, _i64, _P64, _i32, _vp, _sz, _vp]),
     "qmc_plan_create_poly": (_i32, [C.POINTER(_vp), _i32, C.c_uint64, _i64, _P64, _i32, _vp, _sz, _vp]),
     "qmc_plan_create_shifted": (_i32, [C.POINTER(_vp), _i64, _i64, _P64, _i32, _d, _vp, _sz, _vp]),
+    "qmc_shift_workspace_size": (_i32, [_vp, _PSZ]),
+    "qmc_plan_shift": (_i32, [C.POINTER(_vp), _vp, _d, _vp, _sz, _vp]),
+    "qmc_replicate_mean": (_i32, [_vp, _i64, _i64, _i64, _vp, _vp, _vp]),
     "qmc_matmul": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp, _sz, _vp]),
     "qmc_pset_matmul": (_i32, [_vp, _vp, _i64, _i64, _vp, _i64, _vp]),
     "qmc_mean": (_i32, [_vp, _vp, _i64, _i64, _i32, _d, _vp, _vp, _i64, _vp, _sz, _vp]),
@@ -142,6 +146,23 @@ def qmc_plan_create_shifted(N: int, s: int, z, phi: int, delta: float, plan_ws, 
     _check(_lib.qmc_plan_create_shifted(C.byref(h), N, s, p, phi, delta, ptr(plan_ws), plan_ws_bytes, stream),
            "qmc_plan_create_shifted")
     return h
+
+
+def qmc_shift_workspace_size(base) -> int:
+    out = C.c_size_t(0)
+    _check(_lib.qmc_shift_workspace_size(base, C.byref(out)), "qmc_shift_workspace_size")
+    return out.value
+
+
+def qmc_plan_shift(base, delta: float, shift_ws, shift_ws_bytes: int, stream=None):
+    h = _vp()
+    _check(_lib.qmc_plan_shift(C.byref(h), base, delta, ptr(shift_ws), shift_ws_bytes, stream), "qmc_plan_shift")
+    return h
+
+
+def qmc_replicate_mean(means, R: int, t: int, ld: int, mean_out, stderr_out=None, stream=None):
+    _check(_lib.qmc_replicate_mean(ptr(means), R, t, ld, ptr(mean_out), ptr(stderr_out), stream),
+           "qmc_replicate_mean")
 
 
 def qmc_plan_create_poly(D: int, p: int, s: int, q, phi: int, plan_ws, plan_ws_bytes: int, stream=None):

@@ -229,16 +229,61 @@ class KorobovPSet:
         return buf[1:]
 
 
+class ShiftedPlan(Plan):
+    """A replicate of `base` with every point shifted by Δ (qmc_plan_shift):
+    shares base's tables, owns only ζ, φ(x_0) and the spectrum (about
+    8m + 16L bytes).  Keeps `base` alive."""
+
+    def __init__(self, base: Plan, delta: float):
+        self.base = base
+        self.device = base.device
+        self.s = base.s
+        nbytes = abi.qmc_shift_workspace_size(base.handle)
+        self.plan_ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            self.handle = abi.qmc_plan_shift(base.handle, float(delta), self.plan_ws, nbytes, _stream(self.device))
+        self.info = abi.qmc_plan_info(self.handle)
+        self.N, self.m, self.phi = self.info["N"], self.info["m"], base.phi
+        self._ws = base._ws if base._ws is not None else None
+        self._ws_need = base._ws_need
+        self._last_mm, self._last_mm_dims = None, None
+        self._last_mean, self._last_mean_dims = None, None
+
+
+def replicate_mean(means: torch.Tensor, with_stderr: bool = True):
+    """(R, t) replicate means -> (mean over r, standard error) by the library's
+    fixed-order kernel (qmc_replicate_mean; reading R28)."""
+    if means.dtype != torch.float64 or means.dim() != 2 or (means.shape[1] > 1 and means.stride(1) != 1):
+        raise ValueError("(R, t) fp64 tensor with contiguous rows required")
+    R, t = means.shape
+    mean = torch.empty(t, dtype=torch.float64, device=means.device)
+    err = torch.empty(t, dtype=torch.float64, device=means.device) if with_stderr else None
+    abi.qmc_replicate_mean(means, R, t, max(means.stride(0), t), mean, err, _stream(means.device))
+    return mean, err
+
+
 def shifted_means(N: int, z, phi: int, A: torch.Tensor, f: int, f_param: float, deltas,
-                  device=None) -> tuple[torch.Tensor, torch.Tensor]:
+                  device=None, return_stderr: bool = False):
     """Randomised QMC: the fused means of f(X) over R
     equally shifted copies of the rule (Δ_r in `deltas`).
-    Returns (per-replicate means R × t, their average over r).  The spread
-    over replicates is the usual error estimate; each replicate is one plan
-    (only ζ changes) and one fused qmc_mean call."""
-    outs = []
-    for d in deltas:
-        plan = Plan.lattice(N, z, phi, device=device, delta=float(d))
-        outs.append(plan.mean(A, f, f_param))
-    R = torch.stack(outs)
-    return R, R.mean(dim=0)
+    Returns (per-replicate means R × t, their average over r[, the standard
+    error]).  One lattice plan holds the tables; each replicate is a
+    qmc_plan_shift view (only ζ and W are rebuilt) and one fused qmc_mean
+    call writing its row of the R × t result; the average and standard error
+    come from qmc_replicate_mean (fixed order r = 0..R-1)."""
+    if f == abi.QMC_F_ROWMEAN_RELU:
+        raise ValueError("shifted_means averages per-column means (f = IDENTITY / AFFINE / EXP)")
+    deltas = [float(d) for d in deltas]
+    base = Plan.lattice(N, z, phi, device=device)
+    t = A.shape[1]
+    out = torch.empty((len(deltas), max(t, 1)), dtype=torch.float64, device=base.device)
+    rep = None
+    for r, d in enumerate(deltas):
+        rep = ShiftedPlan(base, d)
+        rep.mean(A, f, f_param, out=out[r])
+        base._ws = rep._ws  # one call workspace for all replicates
+    R = out[:, :t]
+    avg, err = replicate_mean(R, with_stderr=return_stderr)
+    if return_stderr:
+        return R, avg, err
+    return R, avg

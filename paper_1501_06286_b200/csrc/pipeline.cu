@@ -1979,6 +1979,26 @@ static int pset_dispatch(const qmc_plan* pl, const SmallArgs& sa, int64_t npairs
 
 using namespace qmc;
 
+// randomised-QMC estimate over R replicates (qmc_replicate_mean; reading
+// R28): one thread per column k, replicates summed in the fixed order r = 0..R-1
+__global__ void k_replicate_mean(const double* __restrict__ means, int64_t R, int64_t t, int64_t ld,
+                                 double* __restrict__ mean_out, double* __restrict__ stderr_out) {
+  const int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (k >= t) return;
+  double sum = 0.0;
+  for (int64_t r = 0; r < R; ++r) sum += means[r * ld + k];
+  const double mu = sum / double(R);
+  mean_out[k] = mu;
+  if (stderr_out) {
+    double ss = 0.0;
+    for (int64_t r = 0; r < R; ++r) {
+      const double d = means[r * ld + k] - mu;
+      ss = fma(d, d, ss);
+    }
+    stderr_out[k] = R > 1 ? sqrt(ss / (double(R) * double(R - 1))) : __longlong_as_double(0x7ff8000000000000LL);
+  }
+}
+
 extern "C" {
 
 int qmc_call_workspace_size(qmc_plan_t pl, int64_t t, int f, size_t* call_bytes) {
@@ -2048,6 +2068,16 @@ int qmc_mean_finalize(qmc_plan_t pl, int f, const double* reduced, int64_t t_tot
   }
   QMC_LAUNCHED();
   prof_end(KC_FINALIZE, st);
+  return QMC_OK;
+}
+
+int qmc_replicate_mean(const double* means, int64_t R, int64_t t, int64_t ld, double* mean_out,
+                       double* stderr_out, void* stream) {
+  if (R < 1 || t < 0 || ld < t) return QMC_EINVAL_DIM;
+  if (t == 0) return QMC_OK;
+  if (!means || !mean_out) return QMC_ENULL;
+  k_replicate_mean<<<nblk(t, 128), 128, 0, (cudaStream_t)stream>>>(means, R, t, ld, mean_out, stderr_out);
+  QMC_LAUNCHED();
   return QMC_OK;
 }
 

@@ -587,6 +587,26 @@ static int validate_family(int family, int64_t N_or_D, int64_t s, int64_t* N, in
   return QMC_OK;
 }
 
+// the plan's internal streams: two overlap consecutive batches when the
+// column pass is a persistent pipelined kernel (k_cols_pipe, k_cols_pipe2:
+// L1 <= 192); with the non-persistent k_cols_x (L1 = 256) the overlap
+// measured slower, so such plans use the caller's stream (run() further
+// restricts the two streams to calls where they overlap something)
+static void plan_streams(qmc_plan* pl) {
+  pl->nstreams = 1;
+  pl->mu = new (std::nothrow) std::mutex();
+  const char* one = getenv("QMC_ONE_STREAM");
+  const bool want2 = one ? one[0] != '1' : pl->sp.L1 <= 192;
+  if (want2 && pl->mu &&
+      cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
+      cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
+      cudaEventCreateWithFlags(&pl->ev_join[1], cudaEventDisableTiming) == cudaSuccess)
+    pl->nstreams = 2;
+  cudaGetLastError();
+}
+
 static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p, double delta, int64_t s,
                          const int64_t* z_host, int phi, void* plan_ws, size_t plan_ws_bytes,
                          void* stream) {
@@ -825,23 +845,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_CHECK(cudaStreamSynchronize(st) ? QMC_ECUDA : 0);
 #undef QMC_PLAN_CHECK
 #undef QMC_PLAN_LAUNCHED
-  pl->nstreams = 1;
-  pl->mu = new (std::nothrow) std::mutex();
-  // two internal streams overlap consecutive batches when the column pass is
-  // a persistent pipelined kernel (k_cols_pipe, k_cols_pipe2: L1 <= 192;
-  // measured on B200, config 5: 98.6 vs 105.0 ms/step).  With the
-  // non-persistent k_cols_x (L1 = 256) the overlap measured slower (config 5
-  // before k_cols_pipe2: 119 vs 111 ms), so such plans use the caller's stream.
-  const char* one = getenv("QMC_ONE_STREAM");
-  const bool want2 = one ? one[0] != '1' : sp.L1 <= 192;
-  if (want2 && pl->mu &&
-      cudaStreamCreateWithFlags(&pl->ist[0], cudaStreamNonBlocking) == cudaSuccess &&
-      cudaStreamCreateWithFlags(&pl->ist[1], cudaStreamNonBlocking) == cudaSuccess &&
-      cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-      cudaEventCreateWithFlags(&pl->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
-      cudaEventCreateWithFlags(&pl->ev_join[1], cudaEventDisableTiming) == cudaSuccess)
-    pl->nstreams = 2;
-  cudaGetLastError();
+  plan_streams(pl);
   *out = pl;
   return QMC_OK;
 }
@@ -872,6 +876,64 @@ int qmc_plan_create_shifted(qmc_plan_t* out, int64_t N, int64_t s, const int64_t
                             void* plan_ws, size_t plan_ws_bytes, void* stream) {
   if (!(delta >= 0.0 && delta < 1.0)) return QMC_EINVAL_PHI;
   return create_common(out, QMC_FAMILY_LATTICE, N, 0, delta, s, z_host, phi, plan_ws, plan_ws_bytes, stream);
+}
+
+// a replicate plan of an equally shifted rule shares every table of its base
+// lattice plan except ζ, φ(x_0) and the spectrum W (only the
+// circulant base changes with Δ)
+static size_t shift_ws_layout(const qmc_plan* base, size_t* off_zeta, size_t* off_W) {
+  size_t o = 0;
+  auto take = [&](size_t bytes) {
+    size_t r = o;
+    o = align_up(o + bytes);
+    return r;
+  };
+  take(16 * 8);  // scal
+  *off_zeta = take(size_t(base->m) * 8);
+  *off_W = take(size_t(base->sp.L) * 16);
+  return o;
+}
+
+int qmc_shift_workspace_size(qmc_plan_t base, size_t* bytes) {
+  if (!base || !bytes) return QMC_ENULL;
+  size_t a, b;
+  *bytes = shift_ws_layout(base, &a, &b);
+  return QMC_OK;
+}
+
+int qmc_plan_shift(qmc_plan_t* out, qmc_plan_t base, double delta, void* shift_ws, size_t shift_ws_bytes,
+                   void* stream) {
+  if (!out) return QMC_ENULL;
+  *out = nullptr;
+  if (!base || !shift_ws) return QMC_ENULL;
+  if (base->family != QMC_FAMILY_LATTICE) return QMC_EUNSUPPORTED;
+  if (!(delta >= 0.0 && delta < 1.0)) return QMC_EINVAL_PHI;
+  size_t off_zeta, off_W;
+  const size_t need = shift_ws_layout(base, &off_zeta, &off_W);
+  if (shift_ws_bytes < need || (uintptr_t(shift_ws) % kAlign)) return QMC_EWORKSPACE;
+  qmc_plan* pl = new (std::nothrow) qmc_plan(*base);  // the shared tables: same device pointers
+  if (!pl) return QMC_ECUDA;
+  pl->delta = delta;
+  pl->stream = (cudaStream_t)stream;
+  char* b = (char*)shift_ws;
+  pl->d_scal = (double*)b;
+  pl->d_zeta = (double*)(b + off_zeta);
+  pl->d_W = (double2*)(b + off_W);
+  pl->nstreams = 1;
+  pl->mu = nullptr;
+  const cudaStream_t st = pl->stream;
+  k_zeta<<<blocks(pl->m, 256), 256, 0, st>>>(pl->family, pl->phi, delta, pl->N, pl->p, pl->D, pl->m, pl->d_P,
+                                             pl->d_zeta, pl->d_scal);
+  const bool zeta_ok = cudaPeekAtLastError() == cudaSuccess;
+  if (zeta_ok) g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (!zeta_ok || spectrum_dispatch(pl) != QMC_OK || cudaStreamSynchronize(st) != cudaSuccess) {
+    cudaGetLastError();
+    delete pl;
+    return QMC_ECUDA;
+  }
+  plan_streams(pl);
+  *out = pl;
+  return QMC_OK;
 }
 
 int qmc_plan_create_poly(qmc_plan_t* out, int D, uint64_t p, int64_t s, const int64_t* q_host,

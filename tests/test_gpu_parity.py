@@ -427,19 +427,71 @@ def test_shifted_lattice(qmc, N, s, t, delta, phi):
 
 
 def test_shifted_replicate_means(qmc):
-    """R = 4 equally shifted replicates of config 3's affine mean (c + X): each
-    replicate's fused column means against the oracle's."""
+    """R = 4 equally shifted replicates of config 3's affine mean (c + X), one
+    base plan + qmc_plan_shift views: each replicate's fused column means
+    against the oracle's, and the library's replicate mean / standard error
+    (qmc_replicate_mean) against the oracle's estimate (R28)."""
     import torch
     N, s, t = 4001, 64, 8
     w = W.custom_lattice(N, s, t, W.PHI_SHIFT_HALF, seed=9)
     deltas = [0.1, 0.35, 0.6, 0.85]
-    R, avg = qmc.shifted_means(N, w.z, W.PHI_SHIFT_HALF, qmc.to_device_colmajor(w.A, "cuda"),
-                               W.F_AFFINE, 1.0, deltas)
+    R, avg, err = qmc.shifted_means(N, w.z, W.PHI_SHIFT_HALF, qmc.to_device_colmajor(w.A, "cuda"),
+                                    W.F_AFFINE, 1.0, deltas, return_stderr=True)
     torch.cuda.synchronize()
+    Qo = []
     for r, d in enumerate(deltas):
         Xo = O.oracle_X_full(index_fn(w), O.phi_table_shifted(W.PHI_SHIFT_HALF, N, d), N, w.A)
-        np.testing.assert_allclose(R[r].cpu().numpy(), O.column_means(Xo, O.F_AFFINE, 1.0), rtol=0, atol=1e-12)
-    np.testing.assert_allclose(avg.cpu().numpy(), R.cpu().numpy().mean(axis=0), rtol=1e-15)
+        Qo.append(O.column_means(Xo, O.F_AFFINE, 1.0))
+        np.testing.assert_allclose(R[r].cpu().numpy(), Qo[-1], rtol=0, atol=1e-12)
+    mo, eo = O.replicate_estimate(np.array(Qo))
+    np.testing.assert_allclose(avg.cpu().numpy(), mo, rtol=0, atol=1e-12)
+    # the error is a difference of near-equal means: its absolute error is the means' (1e-12)
+    np.testing.assert_allclose(err.cpu().numpy(), eo, rtol=0, atol=2e-12)
+    # the fixed-order kernel equals the same-order sum of the replicates exactly
+    Rh = R.cpu().numpy()
+    np.testing.assert_array_equal(avg.cpu().numpy(), (((Rh[0] + Rh[1]) + Rh[2]) + Rh[3]) / 4)
+
+
+@pytest.mark.parametrize("N,s,t,phi", [(13, 7, 3, W.PHI_SHIFT_HALF), (65537, 64, 32, W.PHI_INVNORM_MID),
+                                       (4001, 100, 9, W.PHI_TENT)])
+def test_plan_shift_matches_shifted_plan(qmc, N, s, t, phi):
+    """A qmc_plan_shift view of an unshifted plan computes exactly (bitwise)
+    what a plan created with the same Δ computes (same kernels, same tables),
+    and against the oracle; the base plan is unchanged after the view."""
+    import torch
+    w = W.custom_lattice(N, s, t, phi, seed=N + 3 * t)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    base = qmc.Plan.lattice(N, w.z, phi)
+    X0 = base.matmul(A).clone()
+    for delta in (0.25, 0.7123):
+        view = qmc.ShiftedPlan(base, delta)
+        Xv = view.matmul(A).cpu().numpy()
+        Xs = qmc.Plan.lattice(N, w.z, phi, delta=delta).matmul(A).cpu().numpy()
+        torch.cuda.synchronize()
+        np.testing.assert_array_equal(Xv, Xs)
+        tab = O.phi_table_shifted(phi, N, delta)
+        Xo = O.oracle_X_full(index_fn(w), tab, N, w.A)
+        tol = 1e-11 * np.abs(w.A).sum(axis=0) * np.abs(tab).max()
+        assert np.all(np.abs(Xv - Xo).max(axis=0) <= tol)
+    np.testing.assert_array_equal(base.matmul(A).cpu().numpy(), X0.cpu().numpy())
+
+
+def test_replicate_mean_edges(qmc):
+    """qmc_replicate_mean: R = 1 (stderr NaN), t = 0 (no-op), strided rows,
+    bad dimensions rejected."""
+    import torch
+    Q = torch.tensor(np.random.default_rng(5).standard_normal((3, 10)), device="cuda")
+    m, e = qmc.replicate_mean(Q[:1])
+    assert torch.equal(m, Q[0]) and bool(torch.isnan(e).all())
+    m, e = qmc.replicate_mean(Q[:, :4])   # rows strided by 10
+    mo, eo = O.replicate_estimate(Q[:, :4].cpu().numpy())
+    np.testing.assert_allclose(m.cpu().numpy(), mo, rtol=1e-15)
+    np.testing.assert_allclose(e.cpu().numpy(), eo, rtol=1e-13)
+    qmc._abi.qmc_replicate_mean(Q, 3, 0, 0, Q)   # t = 0: no-op
+    with pytest.raises(qmc.QMCError):
+        qmc._abi.qmc_replicate_mean(Q, 0, 4, 4, Q)
+    with pytest.raises(qmc.QMCError):
+        qmc._abi.qmc_replicate_mean(Q, 2, 4, 3, Q)
 
 
 # ------------------------------------------------------------------ CBC (NEXT #4)

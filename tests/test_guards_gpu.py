@@ -104,3 +104,45 @@ def test_report_build_flags(abi):
     f = abi.qmc_build_flags()
     print(f"libqmc build flags = {f} ({'checked' if f & 1 else 'product'} build)")
     assert f in (0, 1, 2, 3)
+
+
+def test_plan_shift_guards(abi):
+    """qmc_plan_shift writes only its own shift workspace (ζ, φ(x_0), W):
+    the base plan's workspace is bitwise unchanged and the shift workspace's
+    guards intact; bad requests are rejected with their status."""
+    import torch
+    w = W.custom_lattice(65537, 64, 6, W.PHI_INVNORM_MID, seed=11)
+    nplan = abi.qmc_plan_workspace_size(abi.QMC_FAMILY_LATTICE, w.N, w.s)
+    pbuf, pws = _guarded(nplan)
+    st = torch.cuda.current_stream().cuda_stream
+    h = abi.qmc_plan_create(w.N, w.s, w.z, w.phi, pws, nplan, st)
+    hs = None
+    try:
+        before = pbuf.clone()
+        nsh = abi.qmc_shift_workspace_size(h)
+        assert nsh < nplan
+        sbuf, sws = _guarded(nsh)
+        hs = abi.qmc_plan_shift(h, 0.3, sws, nsh, st)
+        torch.cuda.synchronize()
+        assert torch.equal(pbuf, before)
+        assert _guards_intact(sbuf, nsh)
+        with pytest.raises(abi.QMCError) as e:
+            abi.qmc_plan_shift(h, 1.0, sws, nsh, st)
+        assert e.value.code == -5
+        with pytest.raises(abi.QMCError) as e:
+            abi.qmc_plan_shift(h, 0.3, sws, nsh - 8, st)
+        assert e.value.code == -8
+        D, p = 8, 285
+        npoly = abi.qmc_plan_workspace_size(abi.QMC_FAMILY_POLY, D, 3)
+        ppoly = torch.empty(npoly, dtype=torch.uint8, device="cuda")
+        hp = abi.qmc_plan_create_poly(D, p, 3, [1, 2, 3], W.PHI_SHIFT_HALF, ppoly, npoly, st)
+        try:
+            with pytest.raises(abi.QMCError) as e:
+                abi.qmc_plan_shift(hp, 0.3, sws, nsh, st)
+            assert e.value.code == abi.QMC_EUNSUPPORTED
+        finally:
+            abi.qmc_plan_destroy(hp)
+    finally:
+        if hs is not None:
+            abi.qmc_plan_destroy(hs)
+        abi.qmc_plan_destroy(h)

@@ -369,6 +369,29 @@ def test_config3_means_closed_form():
     np.testing.assert_allclose(means, want, rtol=0, atol=1e-13)
 
 
+# ---------------------------------------------------------------- randomised QMC (R28)
+def test_replicate_estimate_pins():
+    """The replicate mean and standard error against the statistics module
+    (fmean, sample stdev / sqrt(R)), the R = 2 closed form |Q0 - Q1| / 2,
+    equal replicates (error 0) and R = 1 (NaN)."""
+    rng = np.random.default_rng(28)
+    Q = rng.standard_normal((7, 5))
+    mean, err = O.replicate_estimate(Q)
+    for k in range(5):
+        col = [float(v) for v in Q[:, k]]
+        assert math.isclose(mean[k], statistics.fmean(col), rel_tol=1e-15)
+        assert math.isclose(err[k], statistics.stdev(col) / math.sqrt(7), rel_tol=1e-14)
+    m2, e2 = O.replicate_estimate(Q[:2])
+    np.testing.assert_allclose(e2, np.abs(Q[0] - Q[1]) / 2, rtol=1e-15)
+    np.testing.assert_allclose(m2, (Q[0] + Q[1]) / 2, rtol=1e-15)
+    m3, e3 = O.replicate_estimate(np.tile(Q[:1], (4, 1)))
+    np.testing.assert_array_equal(m3, Q[0])
+    np.testing.assert_array_equal(e3, np.zeros(5))
+    m1, e1 = O.replicate_estimate(Q[:1])
+    np.testing.assert_array_equal(m1, Q[0])
+    assert np.all(np.isnan(e1))
+
+
 # ---------------------------------------------------------------- the fused reductions
 def test_rowmean_relu_pins():
     """Config 2's scalar Q = (1/N) Σ_n max(0, (1/t) Σ_k X[n,k]) (reading R10):
