@@ -40,25 +40,45 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
 
 
+def _compile_link(out: str, flags: list) -> str:
+    """Each translation unit compiled on its own thread (no device code is
+    shared between them), then one shared-library link; returns nvcc's
+    stderr."""
+    import concurrent.futures as cf
+    import tempfile
+
+    tmp = tempfile.mkdtemp(prefix="qmc_build_")
+    objs = [os.path.join(tmp, f + ".o") for f in SOURCES]
+    cflags = [f for f in NVCC_FLAGS if f != "-shared"] + flags
+    cmds = [[_nvcc(), *cflags, "-c", "-o", o, os.path.join(CSRC, f)] for f, o in zip(SOURCES, objs)]
+    with cf.ThreadPoolExecutor(len(cmds)) as ex:
+        results = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    errs = "".join(r.stdout + r.stderr for r in results)
+    if any(r.returncode != 0 for r in results):
+        raise RuntimeError("nvcc failed:\n" + errs)
+    res = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", out, *objs],
+                         capture_output=True, text=True)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(tmp)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc link failed:\n" + res.stdout + res.stderr)
+    return errs
+
+
 def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list | None = None) -> str:
     """Compile libqmc.so (or, with `out`, a variant build with `extra` flags)."""
     if out is not None:
-        cmd = [_nvcc(), *NVCC_FLAGS, *(extra or []), "-o", out] + [os.path.join(CSRC, f) for f in SOURCES]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        _compile_link(os.path.abspath(out), list(extra or []))
         return out
     if not force and not _stale():
         return LIB
-    cmd = [_nvcc(), *NVCC_FLAGS, *os.environ.get("QMC_NVCC_EXTRA", "").split()]
+    flags = os.environ.get("QMC_NVCC_EXTRA", "").split()
     if verbose:
-        cmd += ["-Xptxas", "-v"]
-    cmd += ["-o", LIB + ".tmp"] + [os.path.join(CSRC, f) for f in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
+        flags += ["-Xptxas", "-v"]
+    errs = _compile_link(LIB + ".tmp", flags)
     if verbose:
-        sys.stderr.write(res.stderr)
+        sys.stderr.write(errs)
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

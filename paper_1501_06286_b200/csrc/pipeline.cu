@@ -9,10 +9,12 @@
 //
 //   K0 k_pack*     a of the batch in the K1 slot order (or the dense a', then
 //                  the first DFT dimension by k_dense_cols*)
-//   K1 k_rows16    T'[f1,e2] = Σ_{j: e_j ≡ e2} a_j ω_L^{e'_j f1}   (scatter a' = P a
-//                  fused with the first FFT dimension, PAPER.md:355-357;
-//                  e' = e - e mod NT, the thread part ω_L^{t f1} of the
-//                  four-step twiddle folded into the row FFT's first stage)
+//   K1 k_rows16    T'[f1,e2] = ω_L^{e2 f1} Σ_{j: e_j ≡ e2} a_j ω_{L1}^{e1_j f1}
+//                  (scatter a' = P a fused with the first FFT dimension,
+//                  PAPER.md:355-357; e1_j = e_j div L2; the bucket's common
+//                  four-step twiddle ω_L^{e2 f1} applied to the summed row:
+//                  ω_{16 L1}^{q f1} per register, ω_L^{t f1} in the row FFT's
+//                  first stage)
 //                  → FFT_L2 → ·W → IFFT_L2 → ·conj(ω_L^{e2 f1}) → U[p][f1][e2]
 //                  (fft.cuh dif_fwd / dif_inv, registers + shared memory)
 //   K2 k_cols_*    IFFT_L1 over f1 → B'[L2 e1 + e2]; the reordered row
@@ -266,6 +268,19 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
 }
+// U is read exactly once by the column pass: with QMC_U_EF its cp.async
+// loads carry an L2 evict-first policy (diagnostic build flag)
+__device__ __forceinline__ void cp_async16_u(void* smem, const void* gmem) {
+#ifdef QMC_U_EF
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "l"(pol)
+               : "memory");
+#else
+  cp_async16(smem, gmem);
+#endif
+}
 __device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gmem) : "memory");
@@ -274,6 +289,12 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 // slots of the direct scatter in flight per thread (loop unroll)
+#ifndef QMC_K1_PF
+#define QMC_K1_PF 0
+#endif
+#ifndef QMC_W_PF
+#define QMC_W_PF 0
+#endif
 #ifndef QMC_K1_UNROLL
 #define QMC_K1_UNROLL 4
 #endif
@@ -282,11 +303,15 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define QMC_UNROLL(n) QMC_UNROLL_(n)
 
 // shared memory of K1: the padded row with its padding and overflow slots
-// (k1_row_slots); staged plans add the staging of CH slots (a, twiddle, code:
-// 36 B each, CH a multiple of 4) and its mbarrier
+// (k1_row_slots), the item's 16 register twiddles ω_{16 L1}^{q f1}
+// (kK1Aux slots); staged plans add the staging of CH slots (a, twiddle,
+// code: 36 B each, CH a multiple of 4) and its mbarrier, the others the
+// item's scatter twiddles ω_{L1}^{e1 f1} in kTwRep replicas (k1_item)
+constexpr int kTwRep = 8;
 template <int L2>
-__host__ __device__ constexpr size_t rows_smem(int CH) {
-  return size_t(k1_row_slots(L2, QMC_ROW_E)) * 16 + (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16 : 0);
+__host__ __device__ constexpr size_t rows_smem(int CH, int L1) {
+  return size_t(k1_row_slots(L2, QMC_ROW_E) + kK1Aux) * 16 +
+         (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16 : size_t(L1) * kTwRep * 16);
 }
 
 struct K1Args {
@@ -323,7 +348,7 @@ struct K1Stage {
   int32_t* stE;   // staging: codes
   uint64_t* bar;  // staging complete (one phase per item)
   __device__ K1Stage(double2* base, int CH)
-      : stA(base + k1_row_slots(L2, QMC_ROW_E)),
+      : stA(base + k1_row_slots(L2, QMC_ROW_E) + kK1Aux),
         stW(stA + CH),
         stE(reinterpret_cast<int32_t*>(stW + CH)),
         bar(reinterpret_cast<uint64_t*>(stE + CH)) {}
@@ -376,7 +401,8 @@ __device__ __forceinline__ void k1_issue(const K1Args& a, const K1Stage<L2>& sg,
 // per batch, twj and e2q per plan) into registers, several slots in flight
 // per thread, so no staging buffer, copy or extra barrier is needed.
 template <int L2>
-__device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, int next, unsigned& phase) {
+__device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, int next, unsigned& phase,
+                                        unsigned occm) {
   constexpr int E = QMC_ROW_E;
   constexpr int NT = L2 / E;
   const int tid = threadIdx.x;
@@ -415,13 +441,27 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
     __syncthreads();  // staging consumed
     if (tid == 0 && next >= 0) k1_issue<L2>(a, sg, next);  // overlaps this item's FFTs
   }
+  // the item's scatter twiddles TWs[e1·kTwRep + r] = ω_{L1}^{(e1 f1) mod L1},
+  // replica r read by the lanes l ≡ r (mod 8): a quarter-warp's 16-byte loads
+  // fall in distinct bank groups whatever the e1 (the previous item's reads
+  // ended at its row barrier)
+  double2* TWs = S + k1_row_slots(L2, E) + kK1Aux;
+  if (nch > 0 && a.bal)
+    for (int i = tid; i < L1 * kTwRep; i += NT) TWs[i] = __ldg(&a.tw1[((i / kTwRep) * f1) % L1]);
+  // the item's register twiddles T16[q] = ω_{16 L1}^{q f1}, read as
+  // broadcasts after the row barrier; two buffers by item parity (the
+  // previous item may still read its own; the one before ended at the
+  // previous row barrier)
+  const double2* T16 = S + k1_row_slots(L2, E) + 16 * ((item / int(gridDim.x)) & 1);
+  for (int q = tid; q < 16; q += NT) const_cast<double2*>(T16)[q] = __ldg(&a.tw16[(q * f1) % (16 * L1)]);  // NT >= 2
   for (int c = 0; c < nch; ++c) {
     const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
     // every use of S by the previous item (or the previous chunk's fix-ups)
     // is done before this chunk's stores
     __syncthreads();
     // scatter a' = P a fused with the first DFT dimension:
-    //   T'[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_L^{(e'_j·f1) mod L}
+    //   T'[f1, e2] = Σ_{j: e_j ≡ e2 (mod L2)} a_j ω_{L1}^{(e1_j·f1) mod L1}
+    // (the bucket's common factor ω_L^{e2 f1} is applied to the row below)
     // (S holds the previous item's data elsewhere: only nonempty buckets are
     // read back, by the occupancy mask)
     if (a.bal) {
@@ -430,10 +470,18 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       // stored after every entry (the last store of a piece is its total)
       const int nreg = __ldg(&a.k1c[nch + 1 + c]);
       double2 acc = make_double2(0.0, 0.0);
+      const double2* tws = TWs + (tid & (kTwRep - 1));
       QMC_UNROLL(QMC_K1_UNROLL)
       for (int i = q0 + tid; i < q0 + nreg; i += NT) {
+#if QMC_K1_PF > 0
+        // the slot QMC_K1_PF rounds ahead into L1 (no register held)
+        if (i + QMC_K1_PF * NT < q0 + nreg) {
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(ap + i + QMC_K1_PF * NT));
+          asm volatile("prefetch.global.L1 [%0];" ::"l"(a.e2q + i + QMC_K1_PF * NT));
+        }
+#endif
         const int cd = __ldg(&a.e2q[i]);
-        const double2 pr = cmul(__ldg(&ap[i]), __ldg(&tp[i]));
+        const double2 pr = cmul(__ldg(&ap[i]), tws[((cd >> kK1E1Shift) & 511) * kTwRep]);
         acc = (cd & kK1First) ? pr : cadd(acc, pr);
         QMC_CHECK_IDX(i, a.S1);
         QMC_CHECK_IDX(padE<E>(cd & 0x3fff), k1_row_slots(L2, E));
@@ -473,23 +521,26 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
 #pragma unroll
     for (int q = 0; q < E; ++q) v[q] = Tr[q * NT];
   } else {
-    // nonempty buckets only (the rest of S is stale); NT is a multiple of 32
+    // nonempty buckets only (the rest of S is stale): bit q of occm says
+    // whether bucket t + NT q has an entry (k_rows16 reads the bitmap once)
     const int t0 = tid_fresh();
-    const double2* Sb = S + padE<E>(t0);
-    const uint32_t* ob = a.occ + (t0 >> 5);
 #pragma unroll
-    for (int q = 0; q < E; ++q) {
-      if constexpr (NT % 32 == 0 && NT % E == 0)
-        v[q] = (__ldg(&ob[q * (NT / 32)]) >> (t0 & 31)) & 1u ? Sb[q * (NT + NT / E)] : make_double2(0.0, 0.0);
-      else {
-        const int e2 = t0 + q * NT;
-        v[q] = (__ldg(&a.occ[e2 >> 5]) >> (e2 & 31)) & 1u ? S[padE<E>(e2)] : make_double2(0.0, 0.0);
-      }
-    }
+    for (int q = 0; q < E; ++q)
+      v[q] = (occm >> q) & 1u ? S[padE<E>(t0 + q * NT)] : make_double2(0.0, 0.0);
+#if QMC_W_PF
+    // the item's spectrum row into L1 ahead of dif_fwd's product (no register held)
+#pragma unroll
+    for (int q = 0; q < E; ++q)
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(a.W + int64_t(f1) * L2 + t0 + q * NT));
+#endif
+    // the bucket's common factor ω_L^{e2 f1}, e2 = t + NT q: the register
+    // part ω_L^{NT q f1} = ω_{16 L1}^{q f1} here, the thread part below
+#pragma unroll
+    for (int q = 1; q < E; ++q) v[q] = cmul(v[q], T16[q]);
   }
   // b = ω_L^{t·f1}: the thread's part of the four-step twiddle ω_L^{e2·f1}
-  // (e2 = t + NT q), folded into the first row-FFT stage; the scatter
-  // twiddles (twj) carry the rest, ω_{16 L1}^{q f1} (plan.cu k_twj)
+  // (e2 = t + NT q), folded into the first row-FFT stage (k_dense_cols*
+  // applied the rest to dense rows, the loop above to scattered ones)
   const int t0 = tid_fresh();
   double2 b;
   {
@@ -511,25 +562,24 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
   // the rest of conj(ω_L^{e2 f1}) (the column pass's twiddle): conj(ω_{16 L1}^{q f1})
   {
     static_assert(E == 16, "K1's row FFT holds 16 points per thread");
-    const int M16 = 16 * L1;
-    int y = 0;
 #pragma unroll
-    for (int q = 1; q < E; ++q) {
-      y += f1;  // (q·f1) mod 16 L1
-      if (y >= M16) y -= M16;
-      v[q] = cmulc(v[q], __ldg(&a.tw16[y]));
-    }
+    for (int q = 1; q < E; ++q) v[q] = cmulc(v[q], T16[q]);
   }
   QMC_TS(4);
   // U[p] in column blocks of kUB: [e2 / kUB][f1][e2 % kUB], so that K2 reads
-  // whole sectors of kUB·16 bytes per f1
+  // whole sectors of kUB·16 bytes per f1; evict-first stores (U exceeds L2
+  // on the large configs: the plan's tables and the batch's a stay resident)
   double2* Up = a.U + int64_t(p) * a.L + int64_t(f1) * kUB;
   QMC_CHECK_IDX(p, a.np);
 #pragma unroll
   for (int q = 0; q < E; ++q) {
     const int e2 = tid + q * NT;
     QMC_CHECK_IDX(int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB) + int64_t(f1) * kUB, a.L);
+#ifndef QMC_U_PLAIN_STORES
+    stcs2(reinterpret_cast<double*>(Up + int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)), v[q]);
+#else
     Up[int64_t(e2 / kUB) * (L1 * kUB) + (e2 % kUB)] = v[q];
+#endif
   }
   QMC_TS(5);
 }
@@ -546,8 +596,18 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
     __syncthreads();
     if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sg, blockIdx.x);
   }
+  // the thread's nonempty buckets e2 = t + NT q (a plan constant): bit q
+  unsigned occm = 0;
+  if (!a.dense) {
+    constexpr int NT = L2 / QMC_ROW_E;
+#pragma unroll
+    for (int q = 0; q < QMC_ROW_E; ++q) {
+      const int e2 = int(threadIdx.x) + q * NT;
+      occm |= ((__ldg(&a.occ[e2 >> 5]) >> (e2 & 31)) & 1u) << q;
+    }
+  }
   for (int item = blockIdx.x; item < nitems; item += gridDim.x)
-    k1_item<L2>(a, smem, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1, phase);
+    k1_item<L2>(a, smem, item, item + int(gridDim.x) < nitems ? item + int(gridDim.x) : -1, phase, occm);
 }
 
 // ---------------------------------------------------------------- one-row plans
@@ -1169,7 +1229,7 @@ __device__ __forceinline__ void k2_issue(const K2Args& a, int tile, double2* dst
   const int bx = tile % a.ntx, g = tile / a.ntx;
   for (int i = threadIdx.x; i < PG * NB * BLK; i += NT) {
     const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
-    cp_async16(dst + pp * PSTR + o, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * (NB * BLK) + o);
+    cp_async16_u(dst + pp * PSTR + o, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * (NB * BLK) + o);
   }
   for (int i = threadIdx.x; i < L1 * CB; i += NT) {
     const int e1 = i / CB, cc = i - e1 * CB;
@@ -1303,7 +1363,7 @@ __device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* d
   const int bx = tile % a.ntx, g = tile / a.ntx;
   for (int i = threadIdx.x; i < kP2PG * BLK; i += kP2Thr) {
     const int pp = i / BLK, o = i - pp * BLK;
-    cp_async16(dst + pp * PSTR + o, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK + o);
+    cp_async16_u(dst + pp * PSTR + o, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK + o);
   }
   for (int i = threadIdx.x; i < L1 * kUB; i += kP2Thr) {
     const int e1 = i / kUB, cc = i - e1 * kUB;
@@ -1570,7 +1630,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
 template <int L2>
 static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                        double* colsum, cudaStream_t st) {
-  const size_t smem = rows_smem<L2>(pl->k1_stage);
+  const size_t smem = rows_smem<L2>(pl->k1_stage, int(pl->sp.L1));
   auto kern = k_rows16<L2>;
   static int nsm = 0;
   static size_t last_smem = 0;  // attribute and occupancy of the last shared-memory size (per instantiation)

@@ -386,11 +386,8 @@ __global__ void k_twiddles(double2* __restrict__ tw, int64_t n, int64_t count) {
   tw[k] = make_double2(cv, -sv);
 }
 
-// twj[f1·s + q] = ω_L^{(e_j·f1) mod L}, j = bent[q].x: the twiddle of the
-// q-th entry (bucket order) in row f1 of the scatter fused with the first DFT
-// dimension (K1)
-// twj[f1·S1 + q] = ω_L^{(e_j·f1) mod L} for the column j = jq[q] of slot q of
-// the K1 order (0 for padding slots)
+// twj[f1·S1 + q] = ω_{L1}^{(e1_j·f1) mod L1}, e1_j = e_j div L2, for the
+// column j = jq[q] of slot q of the K1 order (0 for padding slots)
 __global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict__ e, int64_t S1, int64_t L, int L1,
                       int NT, double2* __restrict__ twj) {
   const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -401,12 +398,15 @@ __global__ void k_twj(const int32_t* __restrict__ jq, const int32_t* __restrict_
     twj[i] = make_double2(0.0, 0.0);
     return;
   }
-  // ω_L^{e' f1} with e' = e_j - e_j mod NT: the thread part ω_L^{(e_j mod NT) f1}
-  // of the four-step twiddle is folded into K1's first row-FFT stage
-  const int64_t ej = e[j];
-  const int64_t x = ((ej - ej % NT) * f1) % L;
+  // ω_L^{L2 e1 f1} = ω_{L1}^{(e1 f1) mod L1}, e1 = e_j div L2: the part of
+  // ω_L^{e_j f1} that differs between the entries of a bucket; the bucket's
+  // common factor ω_L^{e2 f1} is applied by K1 to the summed row
+  // (ω_{16 L1}^{q f1} per register, ω_L^{t f1} in the first row-FFT stage)
+  const int64_t L2 = L / L1;
+  const int64_t x = ((e[j] / L2) * f1) % L1;
+  (void)NT;
   double sv, cv;
-  sincospi(2.0 * double(x) / double(L), &sv, &cv);
+  sincospi(2.0 * double(x) / double(L1), &sv, &cv);
   twj[i] = make_double2(cv, -sv);
 }
 
@@ -433,6 +433,8 @@ static bool k1_balanced_order(const std::vector<int32_t>& hb, const std::vector<
     int q0, len, v;
   };
   using Load = std::pair<int, int>;  // (entries, thread)
+  for (size_t q = 0; q < hbent.size(); ++q)  // e1 must fit the code field (L1 <= 512)
+    if (hbent[q].y / L2 >= 512) return false;
   for (int64_t target = budget; target >= NT; target = target * 3 / 4) {
     jq.clear();
     code.clear();
@@ -489,7 +491,8 @@ static bool k1_balanced_order(const std::vector<int32_t>& hb, const std::vector<
           for (int k = 0; k < p.len; ++k, ++i) {
             const size_t slot = base + size_t(i) * NT + t;
             jq[slot] = hbent[p.q0 + k].x;
-            code[slot] = p.v | (k == 0 ? kK1First : 0);
+            // e1 = e_j div L2 selects the scatter twiddle ω_{L1}^{e1 f1} (K1)
+            code[slot] = p.v | (k == 0 ? kK1First : 0) | int((hbent[p.q0 + k].y / L2) << kK1E1Shift);
           }
       }
       cr.push_back(int(nreg));
@@ -818,7 +821,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       // the row kernel's residency): staged and prefetched during the
       // previous item's FFTs; otherwise K1 reads its input from global memory
       const int64_t limit = sp.L2 >= 8192 ? 232448 : 115712;
-      const int64_t room = (limit - k1_row_slots(sp.L2, QMC_ROW_E) * 16 - 16 - 64) / 36 / 4 * 4;
+      const int64_t room = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux) * 16 - 16 - 64) / 36 / 4 * 4;
       if (cr.size() == 1 && chmax <= room) pl->k1_stage = int((chmax + 3) / 4 * 4);
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     } else {

@@ -92,7 +92,13 @@ inline int64_t k1_s1max(int64_t s, int64_t L2, int64_t L) {
 // fix-up records (after a chunk's slots) are e2 | o0 << 14 | count << 20
 // (S[e2] += S[L2+1+o0] + ... in order).
 constexpr int kK1First = 1 << 14;
+// regular slot codes also carry e1 = e_j div L2 (< 512) from bit 15: the
+// index of the scatter twiddle ω_{L1}^{e1 f1}
+constexpr int kK1E1Shift = 15;
 constexpr int kK1Ovf = 64;
+// K1 shared memory after the row: two buffers of the item's 16 register
+// twiddles (pipeline.cu k1_item)
+constexpr int kK1Aux = 32;
 // shared-memory row slots of K1: padE(v) for every v <= L2 + kK1Ovf
 __host__ __device__ inline constexpr int64_t k1_row_slots(int64_t L2, int E) {
   return L2 + kK1Ovf + 1 + (L2 + kK1Ovf) / E + 1;
@@ -169,7 +175,7 @@ struct qmc_plan {
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
   double2* d_tw16;   // [16 L1] ω_{16 L1}^k (K1: the column-register part of ω_L^{e2 f1})
-  double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_L^{(e'_j·f1) mod L}, e' = e - e mod (L2/16), j = jq[q] (K1 scatter
+  double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_{L1}^{(e1_j·f1) mod L1}, e1 = e div L2, j = jq[q] (K1 scatter
                      //        twiddles in the K1 order; 0 for padding slots)
   int32_t* d_jq;     // [S1]  column j of slot q of the K1 order (-1: padding)
   int32_t* d_k1c;    // [k1_nch+1] chunk starts, then [k1_nch] regular-round slots per chunk
