@@ -302,15 +302,19 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #define QMC_UNROLL_(n) QMC_PRAGMA_(unroll n)
 #define QMC_UNROLL(n) QMC_UNROLL_(n)
 
-// shared memory of K1: the padded row with its padding and overflow slots
-// (k1_row_slots), the item's 16 register twiddles ω_{16 L1}^{q f1}
-// (kK1Aux slots); staged plans add the staging of CH slots (a, twiddle,
-// code: 36 B each, CH a multiple of 4) and its mbarrier, the others the
-// item's scatter twiddles ω_{L1}^{e1 f1} in kTwRep replicas (k1_item)
+// shared memory of K1 (16-byte slots): the padded row with its padding and
+// overflow slots (k1_row_slots); then kK1Aux slots — two buffers of the
+// item's 16 register twiddles T16[q] = ω_{16 L1}^{q f1}, the constant
+// Tlo[k] = ω_{16 L1}^k (k < 16) — and the constant T1s[k] = ω_{L1}^k (L1
+// slots); then, for staged plans, the staging of CH slots (a, twiddle, code:
+// 36 B each, CH a multiple of 4) and its mbarrier, for the others the item's
+// scatter twiddles ω_{L1}^{e1 f1} in kTwRep replicas (k1_item)
 constexpr int kTwRep = 8;
 template <int L2>
+__host__ __device__ constexpr int k1_aux_base() { return int(k1_row_slots(L2, QMC_ROW_E)); }
+template <int L2>
 __host__ __device__ constexpr size_t rows_smem(int CH, int L1) {
-  return size_t(k1_row_slots(L2, QMC_ROW_E) + kK1Aux) * 16 +
+  return size_t(k1_aux_base<L2>() + kK1Aux + L1) * 16 +
          (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16 : size_t(L1) * kTwRep * 16);
 }
 
@@ -347,8 +351,8 @@ struct K1Stage {
   double2* stW;   // staging: twiddles
   int32_t* stE;   // staging: codes
   uint64_t* bar;  // staging complete (one phase per item)
-  __device__ K1Stage(double2* base, int CH)
-      : stA(base + k1_row_slots(L2, QMC_ROW_E) + kK1Aux),
+  __device__ K1Stage(double2* base, int CH, int L1)
+      : stA(base + k1_aux_base<L2>() + kK1Aux + L1),
         stW(stA + CH),
         stE(reinterpret_cast<int32_t*>(stW + CH)),
         bar(reinterpret_cast<uint64_t*>(stE + CH)) {}
@@ -413,7 +417,7 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
   const double2* tp = a.twj + int64_t(f1) * a.S1;
   QMC_TS(0);
   if (a.CH > 0) {  // staged mode: this item's chunk was copied during the previous item
-    const K1Stage<L2> sg(S, a.CH);
+    const K1Stage<L2> sg(S, a.CH, a.L1);
     mbar_wait(sg.bar, phase);
     phase ^= 1u;
     __syncthreads();  // every use of S by the previous item is done
@@ -445,15 +449,21 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
   // replica r read by the lanes l ≡ r (mod 8): a quarter-warp's 16-byte loads
   // fall in distinct bank groups whatever the e1 (the previous item's reads
   // ended at its row barrier)
-  double2* TWs = S + k1_row_slots(L2, E) + kK1Aux;
+  // (from the constant tables: shared memory only, no global latency before
+  // the scatter's barrier)
+  const double2* T1s = S + k1_aux_base<L2>() + kK1Aux;
+  double2* TWs = const_cast<double2*>(T1s) + L1;
   if (nch > 0 && a.bal)
-    for (int i = tid; i < L1 * kTwRep; i += NT) TWs[i] = __ldg(&a.tw1[((i / kTwRep) * f1) % L1]);
-  // the item's register twiddles T16[q] = ω_{16 L1}^{q f1}, read as
-  // broadcasts after the row barrier; two buffers by item parity (the
-  // previous item may still read its own; the one before ended at the
-  // previous row barrier)
-  const double2* T16 = S + k1_row_slots(L2, E) + 16 * ((item / int(gridDim.x)) & 1);
-  for (int q = tid; q < 16; q += NT) const_cast<double2*>(T16)[q] = __ldg(&a.tw16[(q * f1) % (16 * L1)]);  // NT >= 2
+    for (int i = tid; i < L1 * kTwRep; i += NT) TWs[i] = T1s[((i / kTwRep) * f1) % L1];
+  // the item's register twiddles T16[q] = ω_{16 L1}^{x} = Tlo[x mod 16]·
+  // ω_{L1}^{x div 16}, x = (q f1) mod 16 L1, read as broadcasts after the row
+  // barrier; two buffers by item parity (the previous item may still read
+  // its own; the one before ended at the previous row barrier)
+  const double2* T16 = S + k1_aux_base<L2>() + 16 * ((item / int(gridDim.x)) & 1);
+  for (int q = tid; q < 16; q += NT) {  // NT >= 2
+    const int x = (q * f1) % (16 * L1);
+    const_cast<double2*>(T16)[q] = cmul(S[k1_aux_base<L2>() + 32 + (x & 15)], T1s[x >> 4]);
+  }
   for (int c = 0; c < nch; ++c) {
     const int q0 = __ldg(&a.k1c[c]), n = __ldg(&a.k1c[c + 1]) - q0;
     // every use of S by the previous item (or the previous chunk's fix-ups)
@@ -591,10 +601,17 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
   const int nitems = a.L1 * a.np;
   unsigned phase = 0;
   if (a.CH > 0) {
-    const K1Stage<L2> sg(smem, a.CH);
+    const K1Stage<L2> sg(smem, a.CH, a.L1);
     if (threadIdx.x == 0) mbar_init(sg.bar, 1);
     __syncthreads();
     if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sg, blockIdx.x);
+  }
+  // the constant twiddle tables after the row (rows_smem): Tlo, T1s
+  {
+    double2* aux = smem + k1_aux_base<L2>();
+    for (int i = threadIdx.x; i < 16 + a.L1; i += blockDim.x)
+      aux[32 + i] = i < 16 ? __ldg(&a.tw16[i]) : __ldg(&a.tw1[i - 16]);
+    __syncthreads();
   }
   // the thread's nonempty buckets e2 = t + NT q (a plan constant): bit q
   unsigned occm = 0;

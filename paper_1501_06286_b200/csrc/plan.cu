@@ -821,7 +821,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       // the row kernel's residency): staged and prefetched during the
       // previous item's FFTs; otherwise K1 reads its input from global memory
       const int64_t limit = sp.L2 >= 8192 ? 232448 : 115712;
-      const int64_t room = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux) * 16 - 16 - 64) / 36 / 4 * 4;
+      const int64_t room = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux + sp.L1) * 16 - 16 - 64) / 36 / 4 * 4;
       if (cr.size() == 1 && chmax <= room) pl->k1_stage = int((chmax + 3) / 4 * 4);
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     } else {

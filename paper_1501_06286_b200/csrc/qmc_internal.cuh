@@ -97,8 +97,9 @@ constexpr int kK1First = 1 << 14;
 constexpr int kK1E1Shift = 15;
 constexpr int kK1Ovf = 64;
 // K1 shared memory after the row: two buffers of the item's 16 register
-// twiddles (pipeline.cu k1_item)
-constexpr int kK1Aux = 32;
+// twiddles and 16 constant ones, before the L1 constant column twiddles
+// (pipeline.cu rows_smem)
+constexpr int kK1Aux = 48;
 // shared-memory row slots of K1: padE(v) for every v <= L2 + kK1Ovf
 __host__ __device__ inline constexpr int64_t k1_row_slots(int64_t L2, int E) {
   return L2 + kK1Ovf + 1 + (L2 + kK1Ovf) / E + 1;
