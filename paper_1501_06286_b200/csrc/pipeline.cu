@@ -46,8 +46,6 @@
 
 namespace qmc {
 
-// column-block width of K1's output U: U[p] is [e2 / kUB][f1][e2 % kUB]
-constexpr int kUB = 4;
 constexpr int kColThreads = 256;  // K2 CTA size
 
 // X is written once and never read back by the library: evict-first stores
@@ -1235,6 +1233,7 @@ struct K2Args {
   EpiArgs E;
   double* __restrict__ part;
   int part_stride;
+  const int32_t* __restrict__ k2n;     // plan.cu k_k2rows: output rows in U column-block order
 };
 
 // stage tile (16 pairs × CB columns): U blocks into dst (pair pitch PSTR),
@@ -1359,8 +1358,9 @@ __global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
 
 // Persistent, software-pipelined two-stage K2 (L1 = R·M, R > 1; config 5:
 // 96 = 6·16): tile = (8 pairs, one U column block of kUB = 4 columns e2),
-// i.e. 8 contiguous runs of L1·kUB complex, staged by cp.async one tile
-// ahead with its output row indices.  Stage A, item (p, c, r): the M values
+// i.e. 8 contiguous runs of L1·kUB complex, staged one tile ahead with its
+// output row indices (the plan's k2n run) by bulk async copies (one thread,
+// an mbarrier per stage).  Stage A, item (p, c, r): the M values
 // f1 = r + R·mm times conj(ω_L^{e2 f1}), M-point inverse DFT, times
 // ω_{L1}^{r k2}, written back in place (position r + R·k2).  Stage B, item
 // (p, c, k2): R-point inverse DFT over r → rows e1 = k2 + M·k1, stored as
@@ -1374,22 +1374,20 @@ __host__ __device__ constexpr size_t cols_pipe2_smem() {
   return size_t(kPipeStages) * (size_t(kP2PG) * pipe2_pair_stride<L1>() * 16 + size_t(L1) * kUB * 4);
 }
 
+// stage tile `tile` into dst (pair pitch PSTR) and its output rows into nd
+// by bulk async copies, one thread: PG contiguous U runs of L1·kUB complex
+// and the tile's run of the plan's row table (k2n), completing on bar
 template <int L1>
-__device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* dst, int* nd) {
+__device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* dst, int* nd, uint64_t* bar) {
   constexpr int BLK = L1 * kUB, PSTR = pipe2_pair_stride<L1>();
+  constexpr unsigned UB = BLK * 16, NB4 = L1 * kUB * 4;
   const int bx = tile % a.ntx, g = tile / a.ntx;
-  for (int i = threadIdx.x; i < kP2PG * BLK; i += kP2Thr) {
-    const int pp = i / BLK, o = i - pp * BLK;
-    cp_async16_u(dst + pp * PSTR + o, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK + o);
-  }
-  for (int i = threadIdx.x; i < L1 * kUB; i += kP2Thr) {
-    const int e1 = i / kUB, cc = i - e1 * kUB;
-    const int64_t ii = int64_t(a.L2) * e1 + bx * kUB + cc;
-    if (ii < a.m)
-      cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
-    else
-      nd[i] = -1;  // zero-padded correlation: not a row of X
-  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's reads before the async writes
+  mbar_expect_tx(bar, kP2PG * UB + NB4);
+#pragma unroll
+  for (int pp = 0; pp < kP2PG; ++pp)
+    bulk_g2s(dst + pp * PSTR, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK, UB, bar);
+  bulk_g2s(nd, a.k2n + int64_t(bx) * (L1 * kUB), NB4, bar);
 }
 
 template <int R, int M, int EP, bool PAD>
@@ -1480,9 +1478,14 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
   for (int i = threadIdx.x; i < L1; i += kP2Thr) tw1s[i] = __ldg(&a.tw1[i]);
   if (a.part)  // this CTA's slot row of column partials starts at zero
     for (int i = threadIdx.x; i < a.part_stride; i += kP2Thr) a.part[int64_t(blockIdx.x) * a.part_stride + i] = 0.0;
+  __shared__ uint64_t bars[kPipeStages];  // stage st complete (phase per use)
   const int ntiles = a.ntx * a.ngroups;
-  if (int(blockIdx.x) < ntiles) k2p2_issue<L1>(a, blockIdx.x, sm, nS);
-  cp_async_commit();
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && int(blockIdx.x) < ntiles) k2p2_issue<L1>(a, blockIdx.x, sm, nS, &bars[0]);
   double2 acc = make_double2(0.0, 0.0);
   int gcur = int(blockIdx.x) / a.ntx;
   int it = 0;
@@ -1490,7 +1493,7 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
     const int st = it & 1;
     // this tile's data has landed, and every thread is done with the
     // previous tile: its buffer takes the next tile (one barrier per tile)
-    cp_async_wait_all();
+    mbar_wait(&bars[st], unsigned(it >> 1) & 1u);
     __syncthreads();
     const int g = tile / a.ntx;
     if (a.part && g != gcur) {
@@ -1498,12 +1501,11 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
       gcur = g;
     }
     const int ahead = tile + gridDim.x;
-    if (ahead < ntiles) k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB));
-    cp_async_commit();
+    if (threadIdx.x == 0 && ahead < ntiles)
+      k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB), &bars[st ^ 1]);
     k2p2_tile<R, M, EP, PAD>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
   }
   if (a.part && int(blockIdx.x) < ntiles) k2p2_flush(a, gcur, acc, red);
-  cp_async_wait_all();
 }
 
 // out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
@@ -1713,6 +1715,7 @@ static K2Args k2_args(const qmc_plan* pl, const CallLayout& cl, const double2* U
   a.E = E;
   a.part = part;
   a.part_stride = cl.part_stride;
+  a.k2n = pl->d_k2n;
   return a;
 }
 

@@ -162,6 +162,7 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_twj = take(k1_dense_certain(s, sp) ? 0 : size_t(sp.L1) * size_t(s1) * 16);
   l.off_jq = take(size_t(s1) * 4);
   l.off_k1c = take(size_t(2 * s1 + 4) * 4);
+  l.off_k2n = take(sp.L1 > 1 ? size_t(sp.L) * 4 : 0);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
   l.total = o;
   return l;
@@ -384,6 +385,20 @@ __global__ void k_twiddles(double2* __restrict__ tw, int64_t n, int64_t count) {
   double sv, cv;
   sincospi(2.0 * double(k) / double(n), &sv, &cv);
   tw[k] = make_double2(cv, -sv);
+}
+
+// k2n[(bx·L1 + e1)·kUB + c] = conventional row n = P[(m - i) mod m] of the
+// reordered row i = L2·e1 + kUB·bx + c, -1 when i >= m
+// (zero-padded length): the output rows of a K2 tile (one U column block of
+// kUB columns e2) in the order of its U block, one contiguous run per tile
+__global__ void k_k2rows(const int32_t* __restrict__ P, int64_t m, int64_t L, int L1, int L2,
+                         int32_t* __restrict__ k2n) {
+  const int64_t idx = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= L) return;
+  const int64_t bx = idx / (int64_t(L1) * kUB), rem = idx % (int64_t(L1) * kUB);
+  const int64_t e1 = rem / kUB, c2 = kUB * bx + rem % kUB;
+  const int64_t i = int64_t(L2) * e1 + c2;
+  k2n[idx] = (c2 < L2 && i < m) ? P[i == 0 ? 0 : m - i] : -1;
 }
 
 // twj[f1·S1 + q] = ω_{L1}^{(e1_j·f1) mod L1}, e1_j = e_j div L2, for the
@@ -690,6 +705,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_tw16 = (double2*)(b + lay.off_tw16);
   pl->d_twj = (double2*)(b + lay.off_twj);
   pl->d_jq = (int32_t*)(b + lay.off_jq);
+  pl->d_k2n = sp.L1 > 1 ? (int32_t*)(b + lay.off_k2n) : nullptr;
   pl->d_k1c = (int32_t*)(b + lay.off_k1c);
   cudaStream_t st = pl->stream;
 
@@ -750,6 +766,10 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   QMC_PLAN_LAUNCHED();
   k_log_scatter<<<blocks(m, 256), 256, 0, st>>>(pl->d_P, m, pl->d_L);
   QMC_PLAN_LAUNCHED();
+  if (pl->d_k2n) {
+    k_k2rows<<<blocks(sp.L, 256), 256, 0, st>>>(pl->d_P, m, sp.L, int(sp.L1), int(sp.L2), pl->d_k2n);
+    QMC_PLAN_LAUNCHED();
+  }
   k_colmap<<<blocks(s, 256), 256, 0, st>>>(d_z, s, pl->d_L, pl->d_e);
   QMC_PLAN_LAUNCHED();
   QMC_PLAN_CHECK(cudaMemsetAsync(pl->d_bstart, 0, size_t(sp.L2 + 1) * 4, st) ? QMC_ECUDA : 0);

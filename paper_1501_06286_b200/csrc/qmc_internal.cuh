@@ -75,7 +75,7 @@ bool choose_split(int64_t m, int64_t s, Split* out);
 // and the create call.
 struct PlanLayout {
   size_t off_scal, off_P, off_L, off_R, off_e, off_bstart, off_bent, off_e2q, off_occ, off_cursor, off_zeta, off_W,
-      off_tw1, off_tw2, off_twL, off_tw16, off_twj, off_jq, off_k1c, off_tmp, total;
+      off_tw1, off_tw2, off_twL, off_tw16, off_twj, off_jq, off_k1c, off_k2n, off_tmp, total;
 };
 // K1 scatter-input order (plan.cu k1_balanced_order): tried when the
 // buckets are small enough to balance (s <= 8·L2), at most k1_s1max slots;
@@ -91,6 +91,8 @@ inline int64_t k1_s1max(int64_t s, int64_t L2, int64_t L) {
 // second and later pieces — and kK1First on the first entry of a piece;
 // fix-up records (after a chunk's slots) are e2 | o0 << 14 | count << 20
 // (S[e2] += S[L2+1+o0] + ... in order).
+// column-block width of K1's output U: U[p] is [e2 / kUB][f1][e2 % kUB]
+constexpr int kUB = 4;
 constexpr int kK1First = 1 << 14;
 // regular slot codes also carry e1 = e_j div L2 (< 512) from bit 15: the
 // index of the scatter twiddle ω_{L1}^{e1 f1}
@@ -176,6 +178,7 @@ struct qmc_plan {
   double2* d_tw2;    // [L2]  ω_{L2}^k
   double2* d_twL;    // [L2]  ω_L^k, k < L2
   double2* d_tw16;   // [16 L1] ω_{16 L1}^k (K1: the column-register part of ω_L^{e2 f1})
+  int32_t* d_k2n;    // [L] conventional row n of reordered row i = L2 e1 + 4 bx + c at [bx][e1][c] (-1: i >= m), K2's tiles
   double2* d_twj;    // [L1·S1] twj[f1·S1 + q] = ω_{L1}^{(e1_j·f1) mod L1}, e1 = e div L2, j = jq[q] (K1 scatter
                      //        twiddles in the K1 order; 0 for padding slots)
   int32_t* d_jq;     // [S1]  column j of slot q of the K1 order (-1: padding)
