@@ -1236,25 +1236,27 @@ struct K2Args {
   const int32_t* __restrict__ k2n;     // plan.cu k_k2rows: output rows in U column-block order
 };
 
-// stage tile (16 pairs × CB columns): U blocks into dst (pair pitch PSTR),
-// output row indices into nd[e1][c]; all 16·CB threads issue (no commit)
+// stage tile (16 pairs × CB columns = CB/kUB U column blocks) by bulk async
+// copies, one thread: per pair one contiguous run of the tile's U blocks into
+// dst (pair pitch PSTR), and the tile's run of the plan's row table k2n into
+// nd ([block][e1][c], k2_nidx), completing on bar
 template <int L1, int CB>
-__device__ __forceinline__ void k2_issue(const K2Args& a, int tile, double2* dst, int* nd) {
-  constexpr int PG = 16, NT = PG * CB, NB = CB / kUB, BLK = L1 * kUB;
+__device__ __forceinline__ void k2_issue(const K2Args& a, int tile, double2* dst, int* nd, uint64_t* bar) {
+  constexpr int PG = 16, NB = CB / kUB, BLK = L1 * kUB;
   constexpr int PSTR = pipe_pair_stride<L1, CB>();
+  constexpr unsigned UB = NB * BLK * 16, NB4 = L1 * CB * 4;
   const int bx = tile % a.ntx, g = tile / a.ntx;
-  for (int i = threadIdx.x; i < PG * NB * BLK; i += NT) {
-    const int pp = i / (NB * BLK), o = i - pp * (NB * BLK);
-    cp_async16_u(dst + pp * PSTR + o, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * (NB * BLK) + o);
-  }
-  for (int i = threadIdx.x; i < L1 * CB; i += NT) {
-    const int e1 = i / CB, cc = i - e1 * CB;
-    const int64_t ii = int64_t(a.L2) * e1 + bx * CB + cc;
-    if (ii < a.m)
-      cp_async4(nd + i, &a.P[ii == 0 ? 0 : a.m - ii]);
-    else
-      nd[i] = -1;  // zero-padded correlation: not a row of X
-  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's reads before the async writes
+  mbar_expect_tx(bar, PG * UB + NB4);
+#pragma unroll
+  for (int pp = 0; pp < PG; ++pp)
+    bulk_g2s(dst + pp * PSTR, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * (NB * BLK), UB, bar);
+  bulk_g2s(nd, a.k2n + int64_t(bx) * (L1 * CB), NB4, bar);
+}
+// index of the output row of (e1, column c of the tile) in the staged k2n run
+template <int L1>
+__device__ __forceinline__ int k2_nidx(int e1, int c) {
+  return (c / kUB) * (L1 * kUB) + e1 * kUB + (c % kUB);
 }
 
 // column pass + epilogue of one staged tile (16·CB threads, one column each)
@@ -1289,11 +1291,10 @@ __device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2
 #pragma unroll
   for (int f1 = 0; f1 < L1; ++f1) v[f1] = src[f1 * kUB];
   reg_dft<L1, +1>(v, a.tw1);  // (the twiddle conj(ω_L^{e2 f1}) was applied by K1)
-  const int* nr = nS + c;
   double r[L1];
 #pragma unroll
   for (int e1 = 0; e1 < L1; ++e1) {
-    const int n = nr[e1 * CB];  // -1: padding row (uniform over the 16 lanes of the row)
+    const int n = nS[k2_nidx<L1>(e1, c)];  // -1: padding row (uniform over the 16 lanes of the row)
     if (n >= 0) {
       emit_fast<EP>(E, v[e1], n, xk, acc, r[e1]);
     } else {
@@ -1303,7 +1304,7 @@ __device__ __forceinline__ void k2_tile(const K2Args& a, int tile, const double2
   if constexpr (EP == EPK_ROWSUM) {
     static_assert(EP != EPK_ROWSUM || L1 == 16, "row sums of the pipelined K2 need L1 = 16");
     const double sum = rowsum_butterfly16(r);
-    const int n = nr[(tid & 15) * CB];
+    const int n = nS[k2_nidx<L1>(tid & 15, c)];
     if (n >= 0) rowpart[n] = sum;
   } else {
     if (a.part) {  // per-column partial sums of this tile (lanes with equal p, then warps)
@@ -1332,28 +1333,31 @@ __global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
   extern __shared__ double2 sm[];
   int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
   __shared__ double2 red[NT / 32][16];
+  __shared__ uint64_t bars[kPipeStages];  // stage complete (phase per use)
   const int ntiles = a.ntx * a.ngroups;
+  if (threadIdx.x == 0) {
 #pragma unroll
-  for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
-    const int tl = blockIdx.x + s0 * gridDim.x;
-    if (tl < ntiles) k2_issue<L1, CB>(a, tl, sm + s0 * STAGE, nS + s0 * (L1 * CB));
-    cp_async_commit();
+    for (int s0 = 0; s0 < kPipeStages; ++s0) mbar_init(&bars[s0], 1);
+#pragma unroll
+    for (int s0 = 0; s0 < kPipeStages - 1; ++s0) {
+      const int tl = blockIdx.x + s0 * gridDim.x;
+      if (tl < ntiles) k2_issue<L1, CB>(a, tl, sm + s0 * STAGE, nS + s0 * (L1 * CB), &bars[s0]);
+    }
   }
+  __syncthreads();  // the barriers are initialised before anyone waits on them
   int it = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
     const int st = it % kPipeStages;
     const int ahead = tile + (kPipeStages - 1) * gridDim.x;
-    if (ahead < ntiles) {
+    if (threadIdx.x == 0 && ahead < ntiles) {  // its buffer was freed by the previous tile's last barrier
       const int sa = (it + kPipeStages - 1) % kPipeStages;
-      k2_issue<L1, CB>(a, ahead, sm + sa * STAGE, nS + sa * (L1 * CB));
+      k2_issue<L1, CB>(a, ahead, sm + sa * STAGE, nS + sa * (L1 * CB), &bars[sa]);
     }
-    cp_async_commit();
-    asm volatile("cp.async.wait_group %0;" ::"n"(kPipeStages - 1) : "memory");
+    mbar_wait(&bars[st], unsigned(it / kPipeStages) & 1u);
     __syncthreads();
     k2_tile<L1, EP, CB>(a, tile, sm + st * STAGE, nS + st * (L1 * CB), red);
     __syncthreads();  // stage st and red are reused
   }
-  cp_async_wait_all();
 }
 
 // Persistent, software-pipelined two-stage K2 (L1 = R·M, R > 1; config 5:

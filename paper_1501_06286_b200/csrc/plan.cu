@@ -162,7 +162,7 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp) {
   l.off_twj = take(k1_dense_certain(s, sp) ? 0 : size_t(sp.L1) * size_t(s1) * 16);
   l.off_jq = take(size_t(s1) * 4);
   l.off_k1c = take(size_t(2 * s1 + 4) * 4);
-  l.off_k2n = take(sp.L1 > 1 ? size_t(sp.L) * 4 : 0);
+  l.off_k2n = take(size_t(sp.L) * 4);
   l.off_tmp = take(size_t(s + 64 + 2) * 8);  // plan-time scratch: z, factors of m, flag
   l.total = o;
   return l;
@@ -705,7 +705,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
   pl->d_tw16 = (double2*)(b + lay.off_tw16);
   pl->d_twj = (double2*)(b + lay.off_twj);
   pl->d_jq = (int32_t*)(b + lay.off_jq);
-  pl->d_k2n = sp.L1 > 1 ? (int32_t*)(b + lay.off_k2n) : nullptr;
+  pl->d_k2n = (int32_t*)(b + lay.off_k2n);
   pl->d_k1c = (int32_t*)(b + lay.off_k1c);
   cudaStream_t st = pl->stream;
 
