@@ -306,14 +306,17 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // Tlo[k] = ω_{16 L1}^k (k < 16) — and the constant T1s[k] = ω_{L1}^k (L1
 // slots); then, for staged plans, the staging of CH slots (a, twiddle, code:
 // 36 B each, CH a multiple of 4) and its mbarrier, for the others the item's
-// scatter twiddles ω_{L1}^{e1 f1} in kTwRep replicas (k1_item)
-constexpr int kTwRep = 8;
+// scatter twiddles ω_{L1}^{e1 f1} in kTwRep replicas (k1_item), followed,
+// when the plan stages the first SRn slots (k1_srn), by their a (16 B) and
+// codes (4 B) and an mbarrier
+constexpr int kTwRep = kK1TwRep;
 template <int L2>
 __host__ __device__ constexpr int k1_aux_base() { return int(k1_row_slots(L2, QMC_ROW_E)); }
 template <int L2>
-__host__ __device__ constexpr size_t rows_smem(int CH, int L1) {
+__host__ __device__ constexpr size_t rows_smem(int CH, int L1, int SRn) {
   return size_t(k1_aux_base<L2>() + kK1Aux + L1) * 16 +
-         (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16 : size_t(L1) * kTwRep * 16);
+         (CH > 0 ? size_t(CH) * (16 + 16 + 4) + 16
+                 : size_t(L1) * kTwRep * 16 + (SRn > 0 ? size_t(SRn) * 20 + 16 : 0));
 }
 
 struct K1Args {
@@ -324,6 +327,7 @@ struct K1Args {
   const int32_t* __restrict__ k1c;     // [nch+1] chunk starts, [nch] regular-round slots
   int nch, bal;
   int CH;                              // > 0: staged (one chunk of CH slots, prefetched)
+  int SRn;                             // CH = 0, one chunk: its first SRn slots (whole rounds) staged
   int dense;                           // asort holds T[p][f1][e2] (k_dense_cols): no scatter
   const double2* __restrict__ twj;     // [L1][S1]
   const double2* __restrict__ tw2;     // [L2] ω_{L2}^i (row-FFT stage twiddles)
@@ -380,6 +384,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
                    smem_u32(dst)),
                "l"(src), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
+}
+
+// Direct mode with staged first rounds (SRn > 0): the a and codes of the
+// NEXT item's first SRn slots are copied into shared memory by two bulk async
+// copies (one thread, an mbarrier) while this item's FFTs run; the item's
+// later slots are read from global memory as before.
+template <int L2>
+struct K1Hyb {
+  double2* stA;   // [SRn] a of the pair
+  int32_t* stE;   // [SRn] codes
+  uint64_t* bar;  // one phase per item
+  __device__ K1Hyb(double2* base, int L1, int SRn)
+      : stA(base + k1_aux_base<L2>() + kK1Aux + L1 + L1 * kTwRep),
+        stE(reinterpret_cast<int32_t*>(stA + SRn)),
+        bar(reinterpret_cast<uint64_t*>(stE + SRn)) {}
+};
+template <int L2>
+__device__ __forceinline__ void k1_issue_hyb(const K1Args& a, const K1Hyb<L2>& hb, int it) {
+  const int p = it / a.L1;
+  const unsigned n = unsigned(a.SRn);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging reads before the async writes
+  mbar_expect_tx(hb.bar, n * 20u);
+  bulk_g2s(hb.stA, a.asort + int64_t(p) * a.S1, n * 16u, hb.bar);
+  bulk_g2s(hb.stE, a.e2q, n * 4u, hb.bar);
 }
 
 // stage the single chunk of item it (a of the pair, twiddles of f1, codes);
@@ -479,8 +507,23 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       const int nreg = __ldg(&a.k1c[nch + 1 + c]);
       double2 acc = make_double2(0.0, 0.0);
       const double2* tws = TWs + (tid & (kTwRep - 1));
+      int i0 = q0 + tid;
+      if (a.SRn > 0) {  // the first SRn slots (one chunk: q0 = 0) were staged during the previous item
+        const K1Hyb<L2> hb(S, L1, a.SRn);
+        mbar_wait(hb.bar, phase);
+        phase ^= 1u;
+#pragma unroll 2
+        for (int i = tid; i < a.SRn; i += NT) {
+          const int cd = hb.stE[i];
+          const double2 pr = cmul(hb.stA[i], tws[((cd >> kK1E1Shift) & 511) * kTwRep]);
+          acc = (cd & kK1First) ? pr : cadd(acc, pr);
+          QMC_CHECK_IDX(padE<E>(cd & 0x3fff), k1_row_slots(L2, E));
+          S[padE<E>(cd & 0x3fff)] = acc;
+        }
+        i0 = a.SRn + tid;
+      }
       QMC_UNROLL(QMC_K1_UNROLL)
-      for (int i = q0 + tid; i < q0 + nreg; i += NT) {
+      for (int i = i0; i < q0 + nreg; i += NT) {
 #if QMC_K1_PF > 0
         // the slot QMC_K1_PF rounds ahead into L1 (no register held)
         if (i + QMC_K1_PF * NT < q0 + nreg) {
@@ -522,6 +565,7 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
     }
   }
   __syncthreads();  // the row T' is complete
+  if (a.SRn > 0 && tid == 0 && next >= 0) k1_issue_hyb<L2>(a, K1Hyb<L2>(S, L1, a.SRn), next);  // overlaps the FFTs
   QMC_TS(1);
   double2 v[E];
   if (a.dense) {  // the first DFT dimension was done by k_dense_cols: load the row
@@ -603,6 +647,11 @@ __global__ void __launch_bounds__(L2 / QMC_ROW_E, (L2 / QMC_ROW_E >= 512 ? QMC_R
     if (threadIdx.x == 0) mbar_init(sg.bar, 1);
     __syncthreads();
     if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue<L2>(a, sg, blockIdx.x);
+  } else if (a.SRn > 0) {
+    const K1Hyb<L2> hb(smem, a.L1, a.SRn);
+    if (threadIdx.x == 0) mbar_init(hb.bar, 1);
+    __syncthreads();
+    if (threadIdx.x == 0 && int(blockIdx.x) < nitems) k1_issue_hyb<L2>(a, hb, blockIdx.x);
   }
   // the constant twiddle tables after the row (rows_smem): Tlo, T1s
   {
@@ -1629,6 +1678,7 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   a.occ = pl->d_occ;
   a.S1 = pl->S1;
   a.CH = pl->k1_stage;
+  a.SRn = (pl->k1_stage == 0 && pl->k1_nch == 1 && pl->k1_bal && !pl->k1_dense) ? pl->k1_srn : 0;
   a.k1c = pl->d_k1c;
   a.nch = pl->k1_nch;
   a.bal = pl->k1_bal;
@@ -1650,10 +1700,13 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   return a;
 }
 
+static int stream_sms(const qmc_plan* pl, cudaStream_t st);
+
 template <int L2>
 static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int64_t pair0, double2* U, int np,
                        double* colsum, cudaStream_t st) {
-  const size_t smem = rows_smem<L2>(pl->k1_stage, int(pl->sp.L1));
+  const size_t smem = rows_smem<L2>(pl->k1_stage, int(pl->sp.L1),
+                                     (pl->k1_stage == 0 && pl->k1_nch == 1 && pl->k1_bal && !pl->k1_dense) ? pl->k1_srn : 0);
   auto kern = k_rows16<L2>;
   static int nsm = 0;
   static size_t last_smem = 0;  // attribute and occupancy of the last shared-memory size (per instantiation)
@@ -1671,7 +1724,7 @@ static int launch_rows(const qmc_plan* pl, const double2* asort, int64_t t, int6
   int per_sm = last_per_sm;
   if (pl->k1_per_sm > 0) per_sm = std::min(per_sm, pl->k1_per_sm);
   const int64_t items = pl->sp.L1 * int64_t(np);
-  int64_t cap = int64_t(nsm) * std::max(per_sm, 1);
+  int64_t cap = int64_t(pl->green ? stream_sms(pl, st) : nsm) * std::max(per_sm, 1);
   if (pl->k1_grid_cap > 0) cap = std::min<int64_t>(cap, pl->k1_grid_cap);
   const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(items, cap)));
   kern<<<grid, L2 / QMC_ROW_E, smem, st>>>(k1_args(pl, asort, t, pair0, U, np, colsum));
@@ -1699,6 +1752,16 @@ static int sm_count_cols() {
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
   }
   return nsm;
+}
+
+// SMs a launch on stream st may use: the plan's green-context partition for
+// its internal streams in green mode, else the whole device
+static int stream_sms(const qmc_plan* pl, cudaStream_t st) {
+  if (pl->green) {
+    if (st == pl->ist[0]) return pl->gsm[0];
+    if (st == pl->ist[1]) return pl->gsm[1];
+  }
+  return sm_count_cols();
 }
 
 static K2Args k2_args(const qmc_plan* pl, const CallLayout& cl, const double2* U, int ntx, int ng, int64_t pair0,
@@ -1751,7 +1814,8 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       if (pl->k2_per_sm > 0) per_sm = std::min(per_sm, pl->k2_per_sm);
       const int ntx = int(pl->sp.L2 / CBP), ng = (np + 15) / 16;
       const int64_t ntiles = int64_t(ntx) * ng;
-      const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(nsm) * std::max(per_sm, 1))));
+      const unsigned grid = unsigned(
+          std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(pl->green ? stream_sms(pl, st) : nsm) * std::max(per_sm, 1))));
       pk<<<grid, 16 * CBP, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum));
       QMC_LAUNCHED();
       *nbx_used = ntx;
@@ -1776,7 +1840,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
       const int ntx = int(pl->sp.L2 / kUB), ng = np / kP2PG;
       const int64_t ntiles = int64_t(ntx) * ng;
       const unsigned grid =
-          unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(sm_count_cols()) * std::max(per_sm, 1))));
+          unsigned(std::max<int64_t>(1, std::min<int64_t>(ntiles, int64_t(stream_sms(pl, st)) * std::max(per_sm, 1))));
       pk<<<grid, kP2Thr, psm, st>>>(k2_args(pl, cl, U, ntx, ng, pair0, E, part, colsum), ilog2(pl->sp.L2));
       QMC_LAUNCHED();
       *nbx_used = int(grid);  // one partial slot row per CTA (k2p2_flush)
@@ -1789,7 +1853,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   const int nbxT = int((pl->sp.L2 + CBx - 1) / CBx), ngr = (np + cl.PG - 1) / cl.PG;
   // enough CTAs for ~8 per SM; each loops over several column groups, so the
   // column means need only gridDim.x partial slots per pair
-  const int gx = std::max(1, std::min(nbxT, (sm_count_cols() * 8 + ngr - 1) / ngr));
+  const int gx = std::max(1, std::min(nbxT, (stream_sms(pl, st) * 8 + ngr - 1) / ngr));
   dim3 g((unsigned)gx, (unsigned)ngr);
   *nbx_used = gx;
   kern<<<g, kColThreads, smem, st>>>(U, pl->sp.L, int(pl->sp.L2), ilog2(pl->sp.L2), pl->m, np, cl.PG, pl->d_P,
@@ -1882,7 +1946,7 @@ static int small_dispatch(const qmc_plan* pl, const SmallArgs& sa, int f, int64_
 // bidx & 1 when two sets are in use): K0, K1, K2 and the column-mean reduce
 static int run_batch(const qmc_plan* pl, const CallLayout& cl, const double* A, int64_t lda, int64_t t, int f,
                      double* out, EpiArgs E, char* ws, int64_t pairs_b, int64_t pair0, int64_t bidx, cudaStream_t bs,
-                     const double* A_host, int64_t lda_host) {
+                     cudaStream_t bs2, const double* A_host, int64_t lda_host) {
   const int64_t npairs_total = (t + 1) / 2;
   const bool colmean = f == QMC_F_IDENTITY || f == QMC_F_AFFINE || f == QMC_F_EXP;
   const int nsets = cl.nsets;
@@ -1894,6 +1958,11 @@ static int run_batch(const qmc_plan* pl, const CallLayout& cl, const double* A, 
   double* part = (double*)(ws + cl.off_part) + size_t(set) * cl.nbx * cl.part_stride;
   E.rowpart = (double*)(ws + cl.off_rowsum);
   double2* asort = (double2*)(ws + cl.off_asort) + size_t(set) * pairs_b * pl->S1;
+  // green mode (bs2 != bs): K0/K1 on bs, K2 and the reduce on bs2 once the
+  // set's U is written; batch bidx reuses the set after batch bidx - 2's K2
+  // and reduce have read it
+  const bool split = bs2 != bs;
+  if (split && bidx >= nsets && cudaStreamWaitEvent(bs, pl->ev_free[set], 0) != cudaSuccess) return QMC_ECUDA;
   if (A_host) {
     const int64_t c0 = 2 * pair0, nc = std::min<int64_t>(2 * int64_t(np), t - c0);
     if (cudaMemcpy2DAsync(const_cast<double*>(A) + c0 * lda, size_t(lda) * 8, A_host + c0 * lda_host,
@@ -1913,7 +1982,7 @@ static int run_batch(const qmc_plan* pl, const CallLayout& cl, const double* A, 
     const size_t psm = size_t(pl->s) * 16;
     set_smem_attr(k_pack_smem, psm);
     // slices of the slots: ~2 CTAs of work per SM in total
-    const int ny = int(std::max<int64_t>(1, std::min<int64_t>((2 * sm_count_cols() + np - 1) / np,
+    const int ny = int(std::max<int64_t>(1, std::min<int64_t>((2 * stream_sms(pl, bs) + np - 1) / np,
                                                               (pl->S1 + 1023) / 1024)));
     k_pack_smem<<<dim3(unsigned(np), unsigned(ny)), 256, psm, bs>>>(A, lda, t, pair0, pl->d_jq, pl->s, pl->S1,
                                                                     asort);
@@ -1926,18 +1995,22 @@ static int run_batch(const qmc_plan* pl, const CallLayout& cl, const double* A, 
   int rc = rows_dispatch(pl, asort, t, pair0, U, np, colsum, bs);
   if (rc) return rc;
   prof_end(KC_ROWS, bs);
-  prof_begin(KC_COLS, bs);
+  if (split && (cudaEventRecord(pl->ev_ready[set], bs) != cudaSuccess ||
+                cudaStreamWaitEvent(bs2, pl->ev_ready[set], 0) != cudaSuccess))
+    return QMC_ECUDA;
+  prof_begin(KC_COLS, bs2);
   int nbx_used = cl.nbx;
-  rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs, &nbx_used);
+  rc = cols_dispatch(pl, cl, U, np, pair0, ep, E, colmean ? part : nullptr, colsum, bs2, &nbx_used);
   if (rc) return rc;
-  prof_end(KC_COLS, bs);
+  prof_end(KC_COLS, bs2);
   if (colmean) {
-    prof_begin(KC_REDUCE, bs);
-    k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs>>>(part, nbx_used, cl.part_stride, 2 * np, 2 * pair0, t,
-                                                       pl->N, out);
+    prof_begin(KC_REDUCE, bs2);
+    k_colpart_reduce<<<nblk(2 * np, 8), 256, 0, bs2>>>(part, nbx_used, cl.part_stride, 2 * np, 2 * pair0, t,
+                                                        pl->N, out);
     QMC_LAUNCHED();
-    prof_end(KC_REDUCE, bs);
+    prof_end(KC_REDUCE, bs2);
   }
+  if (split && cudaEventRecord(pl->ev_free[set], bs2) != cudaSuccess) return QMC_ECUDA;
   return QMC_OK;
 }
 
@@ -2008,10 +2081,12 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   // (measured on B200: c2 0.61 vs 0.68 ms, c3 24.2 vs 26.7, c4 2.37 vs 2.47;
   // c5 (L1 = 96) 78.8 vs 79.0 ms — equal, so its device calls run on the
   // caller's stream, where each kernel's event time is its own)
+  // green mode: K0/K1 of every batch on one SM partition, K2 on the other
+  const bool green = cl.nsets == 2 && pl->green;
 #ifdef QMC_DIAG_TWO_ALWAYS
   const bool two = cl.nsets == 2 && pl->nstreams == 2;
 #else
-  const bool two = cl.nsets == 2 && pl->nstreams == 2 && (A_host || pl->sp.L1 <= 16);
+  const bool two = green || (cl.nsets == 2 && pl->nstreams == 2 && (A_host || pl->sp.L1 <= 16));
 #endif
   if (two) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
@@ -2025,7 +2100,8 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   int64_t bidx = 0;
   int rc = QMC_OK;
   for (int64_t pair0 = 0; pair0 < npairs_total && rc == QMC_OK; pair0 += pairs_b, ++bidx) {
-    rc = run_batch(pl, cl, A, lda, t, f, out, E, ws, pairs_b, pair0, bidx, two ? pl->ist[bidx & 1] : st, A_host,
+    const cudaStream_t bs = green ? pl->ist[0] : two ? pl->ist[bidx & 1] : st;
+    rc = run_batch(pl, cl, A, lda, t, f, out, E, ws, pairs_b, pair0, bidx, bs, green ? pl->ist[1] : bs, A_host,
                    lda_host);
   }
   if (two) {  // join (also after an error: the caller's stream must not run ahead of queued batches)

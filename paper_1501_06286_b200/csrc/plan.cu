@@ -12,6 +12,7 @@
 //
 // The plan is excluded from the paper's timings and from
 // bench.py's timed region.
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -610,9 +611,111 @@ static int validate_family(int family, int64_t N_or_D, int64_t s, int64_t* N, in
 // L1 <= 192); with the non-persistent k_cols_x (L1 = 256) the overlap
 // measured slower, so such plans use the caller's stream (run() further
 // restricts the two streams to calls where they overlap something)
+// Green-context SM partitions (driver API through cudaGetDriverEntryPoint, so
+// libqmc.so links no libcuda): the device's SMs split into groups of 8; the
+// last ceil(G/8) groups form partition 1, the rest (and the remainder)
+// partition 0.  Created once per (device, G) and kept for the process.
+struct GreenParts {
+  int dev = -1, G = 0, ok = 0;
+  CUgreenCtx g[2] = {nullptr, nullptr};
+  int nsm[2] = {0, 0};
+};
+typedef CUresult (*PFN_getRes)(CUdevice, CUdevResource*, CUdevResourceType);
+typedef CUresult (*PFN_split)(CUdevResource*, unsigned*, const CUdevResource*, CUdevResource*, unsigned, unsigned);
+typedef CUresult (*PFN_desc)(CUdevResourceDesc*, CUdevResource*, unsigned);
+typedef CUresult (*PFN_gctx)(CUgreenCtx*, CUdevResourceDesc, CUdevice, unsigned);
+typedef CUresult (*PFN_gstream)(CUstream*, CUgreenCtx, unsigned, int);
+template <typename F>
+static bool drv_fn(const char* name, F* f) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+      !p)
+    return false;
+  *f = reinterpret_cast<F>(p);
+  return true;
+}
+static std::mutex g_green_mu;
+static GreenParts g_green[8];
+static const GreenParts* green_parts(int G) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 8) return nullptr;
+  std::lock_guard<std::mutex> lk(g_green_mu);
+  GreenParts& gp = g_green[dev];
+  if (gp.dev == dev && gp.G == G) return gp.ok ? &gp : nullptr;
+  if (gp.dev == dev) return nullptr;  // one partitioning per device and process
+  gp.dev = dev;
+  gp.G = G;
+  PFN_getRes getRes;
+  PFN_split split;
+  PFN_desc desc;
+  PFN_gctx gctx;
+  if (!drv_fn("cuDeviceGetDevResource", &getRes) || !drv_fn("cuDevSmResourceSplitByCount", &split) ||
+      !drv_fn("cuDevResourceGenerateDesc", &desc) || !drv_fn("cuGreenCtxCreate", &gctx))
+    return nullptr;
+  CUdevResource all, rem;
+  unsigned ng = 0;
+  if (getRes(CUdevice(dev), &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS ||
+      split(nullptr, &ng, &all, nullptr, 0, 8) != CUDA_SUCCESS || ng < 2)
+    return nullptr;
+  std::vector<CUdevResource> grp(ng);
+  memset(&rem, 0, sizeof(rem));
+  if (split(grp.data(), &ng, &all, &rem, 0, 8) != CUDA_SUCCESS) return nullptr;
+  const unsigned n1 = unsigned(std::min<int>((G + 7) / 8, int(ng) - 1));
+  std::vector<CUdevResource> r0(grp.begin(), grp.end() - n1), r1(grp.end() - n1, grp.end());
+  if (rem.sm.smCount > 0) r0.push_back(rem);
+  CUdevResourceDesc d0, d1;
+  if (desc(&d0, r0.data(), unsigned(r0.size())) != CUDA_SUCCESS ||
+      desc(&d1, r1.data(), unsigned(r1.size())) != CUDA_SUCCESS ||
+      gctx(&gp.g[0], d0, CUdevice(dev), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS ||
+      gctx(&gp.g[1], d1, CUdevice(dev), CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+    return nullptr;
+  for (const CUdevResource& r : r0) gp.nsm[0] += int(r.sm.smCount);
+  for (const CUdevResource& r : r1) gp.nsm[1] += int(r.sm.smCount);
+  gp.ok = 1;
+  return &gp;
+}
+
+// green mode: the two internal streams on the two SM partitions, and the
+// per-set hand-off events
+static bool plan_green_streams(qmc_plan* pl, int G) {
+  const GreenParts* gp = green_parts(G);
+  PFN_gstream gstream;
+  if (!gp || !drv_fn("cuGreenCtxStreamCreate", &gstream)) return false;
+  CUstream s0 = nullptr, s1 = nullptr;
+  if (gstream(&s0, gp->g[0], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) return false;
+  if (gstream(&s1, gp->g[1], CU_STREAM_NON_BLOCKING, 0) != CUDA_SUCCESS) {
+    cudaStreamDestroy(cudaStream_t(s0));
+    return false;
+  }
+  pl->ist[0] = cudaStream_t(s0);
+  pl->ist[1] = cudaStream_t(s1);
+  bool ok = cudaEventCreateWithFlags(&pl->ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&pl->ev_join[0], cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&pl->ev_join[1], cudaEventDisableTiming) == cudaSuccess;
+  for (int i = 0; i < 2 && ok; ++i)
+    ok = cudaEventCreateWithFlags(&pl->ev_ready[i], cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&pl->ev_free[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) return false;  // (a plan without its events is not created: create_common fails on nstreams)
+  pl->gsm[0] = gp->nsm[0];
+  pl->gsm[1] = gp->nsm[1];
+  pl->green = 1;
+  return true;
+}
+
 static void plan_streams(qmc_plan* pl) {
   pl->nstreams = 1;
+  pl->green = 0;
   pl->mu = new (std::nothrow) std::mutex();
+  if (const char* gv = getenv("QMC_GREEN")) {  // K2 partition of G SMs (multiple of 8)
+    const int G = int(strtol(gv, nullptr, 10));
+    if (G > 0 && pl->mu && plan_green_streams(pl, G)) {
+      pl->nstreams = 2;
+      cudaGetLastError();
+      return;
+    }
+    cudaGetLastError();
+  }
   const char* one = getenv("QMC_ONE_STREAM");
   const bool want2 = one ? one[0] != '1' : pl->sp.L1 <= 192;
   if (want2 && pl->mu &&
@@ -843,6 +946,14 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       const int64_t limit = sp.L2 >= 8192 ? 232448 : 115712;
       const int64_t room = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux + sp.L1) * 16 - 16 - 64) / 36 / 4 * 4;
       if (cr.size() == 1 && chmax <= room) pl->k1_stage = int((chmax + 3) / 4 * 4);
+      // otherwise (one chunk, read from global memory): its first whole
+      // rounds of (a, code) — 20 B per slot, the twiddle comes from the
+      // item's shared table — fill the rest of the shared memory, copied
+      // during the previous item's FFTs; the later rounds stay direct
+      const int64_t room20 = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux + sp.L1) * 16 -
+                              sp.L1 * kK1TwRep * 16 - 16 - 64) / 20;
+      if (!pl->k1_stage && cr.size() == 1 && !getenv("QMC_K1_NOHYB"))
+        pl->k1_srn = int(std::min<int64_t>(room20 / NT, cr[0] / NT) * NT);
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     } else {
       // bucket order, one chunk
@@ -1043,6 +1154,12 @@ const char* qmc_profile_class_name(int k) {
 
 void qmc_plan_destroy(qmc_plan_t pl) {
   if (!pl) return;
+  if (pl->green) {
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(pl->ev_ready[i]);
+      cudaEventDestroy(pl->ev_free[i]);
+    }
+  }
   if (pl->nstreams == 2) {
     cudaStreamDestroy(pl->ist[0]);
     cudaStreamDestroy(pl->ist[1]);

@@ -102,6 +102,8 @@ constexpr int kK1Ovf = 64;
 // twiddles and 16 constant ones, before the L1 constant column twiddles
 // (pipeline.cu rows_smem)
 constexpr int kK1Aux = 48;
+// replicas of the item's scatter-twiddle table in K1's shared memory (direct mode)
+constexpr int kK1TwRep = 8;
 // shared-memory row slots of K1: padE(v) for every v <= L2 + kK1Ovf
 __host__ __device__ inline constexpr int64_t k1_row_slots(int64_t L2, int E) {
   return L2 + kK1Ovf + 1 + (L2 + kK1Ovf) / E + 1;
@@ -149,6 +151,7 @@ struct qmc_plan {
   int64_t S1;
   int k1_bal, k1_nch, k1_ch;
   int k1_stage;  // > 0: the balanced order is one chunk of k1_stage slots, staged in shared memory
+  int k1_srn;    // direct mode: the first k1_srn slots (whole rounds; a and code, 20 B each) staged
   int k1_dense;  // 1: dense first pass (k_pack_dense + k_dense_cols), S1 = L, no chunks
   cudaStream_t stream;
   // batches alternate over nstreams internal streams (fork/join from the
@@ -156,6 +159,12 @@ struct qmc_plan {
   int nstreams;
   cudaStream_t ist[2];
   cudaEvent_t ev_fork, ev_join[2];
+  // green mode (QMC_GREEN, plan_streams): ist[0] runs on one green-context
+  // SM partition (K0, K1: gsm[0] SMs), ist[1] on the other (K2: gsm[1] SMs);
+  // ev_ready[set] = the set's U is written, ev_free[set] = it was read
+  int green;
+  int gsm[2];
+  cudaEvent_t ev_ready[2], ev_free[2];
   std::mutex* mu;
   // device pointers into plan_ws
   char* ws;
