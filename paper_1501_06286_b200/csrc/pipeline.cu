@@ -508,12 +508,36 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       double2 acc = make_double2(0.0, 0.0);
       const double2* tws = TWs + (tid & (kTwRep - 1));
       int i0 = q0 + tid;
+      // Slots go in groups of U rounds: every load of a group (codes, a, then
+      // the twiddles the codes select) is issued before the group's first
+      // store to S — the compiler cannot reorder the shared-memory loads
+      // across those stores itself (same base pointer), which serialised the
+      // slots' latency chains
+      constexpr int U = QMC_K1_UNROLL;
       if (a.SRn > 0) {  // the first SRn slots (one chunk: q0 = 0) were staged during the previous item
         const K1Hyb<L2> hb(S, L1, a.SRn);
         mbar_wait(hb.bar, phase);
         phase ^= 1u;
-#pragma unroll 2
-        for (int i = tid; i < a.SRn; i += NT) {
+        int i = tid;
+        for (; i + (U - 1) * NT < a.SRn; i += U * NT) {
+          int cd[U];
+          double2 av[U], tw[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            cd[u] = hb.stE[i + u * NT];
+            av[u] = hb.stA[i + u * NT];
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) tw[u] = tws[((cd[u] >> kK1E1Shift) & 511) * kTwRep];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const double2 pr = cmul(av[u], tw[u]);
+            acc = (cd[u] & kK1First) ? pr : cadd(acc, pr);
+            QMC_CHECK_IDX(padE<E>(cd[u] & 0x3fff), k1_row_slots(L2, E));
+            S[padE<E>(cd[u] & 0x3fff)] = acc;
+          }
+        }
+        for (; i < a.SRn; i += NT) {
           const int cd = hb.stE[i];
           const double2 pr = cmul(hb.stA[i], tws[((cd >> kK1E1Shift) & 511) * kTwRep]);
           acc = (cd & kK1First) ? pr : cadd(acc, pr);
@@ -522,7 +546,29 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
         }
         i0 = a.SRn + tid;
       }
-      QMC_UNROLL(QMC_K1_UNROLL)
+      {
+        int i = i0;
+        for (; i + (U - 1) * NT < q0 + nreg; i += U * NT) {
+          int cd[U];
+          double2 av[U], tw[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            cd[u] = __ldg(&a.e2q[i + u * NT]);
+            av[u] = __ldg(&ap[i + u * NT]);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) tw[u] = tws[((cd[u] >> kK1E1Shift) & 511) * kTwRep];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const double2 pr = cmul(av[u], tw[u]);
+            acc = (cd[u] & kK1First) ? pr : cadd(acc, pr);
+            QMC_CHECK_IDX(i + u * NT, a.S1);
+            QMC_CHECK_IDX(padE<E>(cd[u] & 0x3fff), k1_row_slots(L2, E));
+            S[padE<E>(cd[u] & 0x3fff)] = acc;
+          }
+        }
+        i0 = i;
+      }
       for (int i = i0; i < q0 + nreg; i += NT) {
 #if QMC_K1_PF > 0
         // the slot QMC_K1_PF rounds ahead into L1 (no register held)

@@ -952,8 +952,10 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       // during the previous item's FFTs; the later rounds stay direct
       const int64_t room20 = (limit - (k1_row_slots(sp.L2, QMC_ROW_E) + kK1Aux + sp.L1) * 16 -
                               sp.L1 * kK1TwRep * 16 - 16 - 64) / 20;
+      int64_t sr_cap = room20 / NT;  // QMC_K1_SR: cap on the staged rounds (tuning)
+      if (const char* ev = getenv("QMC_K1_SR")) sr_cap = std::min<int64_t>(sr_cap, strtol(ev, nullptr, 10));
       if (!pl->k1_stage && cr.size() == 1 && !getenv("QMC_K1_NOHYB"))
-        pl->k1_srn = int(std::min<int64_t>(room20 / NT, cr[0] / NT) * NT);
+        pl->k1_srn = int(std::min<int64_t>(sr_cap, cr[0] / NT) * NT);
       QMC_PLAN_CHECK(cudaMemcpy(pl->d_e2q, code.data(), 4 * code.size(), cudaMemcpyHostToDevice) ? QMC_ECUDA : 0);
     } else {
       // bucket order, one chunk
