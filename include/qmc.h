@@ -257,7 +257,10 @@ int qmc_cbc_step(int64_t N, const double* crit, int64_t zmax, double gamma, doub
  * encoding of x = 2), L (FFT length; L = m or padded L >= 2m-1), L1, L2,
  * pairs per batch, D, p, then the row kernel's scatter-input layout:
  * bucket order (0), balanced (1) or dense (2), staged slots per pair,
- * chunks, slots per chunk.  Host pointer, >= 16 int64. */
+ * chunks, slots per chunk; info[16] = slots of the direct scatter's first
+ * rounds staged in shared memory (0: none), info[17] = SMs of the column
+ * pass's green-context partition (0: green mode off, QMC_GREEN).  Host
+ * pointer, >= 18 int64. */
 int qmc_plan_info(qmc_plan_t plan, int64_t* info);
 
 /* D2H copies of the plan tables for bit-exact tests (host buffers; any may

@@ -219,10 +219,10 @@ def qmc_cbc_step(N: int, crit, zmax: int, gamma: float, p, z_out, d: int, stream
 
 
 def qmc_plan_info(plan) -> dict:
-    buf = (C.c_int64 * 16)()
+    buf = (C.c_int64 * 18)()
     _check(_lib.qmc_plan_info(plan, buf), "qmc_plan_info")
     keys = ["family", "N", "m", "s", "phi", "gen", "L", "L1", "L2", "batch_pairs", "D", "p",
-            "k1_order", "k1_slots", "k1_chunks", "k1_chunk_slots"]
+            "k1_order", "k1_slots", "k1_chunks", "k1_chunk_slots", "k1_staged_slots", "green_k2_sms"]
     return dict(zip(keys, list(buf)))
 
 

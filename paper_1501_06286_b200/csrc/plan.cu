@@ -1095,6 +1095,8 @@ int qmc_plan_info(qmc_plan_t pl, int64_t* info) {
   info[13] = pl->S1;
   info[14] = pl->k1_nch;
   info[15] = pl->k1_ch;
+  info[16] = pl->k1_srn;
+  info[17] = pl->green ? pl->gsm[1] : 0;
   return QMC_OK;
 }
 

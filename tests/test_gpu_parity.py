@@ -639,3 +639,62 @@ def test_dense_input_with_collisions(qmc, monkeypatch, N, s, t):
     plan_s = qmc.Plan.from_workload(w)
     assert plan_s.info["k1_order"] != 2
     check_X(w, X.cpu().numpy(), plan_s.matmul(A).cpu().numpy())
+
+
+# ------------------------------------------------------------------ K1 staged first rounds, green mode
+@pytest.mark.parametrize("N,s,t", [(40961, 4096, 4), (786433, 8192, 2)])
+def test_k1_staged_rounds_bitwise(qmc, monkeypatch, N, s, t):
+    """The direct scatter with its first rounds staged in shared memory
+    (k1_srn, the default where room is left beside the row), with one staged
+    round (QMC_K1_SR=1) and with none (QMC_K1_NOHYB) sums the same slots in
+    the same order, so X is bitwise equal; and within the bar of the oracle."""
+    import torch
+    w = W.custom_lattice(N, s, t, W.PHI_INVNORM_MID, seed=N + 7 * s)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    plan = qmc.Plan.from_workload(w)
+    nt = plan.info["L2"] // 16
+    assert plan.info["k1_order"] == 1 and plan.info["k1_staged_slots"] >= nt
+    assert plan.info["k1_staged_slots"] % nt == 0
+    X0 = plan.matmul(A).clone()
+    monkeypatch.setenv("QMC_K1_SR", "1")
+    p1 = qmc.Plan.from_workload(w)
+    assert p1.info["k1_staged_slots"] == nt
+    X1 = p1.matmul(A).clone()
+    monkeypatch.delenv("QMC_K1_SR")
+    monkeypatch.setenv("QMC_K1_NOHYB", "1")
+    p2 = qmc.Plan.from_workload(w)
+    assert p2.info["k1_staged_slots"] == 0
+    X2 = p2.matmul(A).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(X0, X1) and torch.equal(X0, X2)
+    rows = sample_rows(w.N, 128, seed=s + 1)
+    check_X(w, X0.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy(), X_rows(w, rows))
+
+
+@pytest.mark.parametrize("f", [W.F_EXP, W.F_ROWMEAN_RELU])
+def test_green_partitions(qmc, monkeypatch, f):
+    """Green mode (QMC_GREEN): K0/K1 on one SM partition and K2 on the other,
+    batches handed over by per-set events; X and the fused reductions equal
+    the single-stream results bitwise (same kernels, same order per column)
+    across several batches, and the partition sizes add up to the device."""
+    import torch
+    N, s, t = 65537, 512, 96
+    monkeypatch.setenv("QMC_BATCH_PAIRS", "16")  # three batches: both sets, reuse after the hand-off
+    phi = W.PHI_INVNORM_MID if f == W.F_EXP else W.PHI_SHIFT_HALF
+    w = W.custom_lattice(N, s, t, phi, seed=11 + f)
+    if f == W.F_EXP:
+        w.A = np.asfortranarray(w.A * 0.05)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    plan = qmc.Plan.from_workload(w)
+    X0 = qmc.x_empty(plan.N, t, "cuda")
+    m0 = plan.mean(A, f, 0.0, X=X0).clone()
+    monkeypatch.setenv("QMC_GREEN", "24")
+    pg = qmc.Plan.from_workload(w)
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    assert 24 <= pg.info["green_k2_sms"] < nsm
+    X1 = qmc.x_empty(pg.N, t, "cuda")
+    m1 = pg.mean(A, f, 0.0, X=X1).clone()
+    torch.cuda.synchronize()
+    assert torch.equal(X0, X1) and torch.equal(m0, m1)
+    rows = sample_rows(w.N, 64, seed=3)
+    check_X(w, X1.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy(), X_rows(w, rows))
