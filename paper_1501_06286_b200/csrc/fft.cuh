@@ -552,8 +552,10 @@ __device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const doub
     const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);
     if constexpr (SUB == 256 && RHO == 1) twiddle16_fold<-1>(v, w, b);
     else twiddle16<-1>(v, w);
+#ifndef QMC_DIAG_NO_XW
 #pragma unroll
     for (int k = 0; k < 16; ++k) B[j + 17 * k] = v[k];
+#endif
     // v is dead until the exchange's reads: the first half of the spectrum
     // row goes in flight now (its latency overlaps the exchange and the last
     // butterflies)
@@ -562,8 +564,10 @@ __device__ __forceinline__ void dif_fwd(double2 (&v)[16], double2* S, const doub
       for (int q = 0; q < WA; ++q) wv[q] = ldg_ordered(&Wr[q * NT]);
     }
     __syncwarp(NT >= 32 ? 0xffffffffu : 0xffffu);  // the half-warp group (rows of 256: 16 lanes exist)
+#ifndef QMC_DIAG_NO_XW  // diagnostic: the half-warp exchange skipped (wrong results; timing bound)
 #pragma unroll
     for (int p = 0; p < 16; ++p) v[p] = B[17 * j + p];
+#endif
   } else if (Wr) {
 #pragma unroll
     for (int q = 0; q < WA; ++q) wv[q] = ldg_ordered(&Wr[q * NT]);
@@ -592,11 +596,15 @@ __device__ __forceinline__ void dif_inv(double2 (&v)[16], double2* S, const doub
   if constexpr (SUB >= 256) {
     const int k = SUB == 4096 ? (j0 >> 4) : 0, j = j0 & 15;
     double2* B2 = B + 272 * k;
+#ifndef QMC_DIAG_NO_XW
 #pragma unroll
     for (int p = 0; p < 16; ++p) B2[17 * j + p] = v[p];
+#endif
     __syncwarp(NT >= 32 ? 0xffffffffu : 0xffffu);  // the half-warp group (rows of 256: 16 lanes exist)
+#ifndef QMC_DIAG_NO_XW
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = B2[j + 17 * r];
+#endif
     const double2 w = ldg_ordered(&tw2[j * (L2 / 256)]);
     if constexpr (SUB == 256 && RHO == 1) twiddle16_fold<+1>(v, w, b);
     else twiddle16<+1>(v, w);

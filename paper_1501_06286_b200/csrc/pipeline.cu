@@ -438,7 +438,11 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
   const int tid = threadIdx.x;
   const int L1 = a.L1;
   const int f1 = item % L1, p = item / L1;
+#ifndef QMC_DIAG_NO_SCATTER
   const int nch = a.CH > 0 ? 0 : a.nch;
+#else  // diagnostic: no scatter (the row holds stale data; timing bound of the rest)
+  const int nch = 0;
+#endif
   const double2* ap = a.asort + int64_t(p) * a.S1;
   const double2* tp = a.twj + int64_t(f1) * a.S1;
   QMC_TS(0);
@@ -1725,6 +1729,9 @@ static K1Args k1_args(const qmc_plan* pl, const double2* asort, int64_t t, int64
   a.S1 = pl->S1;
   a.CH = pl->k1_stage;
   a.SRn = (pl->k1_stage == 0 && pl->k1_nch == 1 && pl->k1_bal && !pl->k1_dense) ? pl->k1_srn : 0;
+#ifdef QMC_DIAG_NO_SCATTER
+  a.SRn = 0;
+#endif
   a.k1c = pl->d_k1c;
   a.nch = pl->k1_nch;
   a.bal = pl->k1_bal;
