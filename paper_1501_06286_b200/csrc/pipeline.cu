@@ -296,6 +296,9 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef QMC_K1_UNROLL
 #define QMC_K1_UNROLL 4
 #endif
+#ifndef QMC_K1_UNROLL_BIG  // rows of 8192 (one CTA per SM): 8 measured best (c5 K1 48.6 -> 47.7 ms, c4 2.39 -> 2.33 ms/step)
+#define QMC_K1_UNROLL_BIG 8
+#endif
 #define QMC_PRAGMA_(x) _Pragma(#x)
 #define QMC_UNROLL_(n) QMC_PRAGMA_(unroll n)
 #define QMC_UNROLL(n) QMC_UNROLL_(n)
@@ -517,7 +520,7 @@ __device__ __forceinline__ void k1_item(const K1Args& a, double2* S, int item, i
       // store to S — the compiler cannot reorder the shared-memory loads
       // across those stores itself (same base pointer), which serialised the
       // slots' latency chains
-      constexpr int U = QMC_K1_UNROLL;
+      constexpr int U = L2 >= 8192 ? QMC_K1_UNROLL_BIG : QMC_K1_UNROLL;
       if (a.SRn > 0) {  // the first SRn slots (one chunk: q0 = 0) were staged during the previous item
         const K1Hyb<L2> hb(S, L1, a.SRn);
         mbar_wait(hb.bar, phase);
