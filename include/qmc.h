@@ -100,9 +100,12 @@ enum {
  * qmc_plan_create / qmc_plan_create_poly.  Validates N (or D) and s. */
 int qmc_plan_workspace_size(int family, int64_t N_or_D, int64_t s, size_t* plan_bytes);
 
-/* Bytes of device scratch one qmc_matmul / qmc_mean call on t columns
- * needs (call_ws).  Independent of A and X.  Dominated by U, the batch's
- * row-FFT output (two sets of up to ~768 MB); for ROWMEAN_RELU add one
+/* Bytes of device scratch one qmc_matmul / qmc_mean / qmc_mean_host call
+ * on t columns needs (call_ws).  Independent of A and X.  Dominated by U, the
+ * batch's row-FFT output: two sets of up to ~768 MB for calls on the two
+ * internal streams (host entry, plans with L1 <= 16), one set of up to
+ * ~16 GB for device calls of plans with L1 > 16, which run on the caller's
+ * stream in large batches; the larger of the two; for ROWMEAN_RELU add one
  * N-vector of partial row sums per group of 16 column pairs
  * (8·N·ceil(t/32) bytes). */
 int qmc_call_workspace_size(qmc_plan_t plan, int64_t t, int f, size_t* call_bytes);

@@ -1664,12 +1664,30 @@ struct CallLayout {
   int PG, ngroups, ngroups_all, nbx, nsets, part_stride;
 };
 
-// pairs per batch of a call on t columns: the plan's batch, capped at half
-// the call's pairs (rounded up to the pair group) so that two batches overlap
-static int64_t call_batch(const qmc_plan* pl, int64_t t) {
+// Whether a call may run its batches on the two internal streams: where they
+// overlap something — the per-batch host copies of qmc_mean_host (host), or
+// the column pass of plans with L1 <= 16 (measured on B200: c2 0.61 vs 0.68
+// ms, c3 24.2 vs 26.7, c4 2.37 vs 2.47; c5 (L1 = 96) 78.8 vs 79.0 ms —
+// equal, so its device calls run on the caller's stream, where each kernel's
+// event time is its own); green mode: K0/K1 on one SM partition, K2 on the
+// other
+static bool two_stream_mode(const qmc_plan* pl, bool host) {
+#ifdef QMC_DIAG_TWO_ALWAYS
+  return pl->nstreams == 2;
+#else
+  return pl->green || (pl->nstreams == 2 && (host || pl->sp.L1 <= 16));
+#endif
+}
+
+// pairs per batch of a call on t columns: the plan's batch (the large
+// single-stream batch for device calls that stay on the caller's stream),
+// capped at half the call's pairs (rounded up to the pair group) so that two
+// batches overlap
+static int64_t call_batch(const qmc_plan* pl, int64_t t, bool host) {
   const int64_t npairs = std::max<int64_t>(1, (t + 1) / 2);
-  int64_t b = pl->batch_pairs;
-  if (npairs >= 128 && !pl->batch_fixed) {  // small calls: one batch (launch-bound)
+  const bool one = !two_stream_mode(pl, host);
+  int64_t b = one ? pl->batch_pairs_1s : pl->batch_pairs;
+  if (npairs >= 128 && !pl->batch_fixed && !one) {  // small calls: one batch (launch-bound)
     const int64_t half = ((npairs + 1) / 2 + 15) / 16 * 16;
     b = std::min(b, half);
   }
@@ -1681,9 +1699,9 @@ static int64_t call_batch(const qmc_plan* pl, int64_t t) {
   return std::min(b, npairs);
 }
 
-static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
+static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f, bool host) {
   CallLayout c;
-  const int64_t pairs = call_batch(pl, t);
+  const int64_t pairs = call_batch(pl, t, host);
   size_t o = 0;
   auto take = [&](size_t b) {
     size_t r = o;
@@ -1692,7 +1710,7 @@ static CallLayout call_layout(const qmc_plan* pl, int64_t t, int f) {
   };
   // one scratch set (U, partial sums) per internal stream in use
   const int64_t nbatch = ((t + 1) / 2 + pairs - 1) / pairs;
-  c.nsets = (pl->nstreams == 2 && nbatch > 1) ? 2 : 1;
+  c.nsets = (two_stream_mode(pl, host) && nbatch > 1) ? 2 : 1;
   c.PG = pair_group(pairs);
   c.ngroups = int((pairs + c.PG - 1) / c.PG);
   // column-partial slots: the larger of the two K2 tilings (k_cols_x: CB
@@ -2118,10 +2136,10 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
     prof_end(KC_ROWS, st);
     return QMC_OK;
   }
-  const CallLayout cl = call_layout(pl, t, f);
+  const CallLayout cl = call_layout(pl, t, f, A_host != nullptr);
   if (call_ws_bytes < cl.total || (uintptr_t(call_ws) % kAlign)) return QMC_EWORKSPACE;
   char* ws = (char*)call_ws;
-  const int64_t pairs_b = call_batch(pl, t);
+  const int64_t pairs_b = call_batch(pl, t, A_host != nullptr);
   const int64_t npairs_total = (t + 1) / 2;
   EpiArgs E;
   E.fparam = f == QMC_F_AFFINE ? fparam : 0.0;
@@ -2132,18 +2150,11 @@ static int run(const qmc_plan* pl, const double* A, int64_t lda, int64_t t, int 
   E.N = pl->N;
   E.rowpart = (double*)(ws + cl.off_rowsum);
   std::unique_lock<std::mutex> lock;
-  // two internal streams where they overlap something: the per-batch host
-  // copies of qmc_mean_host, or the column pass of plans with L1 <= 16
-  // (measured on B200: c2 0.61 vs 0.68 ms, c3 24.2 vs 26.7, c4 2.37 vs 2.47;
-  // c5 (L1 = 96) 78.8 vs 79.0 ms — equal, so its device calls run on the
-  // caller's stream, where each kernel's event time is its own)
-  // green mode: K0/K1 of every batch on one SM partition, K2 on the other
+  // two internal streams where they overlap something (two_stream_mode; the
+  // layout holds two scratch sets exactly then); green mode: K0/K1 of every
+  // batch on one SM partition, K2 on the other
   const bool green = cl.nsets == 2 && pl->green;
-#ifdef QMC_DIAG_TWO_ALWAYS
-  const bool two = cl.nsets == 2 && pl->nstreams == 2;
-#else
-  const bool two = green || (cl.nsets == 2 && pl->nstreams == 2 && (A_host || pl->sp.L1 <= 16));
-#endif
+  const bool two = cl.nsets == 2;
   if (two) {  // fork: both internal streams start after the caller's prior work
     lock = std::unique_lock<std::mutex>(*pl->mu);
     if (cudaEventRecord(pl->ev_fork, st) != cudaSuccess ||
@@ -2221,7 +2232,8 @@ int qmc_call_workspace_size(qmc_plan_t pl, int64_t t, int f, size_t* call_bytes)
   if (!pl || !call_bytes) return QMC_ENULL;
   if (t < 0) return QMC_EINVAL_DIM;
   if (f < -1 || f > QMC_F_ROWMEAN_RELU) return QMC_EINVAL_F;
-  *call_bytes = call_layout(pl, t, f).total;
+  // the larger of the device-call and host-entry layouts (their batches differ)
+  *call_bytes = std::max(call_layout(pl, t, f, false).total, call_layout(pl, t, f, true).total);
   return QMC_OK;
 }
 

@@ -777,6 +777,18 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
     bp = std::min<int64_t>(bp, 4096);
     bp = bp >= 16 ? bp / 16 * 16 : bp >= 8 ? 8 : bp >= 4 ? 4 : bp;
     pl->batch_pairs = bp;
+    // Device calls of plans with L1 > 16 run on the caller's stream (one
+    // scratch set, nothing to overlap): the batch only sets how many K1/K2
+    // launches — each with a persistent grid's tail, its column-partial
+    // reduce and K0 — the call takes, so it is large: ~98304 K1 items per
+    // launch (~664 per SM), U at most ~16 GB (measured on B200, config 5:
+    // 64 pairs 72.0 ms, 1024 pairs 68.0 ms, 2048 pairs 67.8 ms per step)
+    {
+      int64_t b1 = std::max<int64_t>(bp, (98304 + sp.L1 - 1) / sp.L1);
+      b1 = std::max<int64_t>(1, std::min<int64_t>(b1, (int64_t(16) << 30) / per_pair));
+      b1 = std::min<int64_t>(b1, 4096);
+      pl->batch_pairs_1s = b1 >= 16 ? b1 / 16 * 16 : bp;
+    }
     if (const char* ev = getenv("QMC_K1_PER_SM")) pl->k1_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_K2_PER_SM")) pl->k2_per_sm = int(strtol(ev, nullptr, 10));  // tuning
     if (const char* ev = getenv("QMC_K1_GRID")) pl->k1_grid_cap = int(strtol(ev, nullptr, 10));     // tuning
@@ -784,6 +796,7 @@ static int create_common(qmc_plan_t* out, int family, int64_t N_or_D, uint64_t p
       const long v = strtol(ev, nullptr, 10);
       if (v > 0) {
         pl->batch_pairs = v;
+        pl->batch_pairs_1s = v;
         pl->batch_fixed = 1;
       }
     }
@@ -1088,7 +1101,7 @@ int qmc_plan_info(qmc_plan_t pl, int64_t* info) {
   info[6] = pl->sp.L;
   info[7] = pl->sp.L1;
   info[8] = pl->sp.L2;
-  info[9] = pl->batch_pairs;
+  info[9] = (pl->sp.L1 > 16 && !pl->green) ? pl->batch_pairs_1s : pl->batch_pairs;  // device calls' batch
   info[10] = pl->D;
   info[11] = int64_t(pl->p);
   info[12] = pl->k1_dense ? 2 : pl->k1_bal;

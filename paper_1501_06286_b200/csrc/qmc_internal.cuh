@@ -137,7 +137,8 @@ struct qmc_plan {
   uint64_t p;
   int64_t gen;
   qmc::Split sp;
-  int64_t batch_pairs;  // column pairs per batch (U sized to stay in L2)
+  int64_t batch_pairs;  // column pairs per batch of two-stream calls (one U set <= ~768 MB)
+  int64_t batch_pairs_1s;  // column pairs per batch of single-stream device calls (L1 > 16)
   int k1_per_sm;        // persistent K1 CTAs per SM (0: as many as fit)
   int k2_per_sm;        // persistent K2 CTAs per SM (0: as many as fit)
   int k1_grid_cap;      // QMC_K1_GRID: cap on K1's persistent grid (0: none; leaves SMs to the other stream)
