@@ -698,3 +698,44 @@ def test_green_partitions(qmc, monkeypatch, f):
     assert torch.equal(X0, X1) and torch.equal(m0, m1)
     rows = sample_rows(w.N, 64, seed=3)
     check_X(w, X1.index_select(0, torch.from_numpy(rows).cuda()).cpu().numpy(), X_rows(w, rows))
+
+
+def test_single_stream_batch_invariant(qmc, monkeypatch):
+    """Plans with L1 > 16 run device calls on the caller's stream in one large
+    batch (config 5: 1024 pairs); X is bitwise the same as with small batches
+    (every pair's K1/K2 arithmetic is independent of the batching), the exp
+    means agree to rounding, and the host entry (two streams, the two-stream
+    batch) gives bitwise the same X out of the same workspace."""
+    import torch
+    N, s, t = 786433, 64, 40
+    w = W.custom_lattice(N, s, t, W.PHI_INVNORM_MID, seed=7)
+    A = qmc.to_device_colmajor(w.A, "cuda")
+    res = {}
+    for bp in (None, "4"):
+        if bp:
+            monkeypatch.setenv("QMC_BATCH_PAIRS", bp)
+        plan = qmc.Plan.from_workload(w)
+        assert plan.info["L1"] > 16
+        X = qmc.x_empty(plan.N, t, "cuda")
+        m = plan.mean(A, W.F_EXP, 0.0, X=X)
+        torch.cuda.synchronize()
+        res[bp] = (X.clone(), m.clone(), plan)
+    monkeypatch.delenv("QMC_BATCH_PAIRS")
+    from paper_1501_06286_b200 import _abi as abi
+    (X1, m1, plan1), (X2, m2, _) = res[None], res["4"]
+    assert plan1.info["batch_pairs"] >= 1024
+    assert torch.equal(X1, X2)
+    torch.testing.assert_close(m1, m2, rtol=1e-14, atol=0)
+    # host entry on the large-batch plan: its own (two-stream) layout fits the
+    # workspace the size query returns
+    A_pin = torch.from_numpy(np.ascontiguousarray(w.A.T)).pin_memory()
+    A_dev = torch.empty(A_pin.shape, dtype=torch.float64, device="cuda")
+    Xh = qmc.x_empty(plan1.N, t, "cuda")
+    out_pin = torch.empty(t, dtype=torch.float64).pin_memory()
+    out_dev = torch.empty(max(plan1.N, t), dtype=torch.float64, device="cuda")
+    ws = plan1.call_workspace(t, W.F_EXP)
+    abi.qmc_mean_host(plan1.handle, A_pin, s, t, W.F_EXP, 0.0, out_pin, A_dev, Xh, t, out_dev, ws,
+                      ws.numel(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(X1, Xh)
+    torch.testing.assert_close(out_pin.to("cuda"), m1, rtol=1e-14, atol=0)
