@@ -113,10 +113,15 @@ PlanLayout plan_layout(int64_t N, int64_t m, int64_t s, const Split& sp);
 // K2 column-pass splits L1 = R·M (pipeline.cu k_cols_x): R = 1 is one thread
 // per column with L1 values in registers; R > 1 is two register stages
 // through shared memory.  X(R, M) for every supported L1.
+// (QMC_K2_R96: R of config 5's L1 = 96 — 6·16 by default; 8·12 and 12·8
+// are build knobs for the stage balance of k_cols_pipe2)
+#ifndef QMC_K2_R96
+#define QMC_K2_R96 6
+#endif
 #define QMC_K2_SPLITS(X)                                                                       \
   X(1, 1) X(1, 2) X(1, 3) X(1, 4) X(1, 5) X(1, 6) X(1, 8) X(1, 9) X(1, 10) X(1, 12) X(1, 15)   \
-  X(1, 16) X(2, 10) X(2, 12) X(5, 5) X(2, 16) X(4, 10) X(3, 16) X(4, 16) X(5, 16) X(6, 16)       \
-  X(8, 16) X(10, 16) X(12, 16) X(16, 16)
+  X(1, 16) X(2, 10) X(2, 12) X(5, 5) X(2, 16) X(4, 10) X(3, 16) X(4, 16) X(5, 16)               \
+  X(QMC_K2_R96, (96 / QMC_K2_R96)) X(8, 16) X(10, 16) X(12, 16) X(16, 16)
 // R of the K2 split of L1 (0: L1 not supported)
 inline int k2_split_R(int64_t L1) {
 #define QMC_K2_R(RR, MM) \
