@@ -1471,13 +1471,25 @@ __global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
 // ω_{L1}^{r k2}, written back in place (position r + R·k2).  Stage B, item
 // (p, c, k2): R-point inverse DFT over r → rows e1 = k2 + M·k1, stored as
 // 8-pair row chunks (128 B) of X.  Same arithmetic as k_cols_x<R, M>.
-constexpr int kP2PG = 8;    // pairs per tile
-constexpr int kP2Thr = 256;
+// Pairs per tile: 16 (512 threads, 256-byte row chunks of X, one CTA per SM)
+// where L1 >= 80 and two stages of 16 pairs fit in shared memory — config 5's
+// L1 = 96: K2 20.95 -> 19.41 ms against 8-pair tiles at two CTAs per SM —
+// else 8 (256 threads).  QMC_P2PG forces one value (diagnostic).
+template <int L1>
+__host__ __device__ constexpr int p2pg() {
+#ifdef QMC_P2PG
+  return QMC_P2PG;
+#else
+  return (L1 >= 80 && 2 * (size_t(16) * (L1 * kUB + 1) * 16 + size_t(L1) * kUB * 4) <= 232448) ? 16 : 8;
+#endif
+}
+template <int L1>
+__host__ __device__ constexpr int p2thr() { return 32 * p2pg<L1>(); }
 template <int L1>
 __host__ __device__ constexpr int pipe2_pair_stride() { return L1 * kUB + 1; }  // odd, 16-B units
 template <int L1>
 __host__ __device__ constexpr size_t cols_pipe2_smem() {
-  return size_t(kPipeStages) * (size_t(kP2PG) * pipe2_pair_stride<L1>() * 16 + size_t(L1) * kUB * 4);
+  return size_t(kPipeStages) * (size_t(p2pg<L1>()) * pipe2_pair_stride<L1>() * 16 + size_t(L1) * kUB * 4);
 }
 
 // stage tile `tile` into dst (pair pitch PSTR) and its output rows into nd
@@ -1489,17 +1501,18 @@ __device__ __forceinline__ void k2p2_issue(const K2Args& a, int tile, double2* d
   constexpr unsigned UB = BLK * 16, NB4 = L1 * kUB * 4;
   const int bx = tile % a.ntx, g = tile / a.ntx;
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the buffer's reads before the async writes
-  mbar_expect_tx(bar, kP2PG * UB + NB4);
+  constexpr int PG = p2pg<L1>();
+  mbar_expect_tx(bar, PG * UB + NB4);
 #pragma unroll
-  for (int pp = 0; pp < kP2PG; ++pp)
-    bulk_g2s(dst + pp * PSTR, a.U + int64_t(g * kP2PG + pp) * a.L + int64_t(bx) * BLK, UB, bar);
+  for (int pp = 0; pp < PG; ++pp)
+    bulk_g2s(dst + pp * PSTR, a.U + int64_t(g * PG + pp) * a.L + int64_t(bx) * BLK, UB, bar);
   bulk_g2s(nd, a.k2n + int64_t(bx) * (L1 * kUB), NB4, bar);
 }
 
 template <int R, int M, int EP, bool PAD>
 __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T, const int* nS, double2& acc,
                                           const double2* tw1) {
-  constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = kP2PG;
+  constexpr int L1 = R * M, PSTR = pipe2_pair_stride<L1>(), PG = p2pg<L1>(), kP2Thr = p2thr<L1>();
   const EpiArgs& E = a.E;
   const int tid = threadIdx.x, warp = tid >> 5;
   const int p = tid % PG;
@@ -1552,8 +1565,9 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
 // visits each pair group in one run of consecutive tiles (tile = blockIdx.x
 // + k·gridDim.x, g = tile / ntx nondecreasing), so the slot row of every
 // group it visits is written once and the rest stays zero
+template <int PG>
 __device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc, double2 (*red)[16]) {
-  constexpr int PG = kP2PG;
+  constexpr int kP2Thr = 32 * PG;
   const int tid = threadIdx.x, warp = tid >> 5;
 #pragma unroll
   for (int o = PG; o < 32; o <<= 1) {
@@ -1574,8 +1588,8 @@ __device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc,
 }
 
 template <int R, int M, int EP, bool PAD>
-__global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
-  constexpr int L1 = R * M;
+__global__ void __launch_bounds__(p2thr<R * M>(), p2thr<R * M>() >= 512 ? 1 : 2) k_cols_pipe2(K2Args a, int lg2L2) {
+  constexpr int L1 = R * M, kP2PG = p2pg<L1>(), kP2Thr = p2thr<L1>();
   constexpr int STAGE = kP2PG * pipe2_pair_stride<L1>();
   extern __shared__ double2 sm[];
   int* nS = reinterpret_cast<int*>(sm + kPipeStages * STAGE);  // [stage][e1][c]
@@ -1603,7 +1617,7 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
     __syncthreads();
     const int g = tile / a.ntx;
     if (a.part && g != gcur) {
-      k2p2_flush(a, gcur, acc, red);
+      k2p2_flush<kP2PG>(a, gcur, acc, red);
       gcur = g;
     }
     const int ahead = tile + gridDim.x;
@@ -1611,7 +1625,7 @@ __global__ void __launch_bounds__(kP2Thr, 2) k_cols_pipe2(K2Args a, int lg2L2) {
       k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB), &bars[st ^ 1]);
     k2p2_tile<R, M, EP, PAD>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
   }
-  if (a.part && int(blockIdx.x) < ntiles) k2p2_flush(a, gcur, acc, red);
+  if (a.part && int(blockIdx.x) < ntiles) k2p2_flush<kP2PG>(a, gcur, acc, red);
 }
 
 // out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
@@ -1899,6 +1913,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
   if constexpr (R > 1 && EP != EPK_ROWSUM && cols_pipe2_smem<R * M>() <= 232448) {
     // two-stage column pass, pipelined: whole 8-pair groups, whole pairs,
     // vector X stores, whole U column blocks
+    constexpr int kP2PG = p2pg<L1>(), kP2Thr = p2thr<L1>();
     if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !pl->k2_nopipe) {
       constexpr size_t psm = cols_pipe2_smem<L1>();
       // zero-padded lengths (L > m) skip the rows i >= m; exact lengths need no test
