@@ -1463,14 +1463,14 @@ __global__ void __launch_bounds__(16 * CB, QMC_K2_MINB) k_cols_pipe(K2Args a) {
 }
 
 // Persistent, software-pipelined two-stage K2 (L1 = R·M, R > 1; config 5:
-// 96 = 6·16): tile = (8 pairs, one U column block of kUB = 4 columns e2),
-// i.e. 8 contiguous runs of L1·kUB complex, staged one tile ahead with its
+// 96 = 6·16): tile = (PG pairs, one U column block of kUB = 4 columns e2),
+// i.e. PG contiguous runs of L1·kUB complex, staged one tile ahead with its
 // output row indices (the plan's k2n run) by bulk async copies (one thread,
 // an mbarrier per stage).  Stage A, item (p, c, r): the M values
 // f1 = r + R·mm times conj(ω_L^{e2 f1}), M-point inverse DFT, times
 // ω_{L1}^{r k2}, written back in place (position r + R·k2).  Stage B, item
 // (p, c, k2): R-point inverse DFT over r → rows e1 = k2 + M·k1, stored as
-// 8-pair row chunks (128 B) of X.  Same arithmetic as k_cols_x<R, M>.
+// PG-pair row chunks (16·PG bytes) of X.  Same arithmetic as k_cols_x<R, M>.
 // Pairs per tile: 16 (512 threads, 256-byte row chunks of X, one CTA per SM)
 // where L1 >= 80 and two stages of 16 pairs fit in shared memory — config 5's
 // L1 = 96: K2 20.95 -> 19.41 ms against 8-pair tiles at two CTAs per SM —
@@ -1542,8 +1542,8 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
     for (int k2 = 0; k2 < M; ++k2) Tp[(r + R * k2) * kUB] = x[k2];
   }
   __syncthreads();
-  // stage B: items (p, c, k2), it = p + PG·(c + kUB·k2); a warp = 8 pairs × 4
-  // columns of one k2, so each output row gets one 128-byte chunk
+  // stage B: items (p, c, k2), it = p + PG·(c + kUB·k2); a warp = PG pairs ×
+  // 32/PG columns of one k2, so each output row gets one 16·PG-byte chunk
   for (int it = tid; it < PG * kUB * M; it += kP2Thr) {
     const int c = (it / PG) % kUB, k2 = it / (PG * kUB);
     const double2* Tp = T + p * PSTR + c;
@@ -1911,7 +1911,7 @@ static int launch_cols_ep(const qmc_plan* pl, const CallLayout& cl, const double
     }
   }
   if constexpr (R > 1 && EP != EPK_ROWSUM && cols_pipe2_smem<R * M>() <= 232448) {
-    // two-stage column pass, pipelined: whole 8-pair groups, whole pairs,
+    // two-stage column pass, pipelined: whole PG-pair groups, whole pairs,
     // vector X stores, whole U column blocks
     constexpr int kP2PG = p2pg<L1>(), kP2Thr = p2thr<L1>();
     if (np % kP2PG == 0 && E.t % 2 == 0 && (!E.X || E.xvec) && pl->sp.L2 % kUB == 0 && !pl->k2_nopipe) {

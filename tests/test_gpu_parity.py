@@ -276,6 +276,9 @@ def test_config5_sampled(qmc):
 # N = 65539 (L = 163840 = 20·8192, L1 = 2·10).
 MEAN_CASES = [(65537, 64, 32, None), (65537, 64, 30, None), (40961, 50, 32, None), (65537, 40, 64, 16),
               (786433, 16, 6, None), (786433, 16, 32, None), (3079, 50, 32, None), (65539, 40, 32, None),
+              # L1 = 96 takes 16-pair tiles: two whole groups (t = 64), and 24 pairs (t = 48: not whole
+              # 16-pair groups, the general column pass)
+              (786433, 16, 64, None), (786433, 16, 48, None),
               # one-row plans (the fused k_small): rows of 256 with s > m and odd t; rows of 32 (2 threads)
               (257, 300, 7, None), (13, 5, 4, None)]
 
