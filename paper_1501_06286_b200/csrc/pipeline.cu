@@ -1484,7 +1484,13 @@ __host__ __device__ constexpr int p2pg() {
 #endif
 }
 template <int L1>
-__host__ __device__ constexpr int p2thr() { return 32 * p2pg<L1>(); }
+__host__ __device__ constexpr int p2thr() {
+#ifdef QMC_P2THR
+  return QMC_P2THR;  // diagnostic (a multiple of 32)
+#else
+  return 32 * p2pg<L1>();
+#endif
+}
 template <int L1>
 __host__ __device__ constexpr int pipe2_pair_stride() { return L1 * kUB + 1; }  // odd, 16-B units
 template <int L1>
@@ -1565,9 +1571,8 @@ __device__ __forceinline__ void k2p2_tile(const K2Args& a, int tile, double2* T,
 // visits each pair group in one run of consecutive tiles (tile = blockIdx.x
 // + k·gridDim.x, g = tile / ntx nondecreasing), so the slot row of every
 // group it visits is written once and the rest stays zero
-template <int PG>
+template <int PG, int kP2Thr>
 __device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc, double2 (*red)[16]) {
-  constexpr int kP2Thr = 32 * PG;
   const int tid = threadIdx.x, warp = tid >> 5;
 #pragma unroll
   for (int o = PG; o < 32; o <<= 1) {
@@ -1588,7 +1593,7 @@ __device__ __forceinline__ void k2p2_flush(const K2Args& a, int g, double2& acc,
 }
 
 template <int R, int M, int EP, bool PAD>
-__global__ void __launch_bounds__(p2thr<R * M>(), p2thr<R * M>() >= 512 ? 1 : 2) k_cols_pipe2(K2Args a, int lg2L2) {
+__global__ void __launch_bounds__(p2thr<R * M>(), p2thr<R * M>() > 256 ? 1 : 2) k_cols_pipe2(K2Args a, int lg2L2) {
   constexpr int L1 = R * M, kP2PG = p2pg<L1>(), kP2Thr = p2thr<L1>();
   constexpr int STAGE = kP2PG * pipe2_pair_stride<L1>();
   extern __shared__ double2 sm[];
@@ -1617,7 +1622,7 @@ __global__ void __launch_bounds__(p2thr<R * M>(), p2thr<R * M>() >= 512 ? 1 : 2)
     __syncthreads();
     const int g = tile / a.ntx;
     if (a.part && g != gcur) {
-      k2p2_flush<kP2PG>(a, gcur, acc, red);
+      k2p2_flush<kP2PG, kP2Thr>(a, gcur, acc, red);
       gcur = g;
     }
     const int ahead = tile + gridDim.x;
@@ -1625,7 +1630,7 @@ __global__ void __launch_bounds__(p2thr<R * M>(), p2thr<R * M>() >= 512 ? 1 : 2)
       k2p2_issue<L1>(a, ahead, sm + (st ^ 1) * STAGE, nS + (st ^ 1) * (L1 * kUB), &bars[st ^ 1]);
     k2p2_tile<R, M, EP, PAD>(a, tile, sm + st * STAGE, nS + st * (L1 * kUB), acc, tw1s);
   }
-  if (a.part && int(blockIdx.x) < ntiles) k2p2_flush<kP2PG>(a, gcur, acc, red);
+  if (a.part && int(blockIdx.x) < ntiles) k2p2_flush<kP2PG, kP2Thr>(a, gcur, acc, red);
 }
 
 // out[k] = (1/N) Σ_bx part[bx][kk], k = 2·pair0 + kk: one warp per column,
